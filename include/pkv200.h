@@ -1,0 +1,239 @@
+/*
+ * pkv200 — C ABI of the B200-native paged-attention engine.
+ *
+ * This is the drop-in boundary for the hot path of the reference `pagedkv`
+ * package (arXiv 2506.07311).  The reference is pure Python, so it has no FFI
+ * of its own; every entry point below replaces one reference *Python* function
+ * and is bound from Python with ctypes (INTEGRATION.md shows the binding).
+ * Conventions:
+ *   - every function returns a status code (PKV_OK == 0); the message of the
+ *     last failure on the calling thread is available from pkv_last_error();
+ *   - status codes map 1:1 onto the reference's exception classes
+ *     (reference errors.py:4-41) plus Python's ValueError/IndexError where
+ *     the reference raises those;
+ *   - device entry points take device pointers, launch on the caller's
+ *     cudaStream_t (passed as void*), never allocate and never synchronise;
+ *   - the engine never owns device memory: caches, block-table mirror,
+ *     workspaces and outputs belong to the caller (torch, in the Python shim).
+ */
+#ifndef PKV200_H
+#define PKV200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ---- status codes ------------------------------------------------------ */
+enum pkv_status {
+  PKV_OK = 0,
+  PKV_CAPACITY_EXHAUSTED = 1, /* errors.py:8  CapacityExhausted */
+  PKV_DUPLICATE_SEQUENCE = 2, /* errors.py:12 DuplicateSequence */
+  PKV_UNKNOWN_SEQUENCE = 3,   /* errors.py:16 UnknownSequence   */
+  PKV_INVALID_PREFIX = 4,     /* errors.py:20 InvalidPrefix     */
+  PKV_OUT_OF_RANGE = 5,       /* errors.py:24 OutOfRange        */
+  PKV_SHAPE_MISMATCH = 6,     /* errors.py:28 ShapeMismatch     */
+  PKV_NO_ALLOWED_KEYS = 7,    /* errors.py:32 NoAllowedKeys     */
+  PKV_VALUE_ERROR = 8,        /* Python ValueError (pool.py:97-102, 161, 212) */
+  PKV_INDEX_ERROR = 9,        /* Python IndexError (array index in pool.py:248) */
+  PKV_CONFIG_ERROR = 10,      /* errors.py:40 ConfigError (unsupported shape) */
+  PKV_CUDA_ERROR = 11         /* launch / device failure */
+};
+
+/* element types of caches, queries and outputs */
+enum pkv_dtype { PKV_F32 = 0, PKV_F16 = 1, PKV_BF16 = 2 };
+
+const char* pkv_last_error(void);
+int pkv_abi_version(void);
+
+/* ======================================================================
+ * Page allocator — host control plane (replaces reference pool.py:88-349).
+ * Bit-exact with the reference's PagePool.dump() state contract
+ * (pool.py:309-329), including failed-grant free-stack reordering
+ * (pool.py:143-148) and the clamped bump cursor (pool.py:286-290).
+ * Internally synchronised (one mutex per pool): reserve/grow/free/fork may be
+ * called from many threads as the reference contract allows (pool.py:91-94).
+ * Sequences are caller-chosen int64 handles (the Python shim maps arbitrary
+ * hashable ids onto handles).  Granted pages are returned to the caller, who
+ * must clear them in every attached store (clear-on-grant, pool.py:122-126)
+ * and perform the reported page copies (pool.py:112-120).
+ * ==================================================================== */
+typedef struct pkv_pool pkv_pool;
+
+/* PagePool.__init__            pool.py:96-110 */
+int pkv_pool_create(uint64_t capacity_pages, uint32_t page_size, pkv_pool** out);
+void pkv_pool_destroy(pkv_pool* pool);
+
+/* PagePool.reserve             pool.py:154-174; pages_out must hold
+ * pages_for(length) entries; *n_out receives the grant size */
+int pkv_pool_reserve(pkv_pool* pool, int64_t seq, int64_t length, uint32_t* pages_out,
+                     int64_t* n_out);
+/* PagePool.grow                pool.py:176-187 */
+int pkv_pool_grow(pkv_pool* pool, int64_t seq, int64_t new_len, uint32_t* pages_out,
+                  int64_t* n_out);
+/* PagePool.free                pool.py:189-199 */
+int pkv_pool_free(pkv_pool* pool, int64_t seq, int64_t* reclaimed_out);
+/* PagePool.fork                pool.py:201-236; copy_* report the partial-page
+ * copy (copy_dst == -1 when the prefix is page aligned) */
+int pkv_pool_fork(pkv_pool* pool, int64_t parent, int64_t child, int64_t prefix_len,
+                  int64_t* copy_src, int64_t* copy_dst, int64_t* copy_rows);
+/* PagePool.privatize           pool.py:238-254; *new_page == -1 when the page
+ * was already private; otherwise copy the full page old -> new */
+int pkv_pool_privatize(pkv_pool* pool, int64_t seq, int64_t block_idx, int64_t* old_page,
+                       int64_t* new_page);
+/* PagePool.translate           pool.py:258-266 */
+int pkv_pool_translate(pkv_pool* pool, int64_t seq, int64_t position, uint32_t* page_out,
+                       uint32_t* offset_out);
+
+/* BlockTable access            pool.py:50-71 */
+int pkv_pool_has_sequence(pkv_pool* pool, int64_t seq, int32_t* out);
+int pkv_pool_table_len(pkv_pool* pool, int64_t seq, int64_t* n_out);
+int pkv_pool_table_entries(pkv_pool* pool, int64_t seq, uint32_t* out, int64_t cap);
+int pkv_pool_table_set_entry(pkv_pool* pool, int64_t seq, int64_t idx, uint32_t value);
+int pkv_pool_get_logical_len(pkv_pool* pool, int64_t seq, int64_t* out);
+int pkv_pool_set_logical_len(pkv_pool* pool, int64_t seq, int64_t value);
+/* sequences in insertion order (dict order of pool.py:109) */
+int pkv_pool_sequence_count(pkv_pool* pool, int64_t* n_out);
+int pkv_pool_sequences(pkv_pool* pool, int64_t* out, int64_t cap);
+
+/* introspection                pool.py:272-307 */
+int pkv_pool_refcount(pkv_pool* pool, uint64_t page, int64_t* out);
+/* out[0..4] = capacity, live, free, never_allocated, bump_cursor */
+int pkv_pool_census(pkv_pool* pool, int64_t* out5);
+int pkv_pool_free_stack(pkv_pool* pool, uint32_t* out, int64_t cap, int64_t* n_out);
+
+/* Batched decode-step planning (new; the engine's batched step API):
+ * for each of n sequences append one token at position logical_len — grow the
+ * table to logical_len+1 (pool.py:176-187), privatize the written block
+ * (store.py:143-145) and advance logical_len (store.py:150).  All-or-nothing:
+ * if the pool cannot supply every page the call fails with
+ * PKV_CAPACITY_EXHAUSTED before mutating anything.  Outputs: positions_out[n],
+ * rows_out[n] (mirror rows), granted pages (caller zeroes them in every store)
+ * and copies_out[2n] (old,new page pairs or -1,-1; caller copies full pages). */
+int pkv_pool_prepare_append(pkv_pool* pool, const int64_t* seqs, int64_t n, int32_t* positions_out,
+                            int32_t* rows_out, uint32_t* pages_out, int64_t pages_cap,
+                            int64_t* n_pages_out, int64_t* copies_out);
+
+/* ---- device block-table mirror (new; SURVEY.md §7 decision 3) -----------
+ * Each live table owns one row of an int32 [rows, cols] device matrix.  The
+ * pool records which entries changed; the caller drains them and applies them
+ * on the device with pkv_mirror_apply (or re-uploads the whole matrix after a
+ * shape change, signalled by *full_resync). */
+int pkv_pool_mirror_row(pkv_pool* pool, int64_t seq, int32_t* row_out);
+int pkv_pool_mirror_shape(pkv_pool* pool, int64_t* rows_out, int64_t* cols_out);
+/* pairs_out holds (flat_index, value) int32 pairs; at most cap pairs */
+int pkv_pool_mirror_drain(pkv_pool* pool, int32_t* pairs_out, int64_t cap, int64_t* n_out,
+                          int32_t* full_resync);
+int pkv_pool_mirror_pending(pkv_pool* pool, int64_t* n_out, int32_t* full_resync);
+/* copy the whole host mirror (rows*cols int32) and clear the dirty state */
+int pkv_pool_mirror_export(pkv_pool* pool, int32_t* out, int64_t rows, int64_t cols);
+
+/* ======================================================================
+ * Device data plane (sm_100a kernels).
+ * ==================================================================== */
+
+/* apply drained mirror pairs: table[pairs[2i]] = pairs[2i+1] */
+int pkv_mirror_apply(int32_t* table, const int32_t* pairs, int64_t n_pairs, void* stream);
+
+/* K0a  KvStore.clear_pages      store.py:95-100: zero `n` whole pages of the
+ * K and V caches (page_bytes = page_size * heads * head_dim * elem_size) */
+int pkv_page_zero(void* k_cache, void* v_cache, const int32_t* pages, int64_t n,
+                  int64_t page_bytes, void* stream);
+
+/* K0b  KvStore.copy_rows        store.py:85-93: for each (src, dst, rows)
+ * triple copy the first `rows` rows of page src into page dst and zero the
+ * rest of dst */
+int pkv_page_copy(void* k_cache, void* v_cache, const int32_t* triples, int64_t n,
+                  int64_t row_bytes, int32_t page_size, void* stream);
+
+/* K1   KvStore.assign scatter   store.py:146-150 (reshape-and-cache):
+ * cache[row(tok_row[i*row_stride], tok_pos[i])] = new[i] for K and V, where
+ * row(r, p) = table[r*bt_stride + p/ps]*ps + p%ps.  Positions must be unique
+ * (the shim keeps the last occurrence, reproducing numpy last-write-wins). */
+int pkv_kv_append(const void* k_new, const void* v_new, int64_t n_tok, const int32_t* tok_row,
+                  int32_t tok_row_stride, const int32_t* tok_pos, const int32_t* block_table,
+                  int64_t bt_stride, int32_t page_size, void* k_cache, void* v_cache,
+                  int64_t row_bytes, void* stream);
+
+/* K2   paged_attention          attention.py:259-354 — split-K flash decode
+ * over the block table with an online softmax, plus the K2c combine.
+ * Query i belongs to view sequence q_seq[i] and attends keys 0..q_nkeys[i]-1
+ * of that sequence (causal: q_pos+1, otherwise the sequence length; the
+ * reference mask predicate attention.py:113-134 reduces to this prefix).
+ * Paged mode: block_table != NULL, seq_row[s] = mirror row of view sequence s.
+ * Gathered mode (gathered_attention, attention.py:357-378): block_table ==
+ * NULL and seq_start[s] = first row of sequence s in contiguous K/V.
+ * Query heads: hq = G * hkv; q head h reads kv head h / G.
+ * Output: [n_queries, hq, head_dim] in out_dtype. */
+typedef struct pkv_attention_args {
+  const void* q;          /* [n_queries, hq, head_dim] */
+  int32_t q_dtype;
+  int64_t n_queries;
+  const int32_t* q_seq;   /* [n_queries] view sequence of each query */
+  const int32_t* q_nkeys; /* [n_queries] allowed key prefix of each query */
+  const void* k_cache;    /* [rows, hkv, head_dim] */
+  const void* v_cache;
+  int32_t kv_dtype;
+  const int32_t* block_table; /* paged mode: device mirror, NULL = gathered */
+  int64_t bt_stride;
+  const int32_t* seq_row;     /* paged mode: [n_seqs] */
+  const int64_t* seq_start;   /* gathered mode: [n_seqs] */
+  int32_t page_size;
+  int32_t hq;
+  int32_t hkv;
+  int32_t head_dim;
+  float scale;
+  void* out;
+  int32_t out_dtype;
+  void* workspace; /* pkv_attention_workspace_bytes() bytes, 256-B aligned */
+  int64_t workspace_bytes;
+  int32_t num_sms;  /* 0 = query the device */
+  int32_t target_waves; /* 0 = default work-splitting heuristic */
+  void* prof_start; /* optional cudaEvent_t recorded right before the K2 launch */
+  void* prof_stop;  /* optional cudaEvent_t recorded right after the K2 launch */
+} pkv_attention_args;
+
+/* Workspace bound: the split planner never creates more than
+ * n_queries + 8192 key splits, so the bound depends only on the query count. */
+int64_t pkv_attention_workspace_bytes(int64_t n_queries, int32_t hq, int32_t head_dim);
+int pkv_paged_attention(const pkv_attention_args* args, void* stream);
+
+/* K3   causal / suffix prefill on tcgen05 tensor cores (bf16 only).
+ * Queries of sequence s are the q_len[s] consecutive positions ending at
+ * seq_len[s]-1 (MaskMeta.suffix / self_attention, attention.py:81-110),
+ * stored contiguously from q_start[s]. */
+typedef struct pkv_prefill_args {
+  const void* q;             /* [total_q, hq, head_dim] bf16 */
+  int32_t n_seqs;
+  const int32_t* q_start;    /* [n_seqs] */
+  const int32_t* q_len;      /* [n_seqs] */
+  const int32_t* seq_len;    /* [n_seqs] keys of each sequence */
+  const int32_t* seq_row;    /* [n_seqs] mirror rows */
+  const void* k_cache;       /* bf16 [rows, hkv, head_dim] */
+  const void* v_cache;
+  const int32_t* block_table;
+  int64_t bt_stride;
+  int32_t page_size;
+  int32_t hq;
+  int32_t hkv;
+  int32_t head_dim;
+  float scale;
+  int32_t causal;
+  void* out;                 /* [total_q, hq, head_dim] */
+  int32_t out_dtype;
+  int32_t max_q_len;
+} pkv_prefill_args;
+
+int pkv_prefill_supported(int32_t hq, int32_t hkv, int32_t head_dim, int32_t page_size,
+                          int32_t kv_dtype);
+int pkv_paged_prefill(const pkv_prefill_args* args, void* stream);
+
+/* number of SMs of the current device (0 when no device is visible) */
+int pkv_device_sm_count(int32_t* out);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* PKV200_H */

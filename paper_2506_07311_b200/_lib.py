@@ -1,0 +1,133 @@
+"""ctypes binding of libpkv200.so (the C ABI of include/pkv200.h).
+
+This is the reference-side binding a Python caller adds: it
+loads the in-tree library, declares every entry point and turns non-zero
+status codes into the reference's exception classes.  There is no fallback —
+a missing library raises immediately.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+from . import errors
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libpkv200.so")
+
+PKV_F32, PKV_F16, PKV_BF16 = 0, 1, 2
+
+_STATUS = {
+    1: errors.CapacityExhausted,
+    2: errors.DuplicateSequence,
+    3: errors.UnknownSequence,
+    4: errors.InvalidPrefix,
+    5: errors.OutOfRange,
+    6: errors.ShapeMismatch,
+    7: errors.NoAllowedKeys,
+    8: ValueError,
+    9: IndexError,
+    10: errors.ConfigError,
+    11: errors.DeviceError,
+}
+
+_i32, _i64, _u32, _u64, _f32, _vp = C.c_int32, C.c_int64, C.c_uint32, C.c_uint64, C.c_float, C.c_void_p
+_P = C.POINTER
+
+
+class AttentionArgs(C.Structure):
+    _fields_ = [
+        ("q", _vp), ("q_dtype", _i32), ("n_queries", _i64),
+        ("q_seq", _vp), ("q_nkeys", _vp),
+        ("k_cache", _vp), ("v_cache", _vp), ("kv_dtype", _i32),
+        ("block_table", _vp), ("bt_stride", _i64), ("seq_row", _vp), ("seq_start", _vp),
+        ("page_size", _i32), ("hq", _i32), ("hkv", _i32), ("head_dim", _i32),
+        ("scale", _f32), ("out", _vp), ("out_dtype", _i32),
+        ("workspace", _vp), ("workspace_bytes", _i64),
+        ("num_sms", _i32), ("target_waves", _i32),
+        ("prof_start", _vp), ("prof_stop", _vp),
+    ]
+
+
+class PrefillArgs(C.Structure):
+    _fields_ = [
+        ("q", _vp), ("n_seqs", _i32), ("q_start", _vp), ("q_len", _vp), ("seq_len", _vp),
+        ("seq_row", _vp), ("k_cache", _vp), ("v_cache", _vp), ("block_table", _vp),
+        ("bt_stride", _i64), ("page_size", _i32), ("hq", _i32), ("hkv", _i32), ("head_dim", _i32),
+        ("scale", _f32), ("causal", _i32), ("out", _vp), ("out_dtype", _i32), ("max_q_len", _i32),
+    ]
+
+
+# name -> (restype, argtypes); every symbol the header declares
+SIGNATURES = {
+    "pkv_last_error": (C.c_char_p, []),
+    "pkv_abi_version": (C.c_int, []),
+    "pkv_pool_create": (C.c_int, [_u64, _u32, _P(_vp)]),
+    "pkv_pool_destroy": (None, [_vp]),
+    "pkv_pool_reserve": (C.c_int, [_vp, _i64, _i64, _P(_u32), _P(_i64)]),
+    "pkv_pool_grow": (C.c_int, [_vp, _i64, _i64, _P(_u32), _P(_i64)]),
+    "pkv_pool_free": (C.c_int, [_vp, _i64, _P(_i64)]),
+    "pkv_pool_fork": (C.c_int, [_vp, _i64, _i64, _i64, _P(_i64), _P(_i64), _P(_i64)]),
+    "pkv_pool_privatize": (C.c_int, [_vp, _i64, _i64, _P(_i64), _P(_i64)]),
+    "pkv_pool_prepare_append": (C.c_int, [_vp, _P(_i64), _i64, _P(_i32), _P(_i32), _P(_u32), _i64,
+                                          _P(_i64), _P(_i64)]),
+    "pkv_pool_translate": (C.c_int, [_vp, _i64, _i64, _P(_u32), _P(_u32)]),
+    "pkv_pool_has_sequence": (C.c_int, [_vp, _i64, _P(_i32)]),
+    "pkv_pool_table_len": (C.c_int, [_vp, _i64, _P(_i64)]),
+    "pkv_pool_table_entries": (C.c_int, [_vp, _i64, _P(_u32), _i64]),
+    "pkv_pool_table_set_entry": (C.c_int, [_vp, _i64, _i64, _u32]),
+    "pkv_pool_get_logical_len": (C.c_int, [_vp, _i64, _P(_i64)]),
+    "pkv_pool_set_logical_len": (C.c_int, [_vp, _i64, _i64]),
+    "pkv_pool_sequence_count": (C.c_int, [_vp, _P(_i64)]),
+    "pkv_pool_sequences": (C.c_int, [_vp, _P(_i64), _i64]),
+    "pkv_pool_refcount": (C.c_int, [_vp, _u64, _P(_i64)]),
+    "pkv_pool_census": (C.c_int, [_vp, _P(_i64)]),
+    "pkv_pool_free_stack": (C.c_int, [_vp, _P(_u32), _i64, _P(_i64)]),
+    "pkv_pool_mirror_row": (C.c_int, [_vp, _i64, _P(_i32)]),
+    "pkv_pool_mirror_shape": (C.c_int, [_vp, _P(_i64), _P(_i64)]),
+    "pkv_pool_mirror_drain": (C.c_int, [_vp, _P(_i32), _i64, _P(_i64), _P(_i32)]),
+    "pkv_pool_mirror_pending": (C.c_int, [_vp, _P(_i64), _P(_i32)]),
+    "pkv_pool_mirror_export": (C.c_int, [_vp, _P(_i32), _i64, _i64]),
+    "pkv_mirror_apply": (C.c_int, [_vp, _vp, _i64, _vp]),
+    "pkv_page_zero": (C.c_int, [_vp, _vp, _vp, _i64, _i64, _vp]),
+    "pkv_page_copy": (C.c_int, [_vp, _vp, _vp, _i64, _i64, _i32, _vp]),
+    "pkv_kv_append": (C.c_int, [_vp, _vp, _i64, _vp, _i32, _vp, _vp, _i64, _i32, _vp, _vp, _i64, _vp]),
+    "pkv_attention_workspace_bytes": (_i64, [_i64, _i32, _i32]),
+    "pkv_paged_attention": (C.c_int, [_P(AttentionArgs), _vp]),
+    "pkv_prefill_supported": (C.c_int, [_i32, _i32, _i32, _i32, _i32]),
+    "pkv_paged_prefill": (C.c_int, [_P(PrefillArgs), _vp]),
+    "pkv_device_sm_count": (C.c_int, [_P(_i32)]),
+}
+
+_lib = None
+
+
+def load() -> C.CDLL:
+    """Load libpkv200.so once; raise loudly if it was not built."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise errors.DeviceError(
+            f"{LIB_PATH} is missing: build it with `python -m paper_2506_07311_b200.build` "
+            "(there is no CPU fallback)")
+    lib = C.CDLL(LIB_PATH)
+    for name, (res, args) in SIGNATURES.items():
+        fn = getattr(lib, name)
+        fn.restype = res
+        fn.argtypes = args
+    _lib = lib
+    return lib
+
+
+def check(status: int, what: str = "") -> None:
+    if status == 0:
+        return
+    msg = load().pkv_last_error().decode(errors="replace")
+    exc = _STATUS.get(status, errors.DeviceError)
+    raise exc(f"{what}: {msg}" if what and exc is errors.DeviceError else msg)
+
+
+def call(name: str, *args) -> None:
+    check(getattr(load(), name)(*args), name)

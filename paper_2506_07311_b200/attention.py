@@ -1,0 +1,332 @@
+"""Attention entry points — drop-in for reference attention.py:26-378.
+
+`paged_attention(queries, store, meta, config)` keeps the reference signature
+(attention.py:332-354) and runs on the device:
+
+* decode-shaped and general metas -> K2 split-K flash decode + K2c combine
+  (csrc/kernels.cu), fp32/fp16/bf16 caches;
+* bf16 suffix / self-attention metas with long query runs -> K3 tcgen05
+  prefill (csrc/prefill_sm100.cu) when the shape is supported.
+
+The reference mask predicate (attention.py:113-134) admits, for query i of
+sequence s, exactly the key prefix [0, n_i) of s with n_i = min(q_pos+1, len)
+when causal and len otherwise; the host reduces every MaskMeta to that count,
+so kernels never see the block mask.  `block_mask` / `skip_empty` are accepted
+for signature compatibility: the reference guarantees skip == no-skip bitwise
+(test_attention.py:206-210), and the device path only ever visits allowed keys.
+Grouped-query attention (not in the reference) is enabled by
+`AttentionConfig.kv_head_count`; q head h reads kv head h // G.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import math
+from dataclasses import dataclass, field
+from enum import IntEnum
+
+import numpy as np
+
+from . import _lib
+from .errors import NoAllowedKeys, OutOfRange, ShapeMismatch
+from .store import BatchView, KvStore, _ptr, _stream, to_device, torch_dtype
+
+
+class BlockKind(IntEnum):
+    EMPTY = 0
+    PARTIAL = 1
+    FULL = 2
+
+
+@dataclass
+class AttentionConfig:
+    """attention.py:32-48, plus `kv_head_count` for grouped-query attention."""
+
+    head_count: int
+    head_dim: int
+    scale: float | None = None
+    causal: bool = True
+    page_size: int = 64
+    kv_head_count: int | None = None
+
+    def __post_init__(self):
+        if self.head_count <= 0 or self.head_dim <= 0:
+            raise ValueError("head_count and head_dim must be positive")
+        if self.page_size <= 0 or self.page_size & (self.page_size - 1):
+            raise ValueError("page_size must be a positive power of two")
+        if self.scale is None:
+            self.scale = 1.0 / math.sqrt(self.head_dim)
+        if self.scale <= 0:
+            raise ValueError("scale must be positive")
+        if self.kv_head_count is None:
+            self.kv_head_count = self.head_count
+        if self.kv_head_count <= 0 or self.head_count % self.kv_head_count:
+            raise ValueError("head_count must be a multiple of kv_head_count")
+
+
+@dataclass
+class MaskMeta:
+    """Query-side addressing against a KV batch view (attention.py:51-110)."""
+
+    view: BatchView
+    q_seq: np.ndarray
+    q_pos: np.ndarray
+
+    def __post_init__(self):
+        self.q_seq = np.asarray(self.q_seq, dtype=np.int64)
+        self.q_pos = np.asarray(self.q_pos, dtype=np.int64)
+        if self.q_seq.shape != self.q_pos.shape or self.q_seq.ndim != 1:
+            raise ShapeMismatch("q_seq and q_pos must be 1-D vectors of equal length")
+        if self.q_seq.size:
+            if (np.diff(self.q_seq) < 0).any():
+                raise ValueError("q_seq must be non-decreasing (sequence-major order)")
+            if self.q_seq.min() < 0 or self.q_seq.max() >= len(self.view.lengths):
+                raise OutOfRange("q_seq refers to a sequence outside the view")
+            if (self.q_pos < 0).any() or (self.q_pos >= self.view.lengths[self.q_seq]).any():
+                raise OutOfRange("query positions must be < their sequence length")
+
+    @property
+    def query_count(self) -> int:
+        return int(self.q_seq.shape[0])
+
+    @classmethod
+    def self_attention(cls, view: BatchView) -> "MaskMeta":
+        return cls(view=view, q_seq=view.slot_seq.copy(), q_pos=view.slot_local.copy())
+
+    @classmethod
+    def decode(cls, view: BatchView) -> "MaskMeta":
+        n = len(view.lengths)
+        if (view.lengths <= 0).any():
+            raise OutOfRange("decode meta requires every sequence to have length >= 1")
+        return cls(view=view, q_seq=np.arange(n, dtype=np.int64), q_pos=view.lengths - 1)
+
+    @classmethod
+    def suffix(cls, view: BatchView, q_lengths) -> "MaskMeta":
+        q_lengths = np.asarray(q_lengths, dtype=np.int64)
+        if q_lengths.shape != view.lengths.shape:
+            raise ShapeMismatch("one query count per sequence required")
+        if (q_lengths < 0).any() or (q_lengths > view.lengths).any():
+            raise OutOfRange("query counts must be within sequence lengths")
+        q_seq = np.repeat(np.arange(len(q_lengths), dtype=np.int64), q_lengths)
+        if q_lengths.sum():
+            q_pos = np.concatenate([np.arange(n - q, n, dtype=np.int64)
+                                    for n, q in zip(view.lengths, q_lengths)])
+        else:
+            q_pos = np.zeros(0, dtype=np.int64)
+        return cls(view=view, q_seq=q_seq, q_pos=q_pos)
+
+
+def mask_allow(q_index: int, k_index: int, meta: MaskMeta, causal: bool = True) -> bool:
+    """Pointwise predicate over flat indices (attention.py:113-134)."""
+    if q_index < 0 or q_index >= meta.query_count:
+        raise OutOfRange(f"query index {q_index} outside flat query batch")
+    view = meta.view
+    if k_index < 0 or k_index >= view.total_slots:
+        raise OutOfRange(f"kv index {k_index} outside flat batch of {view.total_slots}")
+    q_seq = int(meta.q_seq[q_index])
+    k_seq = int(view.slot_seq[k_index])
+    if q_seq != k_seq:
+        return False
+    k_local = int(view.slot_local[k_index])
+    if k_local >= int(view.lengths[k_seq]):
+        return False
+    return not (causal and k_local > int(meta.q_pos[q_index]))
+
+
+def allowed_key_counts(meta: MaskMeta, causal: bool) -> np.ndarray:
+    """Length of the allowed key prefix of every query (see module doc)."""
+    lens = meta.view.lengths[meta.q_seq]
+    return np.minimum(meta.q_pos + 1, lens) if causal else lens.copy()
+
+
+@dataclass
+class BlockMask:
+    """FULL/PARTIAL/EMPTY per (query tile, kv tile) of the flat view
+    (attention.py:137-168); host metadata used for KernelStats parity."""
+
+    kinds: np.ndarray = field(repr=False)
+    page_size: int
+    q_len: int
+    kv_len: int
+
+    def kind(self, q_block: int, k_block: int) -> BlockKind:
+        return BlockKind(int(self.kinds[q_block, k_block]))
+
+    def counts(self) -> dict:
+        return {"empty": int((self.kinds == 0).sum()), "partial": int((self.kinds == 1).sum()),
+                "full": int((self.kinds == 2).sum())}
+
+
+def build_block_mask(meta: MaskMeta, config: AttentionConfig) -> BlockMask:
+    """Tile classification (attention.py:171-210), vectorised per query tile:
+    query i admits the flat key interval [prefix[s], prefix[s] + n_i)."""
+    bs = config.page_size
+    nq, nk = meta.query_count, meta.view.total_slots
+    n_qb, n_kb = -(-nq // bs), -(-nk // bs)
+    kinds = np.zeros((n_qb, n_kb), dtype=np.int8)
+    if n_qb and n_kb:
+        lo = meta.view.prefix_sums[meta.q_seq]
+        hi = lo + allowed_key_counts(meta, config.causal)
+        k0 = np.arange(n_kb) * bs
+        k1 = np.minimum(k0 + bs, nk)
+        for qb in range(n_qb):
+            a = lo[qb * bs:(qb + 1) * bs, None]
+            b = hi[qb * bs:(qb + 1) * bs, None]
+            hit = ((a < k1[None]) & (b > k0[None])).any(axis=0)
+            full = ((a <= k0[None]) & (b >= k1[None])).all(axis=0)
+            kinds[qb] = np.where(full, 2, np.where(hit, 1, 0))
+    return BlockMask(kinds=kinds, page_size=bs, q_len=nq, kv_len=nk)
+
+
+@dataclass
+class KernelStats:
+    """Per-run instrumentation (attention.py:213-226), computed on the host
+    from the metadata: the device kernels never visit disallowed keys."""
+
+    visited_blocks: int = 0
+    skipped_blocks: int = 0
+    allowed_pairs: int = 0
+    head_count: int = 0
+    head_dim: int = 0
+
+    @property
+    def attention_flops(self) -> int:
+        return 4 * self.head_count * self.head_dim * self.allowed_pairs
+
+
+def _fill_stats(stats: KernelStats, meta: MaskMeta, config: AttentionConfig, nkeys, block_mask):
+    stats.head_count, stats.head_dim = config.head_count, config.head_dim
+    if meta.query_count == 0:
+        return
+    bm = block_mask if block_mask is not None else build_block_mask(meta, config)
+    visited = int((bm.kinds != 0).sum())
+    stats.visited_blocks += visited
+    stats.skipped_blocks += int(bm.kinds.size) - visited
+    stats.allowed_pairs += int(nkeys.sum())
+
+
+def _check_queries(queries, meta: MaskMeta, config: AttentionConfig):
+    expected = (meta.query_count, config.head_count, config.head_dim)
+    shape = tuple(queries.shape) if hasattr(queries, "shape") else np.asarray(queries).shape
+    if shape != expected:
+        raise ShapeMismatch(f"expected queries of shape {expected}, got {shape}")
+
+
+class _Workspace:
+    """Per-device scratch for split partials and the device split plan."""
+
+    _bufs: dict = {}
+
+    @classmethod
+    def get(cls, device, nbytes: int):
+        import torch
+
+        buf = cls._bufs.get(device)
+        if buf is None or buf.numel() < nbytes:
+            buf = torch.empty(max(nbytes, 1 << 20), dtype=torch.uint8, device=device)
+            cls._bufs[device] = buf
+        return buf
+
+
+def _q_tensor(queries, device):
+    import torch
+
+    q = queries if isinstance(queries, torch.Tensor) else torch.from_numpy(np.ascontiguousarray(queries))
+    if q.dtype == torch.float64:
+        q = q.float()
+    q = q.to(device).contiguous()
+    _, code = torch_dtype(q.dtype)
+    return q, code
+
+
+def _launch_attention(q, qcode, meta, config, nkeys, *, k, v, kv_code, bt, bt_stride, seq_row,
+                      seq_start, out_dtype, device):
+    import torch
+
+    nq = meta.query_count
+    out_t, out_code = torch_dtype(out_dtype)
+    out = torch.empty((nq, config.head_count, config.head_dim), dtype=out_t, device=device)
+    if nq == 0:
+        return out
+    meta_host = np.concatenate([meta.q_seq.astype(np.int32), nkeys.astype(np.int32)])
+    meta_dev = torch.from_numpy(meta_host).to(device)
+    ws_bytes = _lib.load().pkv_attention_workspace_bytes(nq, config.head_count, config.head_dim)
+    ws = _Workspace.get(device, ws_bytes)
+    args = _lib.AttentionArgs(
+        q=q.data_ptr(), q_dtype=qcode, n_queries=nq,
+        q_seq=meta_dev.data_ptr(), q_nkeys=meta_dev.data_ptr() + 4 * nq,
+        k_cache=k.data_ptr(), v_cache=v.data_ptr(), kv_dtype=kv_code,
+        block_table=bt.data_ptr() if bt is not None else None, bt_stride=bt_stride,
+        seq_row=seq_row.data_ptr() if seq_row is not None else None,
+        seq_start=seq_start.data_ptr() if seq_start is not None else None,
+        page_size=config.page_size, hq=config.head_count, hkv=config.kv_head_count,
+        head_dim=config.head_dim, scale=float(config.scale), out=out.data_ptr(), out_dtype=out_code,
+        workspace=ws.data_ptr(), workspace_bytes=ws.numel(), num_sms=0, target_waves=0)
+    _lib.check(_lib.load().pkv_paged_attention(C.byref(args), _stream(device)), "pkv_paged_attention")
+    return out
+
+
+def paged_attention(queries, store: KvStore, meta: MaskMeta, config: AttentionConfig, *,
+                    stats: KernelStats | None = None, block_mask: BlockMask | None = None,
+                    skip_empty: bool = True, out_dtype=None):
+    """Exact attention over scattered pages (attention.py:332-354), on the GPU.
+
+    `queries` is (n_queries, head_count, head_dim), numpy or torch; the result
+    is a device tensor (fp32 unless `out_dtype` says otherwise)."""
+    import torch
+
+    _check_queries(queries, meta, config)
+    if store.head_count != config.kv_head_count or store.head_dim != config.head_dim:
+        raise ShapeMismatch("store head layout does not match attention config")
+    if config.page_size != store.page_size:
+        raise ShapeMismatch("attention page_size does not match the pool")
+    view = meta.view
+    tables = [store.pool.table(s) for s in view.ids]
+    for t, n in zip(tables, view.lengths):
+        if n < 0 or n > len(t.entries) * store.page_size:
+            raise OutOfRange(f"length {int(n)} exceeds reserved capacity of sequence {t.seq_id!r}")
+    nkeys = allowed_key_counts(meta, config.causal)
+    if meta.query_count and (nkeys <= 0).any():
+        bad = np.nonzero(nkeys <= 0)[0].tolist()
+        raise NoAllowedKeys(f"queries {bad} have zero allowed keys")
+    if stats is not None:
+        _fill_stats(stats, meta, config, nkeys, block_mask)
+    device = store.device
+    q, qcode = _q_tensor(queries, device)
+    seq_row = torch.from_numpy(np.asarray([t.mirror_row for t in tables], dtype=np.int32)).to(device)
+    mirror = store.pool.device_table(device)
+    return _launch_attention(q, qcode, meta, config, nkeys, k=store.keys, v=store.values,
+                             kv_code=store.dtype_code, bt=mirror, bt_stride=mirror.shape[1],
+                             seq_row=seq_row, seq_start=None,
+                             out_dtype=out_dtype or torch.float32, device=device)
+
+
+def gathered_attention(queries, keys, values, meta: MaskMeta, config: AttentionConfig, *,
+                       stats: KernelStats | None = None, block_mask: BlockMask | None = None,
+                       skip_empty: bool = True, out_dtype=None, device=None):
+    """Same kernel over contiguous K/V (attention.py:357-378); bitwise equal to
+    the paged path on identical content (the split schedule depends only on
+    logical lengths)."""
+    import torch
+
+    from .store import _device
+
+    _check_queries(queries, meta, config)
+    expected = (meta.view.total_slots, config.kv_head_count, config.head_dim)
+    if tuple(keys.shape) != expected or tuple(values.shape) != expected:
+        raise ShapeMismatch(f"expected K/V of shape {expected}, got {tuple(keys.shape)}/{tuple(values.shape)}")
+    nkeys = allowed_key_counts(meta, config.causal)
+    if meta.query_count and (nkeys <= 0).any():
+        raise NoAllowedKeys("a query has zero allowed keys")
+    if stats is not None:
+        _fill_stats(stats, meta, config, nkeys, block_mask)
+    if device is None:
+        device = keys.device if isinstance(keys, torch.Tensor) and keys.is_cuda else _device(None)
+    k = to_device(keys, device)
+    v = to_device(values, device, k.dtype)
+    _, kv_code = torch_dtype(k.dtype)
+    q, qcode = _q_tensor(queries, device)
+    seq_start = torch.from_numpy(meta.view.prefix_sums.astype(np.int64)).to(device)
+    return _launch_attention(q, qcode, meta, config, nkeys, k=k, v=v, kv_code=kv_code, bt=None,
+                             bt_stride=0, seq_row=None, seq_start=seq_start,
+                             out_dtype=out_dtype or torch.float32, device=device)

@@ -1,0 +1,121 @@
+"""Batched decode step — B sequences advance one token through one
+allocator call, one K1 append launch and one K2 (+K2c) attention launch.
+
+This is the serving-loop form of the reference's per-session
+`DecodeSession.step` (decoder.py:263-284): grow -> assign at `logical_len`
+-> attend over all `logical_len + 1` keys (the new token included,
+attention.py:86-96).  Semantics per sequence are exactly the reference's; the
+batch only amortises host work (one native `pkv_pool_prepare_append` for all
+allocator bookkeeping, one packed metadata upload) and launches.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+
+import numpy as np
+
+from . import _lib
+from .attention import AttentionConfig, _Workspace, _q_tensor
+from .store import KvStore, _ptr, _stream, torch_dtype
+
+
+class DecodeBatch:
+    """Decode B sequences of one pool together.
+
+    `stores` is one KvStore (one layer) or a list of stores on the same pool
+    (one per layer); `step(layer_inputs)` appends and attends layer by layer.
+    """
+
+    def __init__(self, stores, seq_ids, config: AttentionConfig):
+        import torch
+
+        self.stores = list(stores) if isinstance(stores, (list, tuple)) else [stores]
+        self.pool = self.stores[0].pool
+        self.device = self.stores[0].device
+        if any(s.pool is not self.pool for s in self.stores):
+            raise ValueError("all stores of a DecodeBatch must share one pool")
+        self.config = config
+        self.seq_ids = list(seq_ids)
+        self.handles = np.asarray([self.pool.table(s)._handle for s in self.seq_ids], dtype=np.int64)
+        self.n = len(self.seq_ids)
+        self._pos = np.empty(self.n, dtype=np.int32)
+        self._rows = np.empty(self.n, dtype=np.int32)
+        self._copies = np.empty(2 * self.n, dtype=np.int64)
+        self._pages = np.empty(2 * self.n + 1, dtype=np.uint32)
+        # packed per-step metadata [q_seq | nkeys | positions | rows]: a ring of
+        # pinned staging buffers, each reused only after its upload completed
+        self._ring = []
+        for _ in range(4):
+            host = torch.empty(4 * self.n, dtype=torch.int32).pin_memory()
+            host[: self.n] = torch.arange(self.n, dtype=torch.int32)
+            dev = torch.empty(4 * self.n, dtype=torch.int32, device=self.device)
+            self._ring.append((host, dev, torch.cuda.Event()))
+        self._slot = 0
+        self.last_launches = 0
+
+    def prepare(self):
+        """Allocator work of one step (host): returns positions, rows."""
+        n_pages = C.c_int64()
+        i64p, i32p, u32p = C.POINTER(C.c_int64), C.POINTER(C.c_int32), C.POINTER(C.c_uint32)
+        _lib.call("pkv_pool_prepare_append", self.pool._h, self.handles.ctypes.data_as(i64p), self.n,
+                  self._pos.ctypes.data_as(i32p), self._rows.ctypes.data_as(i32p),
+                  self._pages.ctypes.data_as(u32p), self._pages.size, C.byref(n_pages),
+                  self._copies.ctypes.data_as(i64p))
+        launches = 0
+        if n_pages.value:
+            pages = self._pages[: n_pages.value].tolist()
+            self.pool._clear_pages(pages)
+            launches += len(self.pool._stores)
+        for old, new in self._copies.reshape(-1, 2):
+            if new >= 0:
+                self.pool._copy_rows(int(old), int(new), self.pool.page_size)
+                launches += len(self.pool._stores)
+        return launches
+
+    def step(self, queries, k_new, v_new, *, out_dtype=None, layer: int = 0, advance: bool = True):
+        """Append one token per sequence into `stores[layer]` and attend.
+
+        queries [B, Hq, D]; k_new / v_new [B, Hkv, D] (numpy or torch, any
+        device).  With several layers call `prepare()` once per token, then
+        `step(..., layer=i, advance=False)` for every layer."""
+        import torch
+
+        launches = self.prepare() if advance else 0
+        store: KvStore = self.stores[layer]
+        cfg = self.config
+        n = self.n
+        host, dev, done = self._ring[self._slot]
+        self._slot = (self._slot + 1) % len(self._ring)
+        done.synchronize()  # the previous upload from this buffer has landed
+        mh = host.numpy()
+        mh[n:2 * n] = self._pos + 1          # keys attended: the whole context
+        mh[2 * n:3 * n] = self._pos
+        mh[3 * n:] = self._rows
+        dev.copy_(host, non_blocking=True)
+        done.record()
+        mirror = self.pool.device_table(self.device)
+        k = k_new if isinstance(k_new, torch.Tensor) else torch.from_numpy(np.ascontiguousarray(k_new))
+        v = v_new if isinstance(v_new, torch.Tensor) else torch.from_numpy(np.ascontiguousarray(v_new))
+        k = k.to(device=self.device, dtype=store.torch_dtype, non_blocking=True).contiguous()
+        v = v.to(device=self.device, dtype=store.torch_dtype, non_blocking=True).contiguous()
+        stream = _stream(self.device)
+        md = dev.data_ptr()
+        _lib.call("pkv_kv_append", _ptr(k), _ptr(v), n, C.c_void_p(md + 12 * n), 1,
+                  C.c_void_p(md + 8 * n), _ptr(mirror), mirror.shape[1], store.page_size,
+                  _ptr(store.keys), _ptr(store.values), store.row_bytes, stream)
+        q, qcode = _q_tensor(queries, self.device)
+        out_t, out_code = torch_dtype(out_dtype or torch.float32)
+        out = torch.empty((n, cfg.head_count, cfg.head_dim), dtype=out_t, device=self.device)
+        ws_bytes = _lib.load().pkv_attention_workspace_bytes(n, cfg.head_count, cfg.head_dim)
+        ws = _Workspace.get(self.device, ws_bytes)
+        args = _lib.AttentionArgs(
+            q=q.data_ptr(), q_dtype=qcode, n_queries=n, q_seq=md, q_nkeys=md + 4 * n,
+            k_cache=store.keys.data_ptr(), v_cache=store.values.data_ptr(), kv_dtype=store.dtype_code,
+            block_table=mirror.data_ptr(), bt_stride=mirror.shape[1], seq_row=md + 12 * n,
+            seq_start=None, page_size=store.page_size, hq=cfg.head_count, hkv=cfg.kv_head_count,
+            head_dim=cfg.head_dim, scale=float(cfg.scale), out=out.data_ptr(), out_dtype=out_code,
+            workspace=ws.data_ptr(), workspace_bytes=ws.numel(), num_sms=0, target_waves=0)
+        _lib.check(_lib.load().pkv_paged_attention(C.byref(args), stream), "pkv_paged_attention")
+        self.last_launches = launches + 4  # append + plan + decode + combine
+        return out

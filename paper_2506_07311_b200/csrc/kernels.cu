@@ -1,0 +1,823 @@
+// sm_100a data-plane kernels of the paged-attention engine.
+//
+//   K0a page_zero      KvStore.clear_pages        (reference store.py:95-100)
+//   K0b page_copy      KvStore.copy_rows          (reference store.py:85-93)
+//   K1  kv_append      KvStore.assign scatter     (reference store.py:146-150)
+//   K2  split-K decode paged_attention            (reference attention.py:259-354)
+//   K2c combine        merge of split partials
+//   mirror_apply       device block-table mirror update (new)
+//
+// Layout in HBM (one store = one layer): K and V caches are row-major
+// [pages * page_size, Hkv, D] in the element type of the store — the
+// reference's NHD row layout (store.py:74-76) — so one (page, kv-head) slice is
+// page_size rows of D*s bytes at a stride of Hkv*D*s bytes.
+//
+// K2 design (memory bound): the unit of work is one *warp* on
+// (query, kv-head, q-head group, key split).  Each warp streams its split
+// through a private multi-stage cp.async ring in shared memory (16-byte
+// copies, zero-fill past the valid keys), computes scores with the G grouped
+// query heads held in registers (so each K/V byte is read from HBM once per
+// group), and keeps one online-softmax state per lane group; states are merged
+// with warp shuffles at the end of the split.  Splits are planned on the device
+// from the per-query key counts (plan kernel), so a decode step needs no host
+// round trip and the schedule depends only on logical lengths — paged and
+// gathered sources therefore produce bit-identical results.
+#include <cuda_bf16.h>
+#include <cuda_fp16.h>
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "pkv200.h"
+#include "status.h"
+
+namespace {
+
+constexpr int kMaxExtraSplits = 8192;  // planner bound, see workspace_bytes
+constexpr float kLog2e = 1.4426950408889634f;
+
+#define PKV_CHECK_LAUNCH()                                                                \
+  do {                                                                                    \
+    cudaError_t _e = cudaGetLastError();                                                  \
+    if (_e != cudaSuccess)                                                                \
+      return pkv::fail(PKV_CUDA_ERROR, "%s: %s", __func__, cudaGetErrorString(_e));       \
+  } while (0)
+
+inline int elem_bytes(int dt) { return dt == PKV_F32 ? 4 : 2; }
+
+// ---------------------------------------------------------------------------
+// small device helpers
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ uint32_t smem_addr(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+template <int VEC>
+__device__ __forceinline__ void cp_async(uint32_t dst, const void* src, int src_bytes) {
+  if constexpr (VEC == 16) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(dst), "l"(src),
+                 "r"(src_bytes));
+  } else {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], %2, %3;\n" ::"r"(dst), "l"(src),
+                 "n"(VEC), "r"(src_bytes));
+  }
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
+}
+
+// element type traits: convert 16-byte chunks to fp32
+template <typename T>
+struct Elem;
+template <>
+struct Elem<float> {
+  static constexpr int kBytes = 4;
+  static constexpr int kPerChunk = 4;
+  __device__ __forceinline__ static void unpack(const uint4& c, float* f) {
+    f[0] = __uint_as_float(c.x);
+    f[1] = __uint_as_float(c.y);
+    f[2] = __uint_as_float(c.z);
+    f[3] = __uint_as_float(c.w);
+  }
+};
+template <>
+struct Elem<__nv_bfloat16> {
+  static constexpr int kBytes = 2;
+  static constexpr int kPerChunk = 8;
+  __device__ __forceinline__ static void unpack(const uint4& c, float* f) {
+    const uint32_t w[4] = {c.x, c.y, c.z, c.w};
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      f[2 * i] = __uint_as_float(w[i] << 16);
+      f[2 * i + 1] = __uint_as_float(w[i] & 0xffff0000u);
+    }
+  }
+};
+template <>
+struct Elem<__half> {
+  static constexpr int kBytes = 2;
+  static constexpr int kPerChunk = 8;
+  __device__ __forceinline__ static void unpack(const uint4& c, float* f) {
+    const uint32_t w[4] = {c.x, c.y, c.z, c.w};
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      __half2 h = *reinterpret_cast<const __half2*>(&w[i]);
+      float2 v = __half22float2(h);
+      f[2 * i] = v.x;
+      f[2 * i + 1] = v.y;
+    }
+  }
+};
+
+__device__ __forceinline__ float load_as_float(const void* base, int64_t idx, int dtype) {
+  if (dtype == PKV_F32) return static_cast<const float*>(base)[idx];
+  if (dtype == PKV_BF16) return __bfloat162float(static_cast<const __nv_bfloat16*>(base)[idx]);
+  return __half2float(static_cast<const __half*>(base)[idx]);
+}
+__device__ __forceinline__ void store_from_float(void* base, int64_t idx, int dtype, float v) {
+  if (dtype == PKV_F32)
+    static_cast<float*>(base)[idx] = v;
+  else if (dtype == PKV_BF16)
+    static_cast<__nv_bfloat16*>(base)[idx] = __float2bfloat16_rn(v);
+  else
+    static_cast<__half*>(base)[idx] = __float2half_rn(v);
+}
+
+// byte copy with the widest vector the alignment allows
+__device__ __forceinline__ void copy_bytes(char* dst, const char* src, int64_t n, int64_t tid,
+                                           int64_t nthreads) {
+  if ((n & 15) == 0) {
+    for (int64_t i = tid; i < (n >> 4); i += nthreads)
+      reinterpret_cast<uint4*>(dst)[i] = reinterpret_cast<const uint4*>(src)[i];
+  } else if ((n & 3) == 0) {
+    for (int64_t i = tid; i < (n >> 2); i += nthreads)
+      reinterpret_cast<uint32_t*>(dst)[i] = reinterpret_cast<const uint32_t*>(src)[i];
+  } else {
+    for (int64_t i = tid; i < (n >> 1); i += nthreads)
+      reinterpret_cast<uint16_t*>(dst)[i] = reinterpret_cast<const uint16_t*>(src)[i];
+  }
+}
+__device__ __forceinline__ void zero_bytes(char* dst, int64_t n, int64_t tid, int64_t nthreads) {
+  if ((n & 15) == 0) {
+    for (int64_t i = tid; i < (n >> 4); i += nthreads)
+      reinterpret_cast<uint4*>(dst)[i] = make_uint4(0, 0, 0, 0);
+  } else if ((n & 3) == 0) {
+    for (int64_t i = tid; i < (n >> 2); i += nthreads) reinterpret_cast<uint32_t*>(dst)[i] = 0;
+  } else {
+    for (int64_t i = tid; i < (n >> 1); i += nthreads) reinterpret_cast<uint16_t*>(dst)[i] = 0;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// K0 / K1 / mirror
+// ---------------------------------------------------------------------------
+__global__ void mirror_apply_kernel(int32_t* table, const int32_t* pairs, int64_t n) {
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n;
+       i += int64_t(gridDim.x) * blockDim.x)
+    table[pairs[2 * i]] = pairs[2 * i + 1];
+}
+
+__global__ void page_zero_kernel(char* k, char* v, const int32_t* pages, int64_t n,
+                                 int64_t page_bytes) {
+  for (int64_t i = blockIdx.x; i < n; i += gridDim.x) {
+    int64_t off = int64_t(pages[i]) * page_bytes;
+    zero_bytes(k + off, page_bytes, threadIdx.x, blockDim.x);
+    zero_bytes(v + off, page_bytes, threadIdx.x, blockDim.x);
+  }
+}
+
+__global__ void page_copy_kernel(char* k, char* v, const int32_t* triples, int64_t n,
+                                 int64_t row_bytes, int page_size) {
+  for (int64_t i = blockIdx.x; i < n; i += gridDim.x) {
+    const int64_t src = triples[3 * i], dst = triples[3 * i + 1], rows = triples[3 * i + 2];
+    const int64_t pb = row_bytes * page_size;
+    const int64_t keep = rows * row_bytes;
+    // src == dst would alias; the allocator never reports that
+    copy_bytes(k + dst * pb, k + src * pb, keep, threadIdx.x, blockDim.x);
+    copy_bytes(v + dst * pb, v + src * pb, keep, threadIdx.x, blockDim.x);
+    zero_bytes(k + dst * pb + keep, pb - keep, threadIdx.x, blockDim.x);
+    zero_bytes(v + dst * pb + keep, pb - keep, threadIdx.x, blockDim.x);
+  }
+}
+
+// one CTA per token (grid-stride); the slot is resolved in-kernel from the
+// block-table mirror (shift/mask: the page size is a power of two)
+__global__ void kv_append_kernel(const char* __restrict__ kn, const char* __restrict__ vn,
+                                 int64_t n_tok, const int32_t* __restrict__ tok_row,
+                                 int row_stride, const int32_t* __restrict__ tok_pos,
+                                 const int32_t* __restrict__ bt, int64_t bt_stride, int log2ps,
+                                 char* __restrict__ kc, char* __restrict__ vc, int64_t row_bytes) {
+  const int ps = 1 << log2ps;
+  for (int64_t t = blockIdx.x; t < n_tok; t += gridDim.x) {
+    const int32_t pos = tok_pos[t];
+    const int64_t r = tok_row[t * row_stride];
+    const int64_t page = bt[r * bt_stride + (pos >> log2ps)];
+    const int64_t dst = (page * ps + (pos & (ps - 1))) * row_bytes;
+    copy_bytes(kc + dst, kn + t * row_bytes, row_bytes, threadIdx.x, blockDim.x);
+    copy_bytes(vc + dst, vn + t * row_bytes, row_bytes, threadIdx.x, blockDim.x);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// split planner (device): plan[0] = split_pages, plan[1] = total splits,
+// plan[4 + i] = exclusive prefix of per-query split counts (n_queries + 1)
+// ---------------------------------------------------------------------------
+constexpr int kPlanThreads = 1024;
+
+__global__ void __launch_bounds__(kPlanThreads) plan_kernel(
+    const int32_t* __restrict__ q_nkeys, int64_t nq, int log2ps, int head_items,
+    int64_t target_items, int32_t* __restrict__ plan) {
+  __shared__ long long red[kPlanThreads / 32];
+  __shared__ int scan[kPlanThreads / 32];
+  __shared__ long long s_total;
+  __shared__ int s_carry;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int ps = 1 << log2ps;
+  long long pages = 0;
+  for (int64_t i = tid; i < nq; i += kPlanThreads) pages += (q_nkeys[i] + ps - 1) >> log2ps;
+#pragma unroll
+  for (int o = 16; o; o >>= 1) pages += __shfl_xor_sync(0xffffffffu, pages, o);
+  if (lane == 0) red[warp] = pages;
+  __syncthreads();
+  if (tid == 0) {
+    long long t = 0;
+    for (int w = 0; w < kPlanThreads / 32; ++w) t += red[w];
+    s_total = t;
+    s_carry = 0;
+  }
+  __syncthreads();
+  const long long total_pages = s_total;
+  long long sp = (total_pages * head_items + target_items - 1) / target_items;
+  const long long sp_cap = (total_pages + kMaxExtraSplits - 1) / kMaxExtraSplits;
+  if (sp < sp_cap) sp = sp_cap;
+  if (sp < 1) sp = 1;
+  for (int64_t base = 0; base < nq; base += kPlanThreads) {
+    const int64_t i = base + tid;
+    int cnt = 0;
+    if (i < nq) {
+      const long long p = (q_nkeys[i] + ps - 1) >> log2ps;
+      cnt = static_cast<int>((p + sp - 1) / sp);
+    }
+    int x = cnt;  // inclusive warp scan
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      int y = __shfl_up_sync(0xffffffffu, x, o);
+      if (lane >= o) x += y;
+    }
+    if (lane == 31) scan[warp] = x;
+    __syncthreads();
+    if (warp == 0) {
+      int w = scan[lane];
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        int y = __shfl_up_sync(0xffffffffu, w, o);
+        if (lane >= o) w += y;
+      }
+      scan[lane] = w;  // inclusive over warps
+    }
+    __syncthreads();
+    const int carry = s_carry;
+    const int excl = carry + (warp ? scan[warp - 1] : 0) + x - cnt;
+    if (i < nq) plan[4 + i] = excl;
+    __syncthreads();
+    if (tid == kPlanThreads - 1) s_carry = excl + cnt;
+    __syncthreads();
+  }
+  if (tid == 0) {
+    plan[0] = static_cast<int32_t>(sp);
+    plan[1] = s_carry;
+    plan[4 + nq] = s_carry;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// K2: split-K paged decode
+// ---------------------------------------------------------------------------
+struct DecodeParams {
+  const void* q;
+  int q_dtype;
+  int64_t nq;
+  const int32_t* q_seq;
+  const int32_t* q_nkeys;
+  const char* k;
+  const char* v;
+  const int32_t* bt;
+  int64_t bt_stride;
+  const int32_t* seq_row;
+  const int64_t* seq_start;
+  int log2ps;
+  int hq, hkv, d, group, head_items;
+  int64_t row_stride_bytes;  // Hkv * D * s
+  float qscale;              // scale * log2(e)
+  void* out;
+  int out_dtype;
+  const int32_t* plan;
+  float* ws_ml;  // [splits, hq, 2]
+  float* ws_o;   // [splits, hq, D]
+};
+
+// compile-time geometry of one kernel instance
+template <typename T, int DP, int R>
+struct Geo {
+  static constexpr int S = Elem<T>::kBytes;
+  static constexpr int CE = Elem<T>::kPerChunk;      // elements per 16-B chunk
+  static constexpr int ROWB = DP * S;                // padded smem row bytes
+  static constexpr int EPL = (DP < 32 / S) ? DP : 32 / S;  // elements per lane
+  static constexpr int NCH = EPL * S / 16;           // 16-B chunks per lane (1 or 2)
+  static constexpr int LPK = DP / EPL;               // lanes per key
+  static constexpr int KG = 32 / LPK;                // key groups per warp
+  static constexpr int CH0 = 4096 / ROWB;
+  static constexpr int CH = CH0 > 32 ? 32 : (CH0 < 4 ? 4 : CH0);  // keys per chunk
+  static constexpr int KPL = CH / KG;                // keys per lane group per chunk
+  static constexpr int STAGE = 2 * CH * ROWB;        // K + V bytes per stage
+  static_assert(NCH == 1 || NCH == 2, "lane owns one or two 16-byte chunks");
+  static_assert(LPK >= 1 && LPK <= 32 && KPL >= 1, "bad geometry");
+};
+
+constexpr int kWarps = 8;   // warps per CTA (one CTA per SM)
+constexpr int kStages = 3;  // cp.async ring depth per warp
+
+template <typename T, int DP, int R>
+__global__ void __launch_bounds__(kWarps * 32, 1) decode_kernel(const __grid_constant__ DecodeParams p) {
+  using G = Geo<T, DP, R>;
+  extern __shared__ __align__(128) unsigned char smem[];
+  const int lane = threadIdx.x & 31;
+  const int warp = threadIdx.x >> 5;
+  unsigned char* wsm = smem + warp * (kStages * G::STAGE);
+  const uint32_t wsm_addr = smem_addr(wsm);
+  // zero the ring once: row padding (D..DP) is never written by cp.async
+  for (int i = lane; i < kStages * G::STAGE / 16; i += 32)
+    reinterpret_cast<uint4*>(wsm)[i] = make_uint4(0, 0, 0, 0);
+  __syncwarp();
+
+  const int kg = lane / G::LPK;  // key group
+  const int lk = lane % G::LPK;  // lane within key
+  const int ps = 1 << p.log2ps;
+  const int row_real = p.d * G::S;  // real bytes of one head row
+  // copy granularity for the real bytes of a row
+  const int vec = (row_real & 15) == 0 ? 16 : ((row_real & 7) == 0 ? 8 : 4);
+  const int cpr = row_real / vec;  // copies per row
+  const bool cpr_pow2 = (cpr & (cpr - 1)) == 0;
+  const int cpr_sh = __ffs(cpr) - 1;
+
+  const int split_pages = p.plan[0];
+  const int64_t total_items = int64_t(p.plan[1]) * p.head_items;
+  const int32_t* offsets = p.plan + 4;
+  const int64_t gwarp = int64_t(blockIdx.x) * kWarps + warp;
+  const int64_t nwarps = int64_t(gridDim.x) * kWarps;
+  const int qgroups = p.group / R;
+
+  for (int64_t w = gwarp; w < total_items; w += nwarps) {
+    const int64_t sg = w / p.head_items;
+    const int hi = static_cast<int>(w - sg * p.head_items);
+    const int kvh = hi / qgroups;
+    const int qh0 = kvh * p.group + (hi - kvh * qgroups) * R;
+    // query owning split sg: offsets[qi] <= sg < offsets[qi+1]
+    int64_t lo = 0, hi_q = p.nq;
+    while (hi_q - lo > 1) {
+      const int64_t mid = (lo + hi_q) >> 1;
+      if (offsets[mid] <= sg) lo = mid; else hi_q = mid;
+    }
+    const int64_t qi = lo;
+    const int split = static_cast<int>(sg - offsets[qi]);
+    const int nsplit = offsets[qi + 1] - offsets[qi];
+    const int nk = p.q_nkeys[qi];
+    const int sv = p.q_seq[qi];
+    const int kb = split * split_pages * ps;
+    const int ke = min(nk, kb + split_pages * ps);
+    const int n_chunks = (ke - kb + G::CH - 1) / G::CH;
+    const int64_t bt_off = p.bt ? int64_t(p.seq_row[sv]) * p.bt_stride : 0;
+    const int64_t gstart = p.bt ? 0 : p.seq_start[sv];
+    const int npages_seq = (nk + ps - 1) >> p.log2ps;
+    const char* kbase = p.k + int64_t(kvh) * row_real;
+    const char* vbase = p.v + int64_t(kvh) * row_real;
+
+    // ---- queries of the R grouped heads, pre-scaled into the log2 domain
+    float qv[R][G::EPL];
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      const int64_t qoff = (qi * p.hq + qh0 + r) * int64_t(p.d);
+#pragma unroll
+      for (int n = 0; n < G::NCH; ++n)
+#pragma unroll
+        for (int e = 0; e < G::CE; ++e) {
+          const int d = (lk + n * G::LPK) * G::CE + e;
+          if (n * G::CE + e < G::EPL)
+            qv[r][n * G::CE + e] = d < p.d ? load_as_float(p.q, qoff + d, p.q_dtype) * p.qscale : 0.f;
+        }
+    }
+
+    // ---- block-table window: lane i holds the page of logical page win+i
+    int win = -1, win_val = 0;
+    auto issue = [&](int c) {
+      const int stage = c % kStages;
+      const int k0 = kb + c * G::CH;
+      const int nvalid = min(G::CH, ke - k0);
+      int row = 0;
+      if (p.bt) {
+        const int plo = k0 >> p.log2ps, phi = (k0 + G::CH - 1) >> p.log2ps;
+        if (win < 0 || plo < win || phi - win >= 32) {  // warp-uniform
+          win = plo;
+          const int idx = plo + lane;
+          win_val = idx < npages_seq ? p.bt[bt_off + idx] : 0;
+        }
+        const int key = k0 + lane;
+        int src = (key >> p.log2ps) - win;
+        src = src < 0 ? 0 : (src > 31 ? 31 : src);
+        const int page = __shfl_sync(0xffffffffu, win_val, src);
+        row = page * ps + (key & (ps - 1));
+      } else {
+        row = static_cast<int>(gstart + k0 + lane);
+      }
+      const uint32_t kdst = wsm_addr + stage * G::STAGE;
+      const uint32_t vdst = kdst + G::CH * G::ROWB;
+      const int total = G::CH * cpr;
+      for (int base = 0; base < total; base += 32) {
+        const int i = base + lane;
+        const int r = cpr_pow2 ? (i >> cpr_sh) : (i / cpr);
+        const int cc = i - r * cpr;
+        const int rrow = __shfl_sync(0xffffffffu, row, r & 31);
+        if (i < total) {
+          const bool ok = r < nvalid;
+          const int64_t goff = ok ? int64_t(rrow) * p.row_stride_bytes + cc * vec : 0;
+          const uint32_t soff = r * G::ROWB + cc * vec;
+          const int nb = ok ? vec : 0;
+          if (vec == 16) {
+            cp_async<16>(kdst + soff, kbase + goff, nb);
+            cp_async<16>(vdst + soff, vbase + goff, nb);
+          } else if (vec == 8) {
+            cp_async<8>(kdst + soff, kbase + goff, nb);
+            cp_async<8>(vdst + soff, vbase + goff, nb);
+          } else {
+            cp_async<4>(kdst + soff, kbase + goff, nb);
+            cp_async<4>(vdst + soff, vbase + goff, nb);
+          }
+        }
+      }
+    };
+
+    float m[R], l[R], acc[R][G::EPL];
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      m[r] = -INFINITY;
+      l[r] = 0.f;
+#pragma unroll
+      for (int e = 0; e < G::EPL; ++e) acc[r][e] = 0.f;
+    }
+
+#pragma unroll
+    for (int c = 0; c < kStages - 1; ++c) {
+      if (c < n_chunks) issue(c);
+      cp_async_commit();
+    }
+    for (int c = 0; c < n_chunks; ++c) {
+      cp_async_wait<kStages - 2>();
+      __syncwarp();
+      if (c + kStages - 1 < n_chunks) issue(c + kStages - 1);
+      cp_async_commit();
+
+      const unsigned char* ks = wsm + (c % kStages) * G::STAGE;
+      const unsigned char* vs = ks + G::CH * G::ROWB;
+      const int k0 = kb + c * G::CH;
+      // scores
+      float s[R][G::KPL];
+#pragma unroll
+      for (int j = 0; j < G::KPL; ++j) {
+        const int key = kg + j * G::KG;
+        float kf[G::EPL];
+#pragma unroll
+        for (int n = 0; n < G::NCH; ++n) {
+          const uint4 ch = *reinterpret_cast<const uint4*>(ks + key * G::ROWB + (lk + n * G::LPK) * 16);
+          Elem<T>::unpack(ch, kf + n * G::CE);
+        }
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+          float a = 0.f;
+#pragma unroll
+          for (int e = 0; e < G::EPL; ++e) a = fmaf(qv[r][e], kf[e], a);
+          s[r][j] = a;
+        }
+      }
+#pragma unroll
+      for (int o = 1; o < G::LPK; o <<= 1)
+#pragma unroll
+        for (int j = 0; j < G::KPL; ++j)
+#pragma unroll
+          for (int r = 0; r < R; ++r) s[r][j] += __shfl_xor_sync(0xffffffffu, s[r][j], o);
+      // mask + online softmax (per lane group)
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        float mx = m[r];
+#pragma unroll
+        for (int j = 0; j < G::KPL; ++j) {
+          if (k0 + kg + j * G::KG >= ke) s[r][j] = -INFINITY;
+          mx = fmaxf(mx, s[r][j]);
+        }
+        if (mx == -INFINITY) {
+#pragma unroll
+          for (int j = 0; j < G::KPL; ++j) s[r][j] = 0.f;
+          continue;
+        }
+        const float corr = exp2f(m[r] - mx);  // m = -inf -> 0
+        float sum = 0.f;
+#pragma unroll
+        for (int j = 0; j < G::KPL; ++j) {
+          s[r][j] = exp2f(s[r][j] - mx);
+          sum += s[r][j];
+        }
+        l[r] = l[r] * corr + sum;
+        m[r] = mx;
+#pragma unroll
+        for (int e = 0; e < G::EPL; ++e) acc[r][e] *= corr;
+      }
+      // P @ V
+#pragma unroll
+      for (int j = 0; j < G::KPL; ++j) {
+        const int key = kg + j * G::KG;
+        float vf[G::EPL];
+#pragma unroll
+        for (int n = 0; n < G::NCH; ++n) {
+          const uint4 ch = *reinterpret_cast<const uint4*>(vs + key * G::ROWB + (lk + n * G::LPK) * 16);
+          Elem<T>::unpack(ch, vf + n * G::CE);
+        }
+#pragma unroll
+        for (int r = 0; r < R; ++r)
+#pragma unroll
+          for (int e = 0; e < G::EPL; ++e) acc[r][e] = fmaf(s[r][j], vf[e], acc[r][e]);
+      }
+    }
+    cp_async_wait<0>();
+    __syncwarp();
+
+    // ---- merge the KG lane-group states
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      float mx = m[r];
+#pragma unroll
+      for (int o = G::LPK; o < 32; o <<= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+      const float wgt = m[r] == -INFINITY ? 0.f : exp2f(m[r] - mx);
+      l[r] *= wgt;
+#pragma unroll
+      for (int e = 0; e < G::EPL; ++e) acc[r][e] *= wgt;
+#pragma unroll
+      for (int o = G::LPK; o < 32; o <<= 1) {
+        l[r] += __shfl_xor_sync(0xffffffffu, l[r], o);
+#pragma unroll
+        for (int e = 0; e < G::EPL; ++e) acc[r][e] += __shfl_xor_sync(0xffffffffu, acc[r][e], o);
+      }
+      m[r] = mx;
+    }
+    if (kg == 0) {
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        const int qh = qh0 + r;
+        if (nsplit == 1) {
+          const float inv = 1.f / l[r];
+          const int64_t ooff = (qi * p.hq + qh) * int64_t(p.d);
+#pragma unroll
+          for (int n = 0; n < G::NCH; ++n)
+#pragma unroll
+            for (int e = 0; e < G::CE; ++e) {
+              const int d = (lk + n * G::LPK) * G::CE + e;
+              if (n * G::CE + e < G::EPL && d < p.d)
+                store_from_float(p.out, ooff + d, p.out_dtype, acc[r][n * G::CE + e] * inv);
+            }
+        } else {
+          const int64_t slot = sg * p.hq + qh;
+          if (lk == 0) {
+            p.ws_ml[2 * slot] = m[r];
+            p.ws_ml[2 * slot + 1] = l[r];
+          }
+          float* o = p.ws_o + slot * p.d;
+#pragma unroll
+          for (int n = 0; n < G::NCH; ++n)
+#pragma unroll
+            for (int e = 0; e < G::CE; ++e) {
+              const int d = (lk + n * G::LPK) * G::CE + e;
+              if (n * G::CE + e < G::EPL && d < p.d) o[d] = acc[r][n * G::CE + e];
+            }
+        }
+      }
+    }
+  }
+}
+
+// K2c: one warp per (query, q-head) with more than one split; splits merged in
+// ascending order (deterministic)
+__global__ void combine_kernel(const int32_t* __restrict__ plan, int64_t nq, int hq, int d,
+                               const float* __restrict__ ws_ml, const float* __restrict__ ws_o,
+                               void* out, int out_dtype) {
+  const int lane = threadIdx.x & 31;
+  const int64_t item = int64_t(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (item >= nq * hq) return;
+  const int64_t qi = item / hq;
+  const int qh = static_cast<int>(item - qi * hq);
+  const int32_t* offsets = plan + 4;
+  const int s0 = offsets[qi], ns = offsets[qi + 1] - s0;
+  if (ns <= 1) return;
+  float mx = -INFINITY;
+  for (int s = 0; s < ns; ++s) mx = fmaxf(mx, ws_ml[2 * ((int64_t(s0) + s) * hq + qh)]);
+  float den = 0.f;
+  for (int s = 0; s < ns; ++s) {
+    const int64_t slot = (int64_t(s0) + s) * hq + qh;
+    den += exp2f(ws_ml[2 * slot] - mx) * ws_ml[2 * slot + 1];
+  }
+  const float inv = 1.f / den;
+  for (int dd = lane; dd < d; dd += 32) {
+    float a = 0.f;
+    for (int s = 0; s < ns; ++s) {
+      const int64_t slot = (int64_t(s0) + s) * hq + qh;
+      a += exp2f(ws_ml[2 * slot] - mx) * ws_o[slot * d + dd];
+    }
+    store_from_float(out, (qi * hq + qh) * int64_t(d) + dd, out_dtype, a * inv);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// dispatch
+// ---------------------------------------------------------------------------
+using DecodeFn = void (*)(DecodeParams);
+
+template <typename T, int R>
+DecodeFn pick_d(int dp) {
+  switch (dp) {
+    case 4: if constexpr (Elem<T>::kBytes == 4) return decode_kernel<T, 4, R>; else return nullptr;
+    case 8: return decode_kernel<T, 8, R>;
+    case 16: return decode_kernel<T, 16, R>;
+    case 32: return decode_kernel<T, 32, R>;
+    case 64: return decode_kernel<T, 64, R>;
+    case 128: return decode_kernel<T, 128, R>;
+    case 256: return decode_kernel<T, 256, R>;
+    default: return nullptr;
+  }
+}
+template <typename T>
+DecodeFn pick_r(int r, int dp) {
+  if (r == 4) return pick_d<T, 4>(dp);
+  if (r == 2) return pick_d<T, 2>(dp);
+  return pick_d<T, 1>(dp);
+}
+template <typename T, int DP, int R>
+int stage_bytes_of() { return Geo<T, DP, R>::STAGE; }
+
+int ring_bytes(int dtype, int dp) {
+  const int s = elem_bytes(dtype);
+  const int rowb = dp * s;
+  int ch = 4096 / rowb;
+  ch = ch > 32 ? 32 : (ch < 4 ? 4 : ch);
+  return kStages * 2 * ch * rowb;
+}
+
+int g_num_sms = 0;
+
+}  // namespace
+
+extern "C" {
+
+int pkv_device_sm_count(int32_t* out) {
+  int dev = 0, n = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess ||
+      cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) {
+    cudaGetLastError();
+    *out = 0;
+    return pkv::fail(PKV_CUDA_ERROR, "no CUDA device visible");
+  }
+  *out = n;
+  return PKV_OK;
+}
+
+int pkv_mirror_apply(int32_t* table, const int32_t* pairs, int64_t n_pairs, void* stream) {
+  if (n_pairs <= 0) return PKV_OK;
+  const int threads = 256;
+  const int64_t blocks = (n_pairs + threads - 1) / threads;
+  mirror_apply_kernel<<<static_cast<unsigned>(blocks < 4096 ? blocks : 4096), threads, 0,
+                        static_cast<cudaStream_t>(stream)>>>(table, pairs, n_pairs);
+  PKV_CHECK_LAUNCH();
+  return PKV_OK;
+}
+
+int pkv_page_zero(void* k_cache, void* v_cache, const int32_t* pages, int64_t n,
+                  int64_t page_bytes, void* stream) {
+  if (n <= 0) return PKV_OK;
+  if (page_bytes & 1) return pkv::fail(PKV_CONFIG_ERROR, "page bytes must be even");
+  page_zero_kernel<<<static_cast<unsigned>(n < 65535 ? n : 65535), 256, 0,
+                     static_cast<cudaStream_t>(stream)>>>(static_cast<char*>(k_cache),
+                                                          static_cast<char*>(v_cache), pages, n,
+                                                          page_bytes);
+  PKV_CHECK_LAUNCH();
+  return PKV_OK;
+}
+
+int pkv_page_copy(void* k_cache, void* v_cache, const int32_t* triples, int64_t n,
+                  int64_t row_bytes, int32_t page_size, void* stream) {
+  if (n <= 0) return PKV_OK;
+  if (row_bytes & 1) return pkv::fail(PKV_CONFIG_ERROR, "row bytes must be even");
+  page_copy_kernel<<<static_cast<unsigned>(n < 65535 ? n : 65535), 256, 0,
+                     static_cast<cudaStream_t>(stream)>>>(static_cast<char*>(k_cache),
+                                                          static_cast<char*>(v_cache), triples, n,
+                                                          row_bytes, page_size);
+  PKV_CHECK_LAUNCH();
+  return PKV_OK;
+}
+
+int pkv_kv_append(const void* k_new, const void* v_new, int64_t n_tok, const int32_t* tok_row,
+                  int32_t tok_row_stride, const int32_t* tok_pos, const int32_t* block_table,
+                  int64_t bt_stride, int32_t page_size, void* k_cache, void* v_cache,
+                  int64_t row_bytes, void* stream) {
+  if (n_tok <= 0) return PKV_OK;
+  if (page_size <= 0 || (page_size & (page_size - 1)))
+    return pkv::fail(PKV_VALUE_ERROR, "page_size must be a power of two");
+  if (row_bytes & 1) return pkv::fail(PKV_CONFIG_ERROR, "row bytes must be even");
+  int threads = static_cast<int>(row_bytes / 16);
+  threads = threads < 32 ? 32 : (threads > 256 ? 256 : ((threads + 31) / 32) * 32);
+  const int64_t blocks = n_tok < 65535 * 4 ? n_tok : 65535 * 4;
+  kv_append_kernel<<<static_cast<unsigned>(blocks), threads, 0, static_cast<cudaStream_t>(stream)>>>(
+      static_cast<const char*>(k_new), static_cast<const char*>(v_new), n_tok, tok_row,
+      tok_row_stride, tok_pos, block_table, bt_stride, __builtin_ctz(page_size),
+      static_cast<char*>(k_cache), static_cast<char*>(v_cache), row_bytes);
+  PKV_CHECK_LAUNCH();
+  return PKV_OK;
+}
+
+int64_t pkv_attention_workspace_bytes(int64_t n_queries, int32_t hq, int32_t head_dim) {
+  const int64_t splits = n_queries + kMaxExtraSplits;
+  auto up = [](int64_t x) { return (x + 255) / 256 * 256; };
+  return up(4 * (4 + n_queries + 1)) + up(4 * splits * hq * 2) + up(4 * splits * hq * head_dim);
+}
+
+int pkv_paged_attention(const pkv_attention_args* a, void* stream_) {
+  if (!a) return pkv::fail(PKV_VALUE_ERROR, "null args");
+  cudaStream_t stream = static_cast<cudaStream_t>(stream_);
+  if (a->n_queries <= 0) return PKV_OK;
+  if (a->hq <= 0 || a->hkv <= 0 || a->hq % a->hkv)
+    return pkv::fail(PKV_SHAPE_MISMATCH, "query heads (%d) must be a multiple of kv heads (%d)",
+                     a->hq, a->hkv);
+  if (a->page_size <= 0 || (a->page_size & (a->page_size - 1)))
+    return pkv::fail(PKV_VALUE_ERROR, "page_size must be a power of two");
+  const int s = elem_bytes(a->kv_dtype);
+  if (a->head_dim <= 0 || a->head_dim > 256 || (a->head_dim * s) % 4)
+    return pkv::fail(PKV_CONFIG_ERROR,
+                     "head_dim %d unsupported (need 1..256 with head_dim*elem_size %% 4 == 0)",
+                     a->head_dim);
+  int dp = 4;
+  while (dp < a->head_dim) dp *= 2;
+  if (dp * s < 16) dp = 16 / s;
+  const int group = a->hq / a->hkv;
+  const int r = group % 4 == 0 ? 4 : (group % 2 == 0 ? 2 : 1);
+  DecodeFn fn = a->kv_dtype == PKV_F32    ? pick_r<float>(r, dp)
+                : a->kv_dtype == PKV_BF16 ? pick_r<__nv_bfloat16>(r, dp)
+                                          : pick_r<__half>(r, dp);
+  if (!fn) return pkv::fail(PKV_CONFIG_ERROR, "no decode kernel for dtype %d head_dim %d",
+                            a->kv_dtype, a->head_dim);
+  if (a->workspace_bytes < pkv_attention_workspace_bytes(a->n_queries, a->hq, a->head_dim))
+    return pkv::fail(PKV_VALUE_ERROR, "workspace too small");
+  if (!g_num_sms) {
+    int32_t n = 0;
+    pkv_device_sm_count(&n);
+    g_num_sms = n > 0 ? n : 148;
+  }
+  const int num_sms = a->num_sms > 0 ? a->num_sms : g_num_sms;
+  const int waves = a->target_waves > 0 ? a->target_waves : 4;
+
+  auto up = [](int64_t x) { return (x + 255) / 256 * 256; };
+  char* ws = static_cast<char*>(a->workspace);
+  int32_t* plan = reinterpret_cast<int32_t*>(ws);
+  const int64_t splits = a->n_queries + kMaxExtraSplits;
+  float* ws_ml = reinterpret_cast<float*>(ws + up(4 * (4 + a->n_queries + 1)));
+  float* ws_o = reinterpret_cast<float*>(reinterpret_cast<char*>(ws_ml) + up(4 * splits * a->hq * 2));
+
+  const int head_items = a->hkv * (group / r);
+  const int log2ps = __builtin_ctz(a->page_size);
+  plan_kernel<<<1, kPlanThreads, 0, stream>>>(a->q_nkeys, a->n_queries, log2ps, head_items,
+                                              int64_t(num_sms) * kWarps * waves, plan);
+  PKV_CHECK_LAUNCH();
+
+  DecodeParams p;
+  p.q = a->q;
+  p.q_dtype = a->q_dtype;
+  p.nq = a->n_queries;
+  p.q_seq = a->q_seq;
+  p.q_nkeys = a->q_nkeys;
+  p.k = static_cast<const char*>(a->k_cache);
+  p.v = static_cast<const char*>(a->v_cache);
+  p.bt = a->block_table;
+  p.bt_stride = a->bt_stride;
+  p.seq_row = a->seq_row;
+  p.seq_start = a->seq_start;
+  p.log2ps = log2ps;
+  p.hq = a->hq;
+  p.hkv = a->hkv;
+  p.d = a->head_dim;
+  p.group = group;
+  p.head_items = head_items;
+  p.row_stride_bytes = int64_t(a->hkv) * a->head_dim * s;
+  p.qscale = a->scale * kLog2e;
+  p.out = a->out;
+  p.out_dtype = a->out_dtype;
+  p.plan = plan;
+  p.ws_ml = ws_ml;
+  p.ws_o = ws_o;
+  const int smem = kWarps * ring_bytes(a->kv_dtype, dp);
+  static bool attr_set[3][9][3] = {};
+  int di = __builtin_ctz(dp), ri = r == 4 ? 2 : (r == 2 ? 1 : 0);
+  if (!attr_set[a->kv_dtype][di][ri]) {
+    cudaFuncSetAttribute(reinterpret_cast<const void*>(fn),
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    attr_set[a->kv_dtype][di][ri] = true;
+  }
+  if (a->prof_start) cudaEventRecord(static_cast<cudaEvent_t>(a->prof_start), stream);
+  fn<<<num_sms, kWarps * 32, smem, stream>>>(p);
+  PKV_CHECK_LAUNCH();
+  if (a->prof_stop) cudaEventRecord(static_cast<cudaEvent_t>(a->prof_stop), stream);
+  const int64_t items = a->n_queries * a->hq;
+  const int per_block = 8;
+  combine_kernel<<<static_cast<unsigned>((items + per_block - 1) / per_block), per_block * 32, 0,
+                   stream>>>(plan, a->n_queries, a->hq, a->head_dim, ws_ml, ws_o, a->out,
+                             a->out_dtype);
+  PKV_CHECK_LAUNCH();
+  return PKV_OK;
+}
+
+}  // extern "C"

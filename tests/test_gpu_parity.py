@@ -1,0 +1,393 @@
+"""Parity of the CUDA path with the oracle / golden reference vectors.
+
+Run on a B200 (`pytest -m gpu`).  Bars (north star): allocator state and K/V
+contents bit-exact; attention within 1e-5 relative (fp32 arithmetic, the
+reference metric verify.py:40-43) and 2e-2 for bf16 outputs.
+"""
+
+import math
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+
+from oracle import OracleMeta, dense_attention_f64, relative_error  # noqa: E402
+from oracle.attention import round_bf16, streaming_attention  # noqa: E402
+from oracle.workloads import scattered_instance  # noqa: E402
+from paper_2506_07311_b200 import (  # noqa: E402
+    AttentionConfig,
+    BatchView,
+    KernelStats,
+    KvStore,
+    MaskMeta,
+    NoAllowedKeys,
+    OutOfRange,
+    PagePool,
+    ShapeMismatch,
+    gathered_attention,
+    paged_attention,
+)
+from replay import as_numpy, replay_store_script  # noqa: E402
+
+pytestmark = pytest.mark.gpu
+
+FP32_TOL = 1e-5
+BF16_TOL = 2e-2
+
+
+def engine_pool(c, p):
+    return PagePool(c, p)
+
+
+def engine_store_factory(dtype=np.float32):
+    def make(pool, h, d):
+        return KvStore(pool, h, d, dtype=dtype)
+    return make
+
+
+# ---- K1 / K0: store scripts bit-exact ------------------------------------------
+
+def test_store_scripts_bit_exact_against_reference(golden_store):
+    metas, arrays = golden_store
+    for i, meta in enumerate(metas):
+        pre = f"s{i + 1}_"
+        pool, store = replay_store_script(meta, arrays, pre, engine_pool, engine_store_factory())
+        assert pool.dump() == meta["final_dump"]
+        assert np.array_equal(as_numpy(store.keys), arrays[pre + "final_keys"])
+        assert np.array_equal(as_numpy(store.values), arrays[pre + "final_values"])
+        for seq, length in meta["gathers"].items():
+            gk, gv = store.gather(seq, length)
+            assert np.array_equal(as_numpy(gk), arrays[f"{pre}gather_{seq}_k"])
+            assert np.array_equal(as_numpy(gv), arrays[f"{pre}gather_{seq}_v"])
+
+
+def test_assign_lands_at_translated_flat_slot():
+    from array import array
+
+    pool = PagePool(16, page_size=4)
+    store = KvStore(pool, 2, 3)
+    pool.reserve("a", 12)
+    pool.table("a").entries[:] = array("I", [7, 2, 9])
+    row_k = np.full((1, 2, 3), 3.5, dtype=np.float32)
+    row_v = np.full((1, 2, 3), -1.25, dtype=np.float32)
+    store.assign("a", [5], row_k, row_v)
+    assert np.array_equal(as_numpy(store.keys[9]), row_k[0])
+    assert np.array_equal(as_numpy(store.values[9]), row_v[0])
+
+
+def test_duplicate_positions_last_write_wins():
+    pool = PagePool(8, page_size=4)
+    store = KvStore(pool, 2, 3)
+    pool.reserve("a", 4)
+    rng = np.random.default_rng(2)
+    k = rng.standard_normal((3, 2, 3)).astype(np.float32)
+    v = rng.standard_normal((3, 2, 3)).astype(np.float32)
+    store.assign("a", np.array([1, 1, 1]), k, v)
+    gk, gv = store.gather("a", 2)
+    assert np.array_equal(as_numpy(gk)[1], k[2]) and np.array_equal(as_numpy(gv)[1], v[2])
+
+
+@pytest.mark.parametrize("dtype", [np.float16, torch.bfloat16])
+def test_half_precision_store_roundtrip(dtype):
+    pool = PagePool(8, page_size=4)
+    store = KvStore(pool, 2, 8, dtype=dtype)
+    pool.reserve("a", 6)
+    rng = np.random.default_rng(9)
+    k = torch.from_numpy(rng.standard_normal((6, 2, 8)).astype(np.float32)).to(store.torch_dtype)
+    v = torch.from_numpy(rng.standard_normal((6, 2, 8)).astype(np.float32)).to(store.torch_dtype)
+    store.assign("a", np.arange(6), k, v)
+    gk, gv = store.gather("a", 6)
+    assert gk.dtype == store.torch_dtype
+    assert torch.equal(gk.cpu(), k) and torch.equal(gv.cpu(), v)
+
+
+def test_fork_cow_isolation_on_device():
+    rng = np.random.default_rng(3)
+    pool = PagePool(64, page_size=64)
+    store = KvStore(pool, 2, 3)
+    pool.reserve("p", 192)
+    k = rng.standard_normal((192, 2, 3)).astype(np.float32)
+    v = rng.standard_normal((192, 2, 3)).astype(np.float32)
+    store.assign("p", np.arange(192), k, v)
+    pool.fork("p", "c", 100)  # 1 shared page + 36 copied slots
+    ck, cv = store.gather("c", 100)
+    assert np.array_equal(as_numpy(ck), k[:100]) and np.array_equal(as_numpy(cv), v[:100])
+    over = rng.standard_normal((1, 2, 3)).astype(np.float32)
+    store.assign("p", [5], over, over)  # shared page -> CoW in the parent
+    store.assign("c", [10], over * 2, over * 2)
+    assert np.array_equal(as_numpy(store.gather("c", 100)[0])[5], k[5])
+    pk = as_numpy(store.gather("p", 192)[0])
+    assert np.array_equal(pk[5], over[0]) and np.array_equal(pk[10], k[10])
+
+
+# ---- K2: attention vs golden reference outputs ------------------------------------
+
+def _engine_case(case):
+    rng = np.random.default_rng(case["seed"])
+    dtype = torch.bfloat16 if case["bf16"] else np.float32
+    inst = scattered_instance(
+        rng, case["lengths"], kv_heads=case["hkv"], q_heads=case["hq"], head_dim=case["d"],
+        page_size=case["page_size"], q_lengths=case["q_lengths"], make_pool=engine_pool,
+        make_store=engine_store_factory(dtype), cast=round_bf16 if case["bf16"] else None)
+    cfg = AttentionConfig(head_count=case["hq"], head_dim=case["d"], causal=case["causal"],
+                          page_size=case["page_size"], kv_head_count=case["hkv"])
+    return inst, cfg
+
+
+def test_attention_matches_golden_reference(golden_attention):
+    index, arrays = golden_attention
+    for case in index:
+        inst, cfg = _engine_case(case)
+        assert inst.pool.dump() == case["pool_dump"], case["name"]
+        view = inst.store.batch_view(inst.seq_ids, inst.lengths)
+        meta = MaskMeta.suffix(view, inst.q_lengths)
+        stats = KernelStats()
+        out = as_numpy(paged_attention(inst.queries, inst.store, meta, cfg, stats=stats))
+        # identical (bf16-rounded where flagged) inputs, fp32 arithmetic
+        assert relative_error(out, arrays[case["name"] + "_ref64"]) <= FP32_TOL, case["name"]
+        assert relative_error(out, arrays[case["name"] + "_out"]) <= FP32_TOL, case["name"]
+        g = case["hq"] // case["hkv"]  # golden GQA stats come from the G-fold
+        assert stats.allowed_pairs * g == case["stats"]["allowed_pairs"], case["name"]
+        if g == 1:
+            assert stats.visited_blocks == case["stats"]["visited_blocks"], case["name"]
+            assert stats.skipped_blocks == case["stats"]["skipped_blocks"], case["name"]
+        if case["bf16"]:
+            outb = paged_attention(torch.from_numpy(inst.queries).bfloat16(), inst.store, meta, cfg,
+                                   out_dtype=torch.bfloat16)
+            assert relative_error(as_numpy(outb), arrays[case["name"] + "_ref64"]) <= BF16_TOL
+
+
+def test_paged_equals_gathered_bitwise():
+    for seed, (lens, hq, hkv, d, ps, causal) in enumerate([
+            ([33, 50, 7], 2, 2, 16, 16, True), ([300, 1, 77], 8, 2, 128, 16, True),
+            ([1000, 513], 4, 4, 64, 64, False)]):
+        rng = np.random.default_rng(seed)
+        inst = scattered_instance(rng, lens, kv_heads=hkv, q_heads=hq, head_dim=d, page_size=ps,
+                                  make_pool=engine_pool, make_store=engine_store_factory())
+        cfg = AttentionConfig(head_count=hq, head_dim=d, causal=causal, page_size=ps, kv_head_count=hkv)
+        view = inst.store.batch_view(inst.seq_ids, inst.lengths)
+        for meta in (MaskMeta.self_attention(view), MaskMeta.decode(view)):
+            q = np.random.default_rng(99).standard_normal((meta.query_count, hq, d)).astype(np.float32)
+            paged = paged_attention(q, inst.store, meta, cfg)
+            gk, gv = inst.store.gather_view(view)
+            gathered = gathered_attention(q, gk, gv, meta, cfg)
+            assert torch.equal(paged, gathered)
+            assert torch.equal(paged, paged_attention(q, inst.store, meta, cfg, skip_empty=False))
+
+
+def _reference_attention_suite_instance(lengths, *, causal=True, page_size=16, heads=2, dim=4,
+                                        seed=0, q_lengths=None):
+    rng = np.random.default_rng(seed)
+    inst = scattered_instance(rng, lengths, kv_heads=heads, head_dim=dim, page_size=page_size,
+                              q_lengths=q_lengths, make_pool=engine_pool,
+                              make_store=engine_store_factory())
+    cfg = AttentionConfig(head_count=heads, head_dim=dim, causal=causal, page_size=page_size)
+    view = inst.store.batch_view(inst.seq_ids, inst.lengths)
+    return inst, cfg, MaskMeta.suffix(view, inst.q_lengths)
+
+
+def test_single_allowed_key_returns_value_row_exactly():
+    inst, cfg, meta = _reference_attention_suite_instance([1], q_lengths=[1])
+    out = as_numpy(paged_attention(inst.queries, inst.store, meta, cfg))
+    assert np.array_equal(out[0], inst.values[0])
+
+
+def test_uniform_scores_average_value_rows():
+    pool = PagePool(8, page_size=4)
+    store = KvStore(pool, 1, 4)
+    pool.reserve("a", 6)
+    k = np.tile(np.array([[0.3, -0.2, 0.9, 0.0]], dtype=np.float32), (6, 1)).reshape(6, 1, 4)
+    v = np.random.default_rng(1).standard_normal((6, 1, 4)).astype(np.float32)
+    store.assign("a", np.arange(6), k, v)
+    view = store.batch_view(["a"])
+    meta = MaskMeta(view=view, q_seq=np.array([0]), q_pos=np.array([5]))
+    cfg = AttentionConfig(head_count=1, head_dim=4, causal=True, page_size=4)
+    q = np.random.default_rng(2).standard_normal((1, 1, 4)).astype(np.float32)
+    out = as_numpy(paged_attention(q, store, meta, cfg))
+    assert np.allclose(out[0, 0], v[:, 0, :].mean(axis=0), atol=1e-6)
+
+
+@pytest.mark.parametrize("page_size", [16, 64, 128])
+@pytest.mark.parametrize("causal", [True, False])
+def test_random_instances_match_reference(page_size, causal):
+    rng = np.random.default_rng(page_size + causal)
+    lengths = [int(rng.integers(1, 300)) for _ in range(4)]
+    inst = scattered_instance(rng, lengths, kv_heads=4, head_dim=16, page_size=page_size,
+                              make_pool=engine_pool, make_store=engine_store_factory())
+    cfg = AttentionConfig(head_count=4, head_dim=16, causal=causal, page_size=page_size)
+    meta = MaskMeta.suffix(inst.store.batch_view(inst.seq_ids, inst.lengths), inst.q_lengths)
+    out = as_numpy(paged_attention(inst.queries, inst.store, meta, cfg))
+    ref = dense_attention_f64(inst.queries, inst.keys, inst.values, inst.lengths, causal=causal,
+                              scale=cfg.scale, q_lengths=inst.q_lengths)
+    assert relative_error(out, ref) <= FP32_TOL
+
+
+def test_causality_zeroing_future_value_changes_nothing():
+    rng = np.random.default_rng(6)
+    pool = PagePool(16, page_size=4)
+    store = KvStore(pool, 2, 4)
+    pool.reserve("a", 10)
+    k = rng.standard_normal((10, 2, 4)).astype(np.float32)
+    v = rng.standard_normal((10, 2, 4)).astype(np.float32)
+    store.assign("a", np.arange(10), k, v)
+    meta = MaskMeta(view=store.batch_view(["a"]), q_seq=np.array([0]), q_pos=np.array([3]))
+    cfg = AttentionConfig(head_count=2, head_dim=4, causal=True, page_size=4)
+    q = rng.standard_normal((1, 2, 4)).astype(np.float32)
+    before = paged_attention(q, store, meta, cfg)
+    store.assign("a", [7], k[7:8], np.zeros((1, 2, 4), dtype=np.float32))
+    after = paged_attention(q, store, meta, cfg)
+    assert torch.equal(before, after)
+
+
+def test_flop_and_block_instrumentation():
+    inst, cfg, meta = _reference_attention_suite_instance([40], seed=3, q_lengths=[1])
+    stats = KernelStats()
+    paged_attention(inst.queries, inst.store, meta, cfg, stats=stats)
+    assert stats.allowed_pairs == 40
+    assert stats.attention_flops == 4 * 2 * 4 * 40
+    assert stats.visited_blocks == 3 and stats.skipped_blocks == 0
+
+
+def test_no_allowed_keys_is_an_error():
+    inst, cfg, meta = _reference_attention_suite_instance([8], q_lengths=[1])
+    meta.view.lengths[0] = 0  # corrupt: every key invalid (reference raises IndexError here)
+    with pytest.raises(NoAllowedKeys):
+        paged_attention(inst.queries, inst.store, meta, cfg)
+
+
+def test_shape_validation():
+    inst, cfg, meta = _reference_attention_suite_instance([8], q_lengths=[2])
+    with pytest.raises(ShapeMismatch):
+        paged_attention(inst.queries[:1], inst.store, meta, cfg)
+    with pytest.raises(ShapeMismatch):
+        gathered_attention(inst.queries, inst.keys[:4], inst.values[:4], meta, cfg)
+
+
+def test_fp16_store_fp32_queries_stay_accurate():
+    rng = np.random.default_rng(13)
+    pool = PagePool(16, page_size=16)
+    store = KvStore(pool, 2, 8, dtype=np.float16)
+    pool.reserve("a", 40)
+    k = rng.standard_normal((40, 2, 8)).astype(np.float16)
+    v = rng.standard_normal((40, 2, 8)).astype(np.float16)
+    store.assign("a", np.arange(40), k, v)
+    meta = MaskMeta.self_attention(store.batch_view(["a"]))
+    cfg = AttentionConfig(head_count=2, head_dim=8, causal=True, page_size=16)
+    q = rng.standard_normal((40, 2, 8)).astype(np.float32)
+    out = paged_attention(q, store, meta, cfg)
+    assert out.dtype == torch.float32
+    ref = dense_attention_f64(q, k, v, [40], causal=True)
+    assert relative_error(as_numpy(out), ref) <= FP32_TOL
+
+
+def test_fault_injection_block_table_corruption_is_detected():
+    """the reference's page-swap fault is invisible to non-causal
+    instances; corrupt one entry to a page with different content on a causal
+    decode and require the output to move."""
+    inst, cfg, meta = _reference_attention_suite_instance([64, 64], page_size=16, heads=2, dim=8,
+                                                          q_lengths=[1, 1], seed=4)
+    good = paged_attention(inst.queries, inst.store, meta, cfg)
+    t0, t1 = inst.pool.table("s0"), inst.pool.table("s1")
+    t0.entries[1] = t1.entries[2]
+    bad = paged_attention(inst.queries, inst.store, meta, cfg)
+    assert not torch.equal(good, bad)
+
+
+# ---- size-independent properties at BASELINE sizes ---------------------------------
+
+def _torch_dense_decode(q, k_rows, v_rows, g):
+    """float64 dense decode reference on the GPU (one sequence)."""
+    qd = q.double()                        # [Hq, D]
+    kd = k_rows.double().repeat_interleave(g, dim=1)  # [L, Hq, D]
+    vd = v_rows.double().repeat_interleave(g, dim=1)
+    s = torch.einsum("hd,lhd->hl", qd, kd) / math.sqrt(q.shape[-1])
+    p = torch.softmax(s, dim=-1)
+    return torch.einsum("hl,lhd->hd", p, vd)
+
+
+@pytest.mark.parametrize("ctx", [2048, 8192, 32768])
+def test_c3_gqa_decode_long_context_bf16(ctx):
+    hq, hkv, d, ps = 32, 8, 128, 16
+    B = 2
+    pool = PagePool(B * (ctx // ps) + 8, page_size=ps)
+    store = KvStore(pool, hkv, d, dtype=torch.bfloat16)
+    gen = torch.Generator(device="cuda").manual_seed(ctx)
+    keys, vals = [], []
+    for b in range(B):
+        pool.reserve(b, ctx)
+        k = torch.randn((ctx, hkv, d), generator=gen, device="cuda").bfloat16()
+        v = torch.randn((ctx, hkv, d), generator=gen, device="cuda").bfloat16()
+        store.assign(b, np.arange(ctx), k, v)
+        keys.append(k)
+        vals.append(v)
+    view = store.batch_view([0, 1])
+    meta = MaskMeta.decode(view)
+    cfg = AttentionConfig(head_count=hq, head_dim=d, page_size=ps, kv_head_count=hkv)
+    q = torch.randn((B, hq, d), generator=gen, device="cuda").bfloat16()
+    out = paged_attention(q, store, meta, cfg)
+    for b in range(B):
+        ref = _torch_dense_decode(q[b], keys[b], vals[b], hq // hkv)
+        assert relative_error(as_numpy(out[b]), ref.cpu().numpy()) <= 1e-4
+    outb = paged_attention(q, store, meta, cfg, out_dtype=torch.bfloat16)
+    assert relative_error(as_numpy(outb), as_numpy(out)) <= BF16_TOL
+
+
+def test_c2_mixed_context_mha_decode_vs_oracle():
+    """BASELINE C2 lengths (seed-0 draw, sum 36,477) on the MHA 32x128 shape,
+    bf16 store; compared with the oracle's dense float64 attention."""
+    from oracle.workloads import config_lengths
+
+    lengths = config_lengths("c2")
+    hq = hkv = 32
+    d, ps = 128, 16
+    pool = PagePool(sum(-(-n // ps) for n in lengths) + 4, page_size=ps)
+    store = KvStore(pool, hkv, d, dtype=torch.bfloat16)
+    rng = np.random.default_rng(0)
+    ks, vs = [], []
+    for i, n in enumerate(lengths):
+        pool.reserve(i, n)
+        k = round_bf16(rng.standard_normal((n, hkv, d)).astype(np.float32))
+        v = round_bf16(rng.standard_normal((n, hkv, d)).astype(np.float32))
+        store.assign(i, np.arange(n), k, v)
+        ks.append(k)
+        vs.append(v)
+    meta = MaskMeta.decode(store.batch_view(list(range(len(lengths)))))
+    cfg = AttentionConfig(head_count=hq, head_dim=d, page_size=ps)
+    q = round_bf16(rng.standard_normal((len(lengths), hq, d)).astype(np.float32))
+    out = as_numpy(paged_attention(q, store, meta, cfg))
+    ref = dense_attention_f64(q, np.concatenate(ks), np.concatenate(vs), lengths, causal=True,
+                              q_lengths=[1] * len(lengths))
+    assert relative_error(out, ref) <= FP32_TOL
+
+
+def test_c1_decode_against_oracle_streaming_kernel():
+    """C1 (B=1, 8x64, ps 16, ctx 512, fp32): engine vs the oracle's restatement
+    of the reference streaming kernel on the same scattered instance."""
+    rng = np.random.default_rng(0)
+    inst = scattered_instance(rng, [512], kv_heads=8, head_dim=64, page_size=16, q_lengths=[1],
+                              make_pool=engine_pool, make_store=engine_store_factory())
+    cfg = AttentionConfig(head_count=8, head_dim=64, page_size=16)
+    meta = MaskMeta.decode(inst.store.batch_view(inst.seq_ids))
+    out = as_numpy(paged_attention(inst.queries, inst.store, meta, cfg))
+    from oracle.store import OracleBatchView
+
+    ometa = OracleMeta.decode(OracleBatchView([512]))
+    want = streaming_attention(inst.queries, inst.keys, inst.values, ometa, scale=cfg.scale,
+                               causal=True, tile=16)
+    assert relative_error(out, want) <= FP32_TOL
+
+
+def test_out_of_range_view_length_rejected():
+    pool = PagePool(8, page_size=4)
+    store = KvStore(pool, 1, 4)
+    pool.reserve("a", 4)
+    store.assign("a", np.arange(4), np.ones((4, 1, 4), np.float32), np.ones((4, 1, 4), np.float32))
+    with pytest.raises(OutOfRange):
+        store.batch_view(["a"], [5])
+    view = BatchView.from_lengths([4], ids=["a"])
+    view.lengths[0] = 9  # beyond capacity
+    cfg = AttentionConfig(head_count=1, head_dim=4, page_size=4, causal=False)
+    meta = MaskMeta(view=view, q_seq=np.array([0]), q_pos=np.array([0]))
+    with pytest.raises(OutOfRange):
+        paged_attention(np.ones((1, 1, 4), np.float32), store, meta, cfg)
