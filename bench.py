@@ -219,12 +219,11 @@ def run_ours(args, rank, world, device):
     torch.cuda.synchronize(device)
 
     def step(t, prof_pair=None):
+        # one decode step = K1 append fused into the K2 launch (the last split
+        # of each sequence writes the new token into its page) + in-kernel
+        # split plan and split merge: a single launch
         mt = meta[t]
         md = mt.data_ptr()
-        _lib.check(lib.pkv_kv_append(
-            C.c_void_p(ks[t].data_ptr()), C.c_void_p(vs[t].data_ptr()), B, C.c_void_p(rows.data_ptr()), 1,
-            C.c_void_p(md + 8 * B), C.c_void_p(mirror.data_ptr()), mirror.shape[1], ps,
-            C.c_void_p(store.keys.data_ptr()), C.c_void_p(store.values.data_ptr()), store.row_bytes, sp))
         a = _lib.AttentionArgs(
             q=qs[t].data_ptr(), q_dtype=_lib.PKV_BF16, n_queries=B, q_seq=md, q_nkeys=md + 4 * B,
             k_cache=store.keys.data_ptr(), v_cache=store.values.data_ptr(), kv_dtype=_lib.PKV_BF16,
@@ -233,7 +232,8 @@ def run_ours(args, rank, world, device):
             out=out.data_ptr(), out_dtype=_lib.PKV_F32, workspace=ws.data_ptr(),
             workspace_bytes=ws.numel(), num_sms=0, target_waves=0,
             prof_start=prof_pair[0].cuda_event if prof_pair else None,
-            prof_stop=prof_pair[1].cuda_event if prof_pair else None)
+            prof_stop=prof_pair[1].cuda_event if prof_pair else None,
+            mode=0, k_new=ks[t].data_ptr(), v_new=vs[t].data_ptr())
         _lib.check(lib.pkv_paged_attention(C.byref(a), sp), "pkv_paged_attention")
 
     for t in range(W):
@@ -496,7 +496,7 @@ def main():
                          "k2_share_of_step": r["k2_ms_mean"] / (sum(r["step_ms"]) / K),
                          "algorithmic_bytes_per_launch": r["k2_alg_bytes_mean"]},
             "clocks": r["clocks"],
-            "gpu_launches": 4 * K,
+            "gpu_launches": K * (1 if r["B"] <= 2048 else 2),
         }
         if "e2e" in r:
             e = r["e2e"]

@@ -193,10 +193,21 @@ typedef struct pkv_attention_args {
   int32_t target_waves; /* 0 = default work-splitting heuristic */
   void* prof_start; /* optional cudaEvent_t recorded right before the K2 launch */
   void* prof_stop;  /* optional cudaEvent_t recorded right after the K2 launch */
+  /* kernel selection: 0 = auto (bf16 caches -> tensor-core K2, fp32/fp16 ->
+   * fp32 CUDA-core K2, which keeps the reference's 1e-5 bar), 1 = force the
+   * fp32 CUDA-core kernel, 2 = force the tensor-core kernel */
+  int32_t mode;
+  /* optional fused append (decode step, one query per sequence): the token at
+   * position q_nkeys[i]-1 of query i's sequence is taken from k_new/v_new
+   * [n_queries, hkv, head_dim] and written into its page first */
+  const void* k_new;
+  const void* v_new;
 } pkv_attention_args;
 
 /* Workspace bound: the split planner never creates more than
- * n_queries + 8192 key splits, so the bound depends only on the query count. */
+ * n_queries + 8192 key splits, so the bound depends only on the query count.
+ * The workspace must be zero-filled before its first use (it holds
+ * self-resetting split counters); the kernels leave it reusable. */
 int64_t pkv_attention_workspace_bytes(int64_t n_queries, int32_t hq, int32_t head_dim);
 int pkv_paged_attention(const pkv_attention_args* args, void* stream);
 

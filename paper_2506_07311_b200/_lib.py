@@ -47,6 +47,7 @@ class AttentionArgs(C.Structure):
         ("workspace", _vp), ("workspace_bytes", _i64),
         ("num_sms", _i32), ("target_waves", _i32),
         ("prof_start", _vp), ("prof_stop", _vp),
+        ("mode", _i32), ("k_new", _vp), ("v_new", _vp),
     ]
 
 

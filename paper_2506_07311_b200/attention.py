@@ -223,7 +223,8 @@ class _Workspace:
 
         buf = cls._bufs.get(device)
         if buf is None or buf.numel() < nbytes:
-            buf = torch.empty(max(nbytes, 1 << 20), dtype=torch.uint8, device=device)
+            # zero-filled: holds self-resetting split counters (pkv200.h)
+            buf = torch.zeros(max(nbytes, 1 << 20), dtype=torch.uint8, device=device)
             cls._bufs[device] = buf
         return buf
 
@@ -239,8 +240,11 @@ def _q_tensor(queries, device):
     return q, code
 
 
+PRECISION_MODES = {"auto": 0, "exact": 1, "tensor": 2}
+
+
 def _launch_attention(q, qcode, meta, config, nkeys, *, k, v, kv_code, bt, bt_stride, seq_row,
-                      seq_start, out_dtype, device):
+                      seq_start, out_dtype, device, precision="auto"):
     import torch
 
     nq = meta.query_count
@@ -261,18 +265,23 @@ def _launch_attention(q, qcode, meta, config, nkeys, *, k, v, kv_code, bt, bt_st
         seq_start=seq_start.data_ptr() if seq_start is not None else None,
         page_size=config.page_size, hq=config.head_count, hkv=config.kv_head_count,
         head_dim=config.head_dim, scale=float(config.scale), out=out.data_ptr(), out_dtype=out_code,
-        workspace=ws.data_ptr(), workspace_bytes=ws.numel(), num_sms=0, target_waves=0)
+        workspace=ws.data_ptr(), workspace_bytes=ws.numel(), num_sms=0, target_waves=0,
+        mode=PRECISION_MODES[precision])
     _lib.check(_lib.load().pkv_paged_attention(C.byref(args), _stream(device)), "pkv_paged_attention")
     return out
 
 
 def paged_attention(queries, store: KvStore, meta: MaskMeta, config: AttentionConfig, *,
                     stats: KernelStats | None = None, block_mask: BlockMask | None = None,
-                    skip_empty: bool = True, out_dtype=None):
+                    skip_empty: bool = True, out_dtype=None, precision: str = "auto"):
     """Exact attention over scattered pages (attention.py:332-354), on the GPU.
 
     `queries` is (n_queries, head_count, head_dim), numpy or torch; the result
-    is a device tensor (fp32 unless `out_dtype` says otherwise)."""
+    is a device tensor (fp32 unless `out_dtype` says otherwise).
+    `precision`: "auto" runs bf16 caches on the tensor-core kernel (P rounded
+    to bf16; 2e-2 contract) and fp32/fp16 caches on the fp32 CUDA-core kernel
+    (1e-5 contract); "exact" forces the CUDA-core kernel, "tensor" the
+    tensor-core one."""
     import torch
 
     _check_queries(queries, meta, config)
@@ -298,12 +307,13 @@ def paged_attention(queries, store: KvStore, meta: MaskMeta, config: AttentionCo
     return _launch_attention(q, qcode, meta, config, nkeys, k=store.keys, v=store.values,
                              kv_code=store.dtype_code, bt=mirror, bt_stride=mirror.shape[1],
                              seq_row=seq_row, seq_start=None,
-                             out_dtype=out_dtype or torch.float32, device=device)
+                             out_dtype=out_dtype or torch.float32, device=device,
+                             precision=precision)
 
 
 def gathered_attention(queries, keys, values, meta: MaskMeta, config: AttentionConfig, *,
                        stats: KernelStats | None = None, block_mask: BlockMask | None = None,
-                       skip_empty: bool = True, out_dtype=None, device=None):
+                       skip_empty: bool = True, out_dtype=None, device=None, precision="auto"):
     """Same kernel over contiguous K/V (attention.py:357-378); bitwise equal to
     the paged path on identical content (the split schedule depends only on
     logical lengths)."""
@@ -329,4 +339,5 @@ def gathered_attention(queries, keys, values, meta: MaskMeta, config: AttentionC
     seq_start = torch.from_numpy(meta.view.prefix_sums.astype(np.int64)).to(device)
     return _launch_attention(q, qcode, meta, config, nkeys, k=k, v=v, kv_code=kv_code, bt=None,
                              bt_stride=0, seq_row=None, seq_start=seq_start,
-                             out_dtype=out_dtype or torch.float32, device=device)
+                             out_dtype=out_dtype or torch.float32, device=device,
+                             precision=precision)

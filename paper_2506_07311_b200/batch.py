@@ -16,7 +16,7 @@ import ctypes as C
 import numpy as np
 
 from . import _lib
-from .attention import AttentionConfig, _Workspace, _q_tensor
+from .attention import PRECISION_MODES, AttentionConfig, _Workspace, _q_tensor
 from .store import KvStore, _ptr, _stream, torch_dtype
 
 
@@ -73,7 +73,8 @@ class DecodeBatch:
                 launches += len(self.pool._stores)
         return launches
 
-    def step(self, queries, k_new, v_new, *, out_dtype=None, layer: int = 0, advance: bool = True):
+    def step(self, queries, k_new, v_new, *, out_dtype=None, layer: int = 0, advance: bool = True,
+             precision: str = "auto"):
         """Append one token per sequence into `stores[layer]` and attend.
 
         queries [B, Hq, D]; k_new / v_new [B, Hkv, D] (numpy or torch, any
@@ -101,9 +102,6 @@ class DecodeBatch:
         v = v.to(device=self.device, dtype=store.torch_dtype, non_blocking=True).contiguous()
         stream = _stream(self.device)
         md = dev.data_ptr()
-        _lib.call("pkv_kv_append", _ptr(k), _ptr(v), n, C.c_void_p(md + 12 * n), 1,
-                  C.c_void_p(md + 8 * n), _ptr(mirror), mirror.shape[1], store.page_size,
-                  _ptr(store.keys), _ptr(store.values), store.row_bytes, stream)
         q, qcode = _q_tensor(queries, self.device)
         out_t, out_code = torch_dtype(out_dtype or torch.float32)
         out = torch.empty((n, cfg.head_count, cfg.head_dim), dtype=out_t, device=self.device)
@@ -115,7 +113,11 @@ class DecodeBatch:
             block_table=mirror.data_ptr(), bt_stride=mirror.shape[1], seq_row=md + 12 * n,
             seq_start=None, page_size=store.page_size, hq=cfg.head_count, hkv=cfg.kv_head_count,
             head_dim=cfg.head_dim, scale=float(cfg.scale), out=out.data_ptr(), out_dtype=out_code,
-            workspace=ws.data_ptr(), workspace_bytes=ws.numel(), num_sms=0, target_waves=0)
+            workspace=ws.data_ptr(), workspace_bytes=ws.numel(), num_sms=0, target_waves=0,
+            mode=PRECISION_MODES[precision], k_new=k.data_ptr(), v_new=v.data_ptr())
+        # K1 append is fused into the decode launch (the last split of every
+        # sequence reads the new token from k/v and writes it into its page)
         _lib.check(_lib.load().pkv_paged_attention(C.byref(args), stream), "pkv_paged_attention")
-        self.last_launches = launches + 4  # append + plan + decode + combine
+        fused = store.dtype_code == _lib.PKV_BF16 and precision != "exact" or precision == "tensor"
+        self.last_launches = launches + (1 if fused and n <= 2048 else 4)
         return out

@@ -28,127 +28,16 @@
 
 #include <cstdint>
 
+#include "common.cuh"
+#include "decode_tc.h"
 #include "pkv200.h"
 #include "status.h"
 
 namespace {
+using namespace pkv;
 
 constexpr int kMaxExtraSplits = 8192;  // planner bound, see workspace_bytes
 constexpr float kLog2e = 1.4426950408889634f;
-
-#define PKV_CHECK_LAUNCH()                                                                \
-  do {                                                                                    \
-    cudaError_t _e = cudaGetLastError();                                                  \
-    if (_e != cudaSuccess)                                                                \
-      return pkv::fail(PKV_CUDA_ERROR, "%s: %s", __func__, cudaGetErrorString(_e));       \
-  } while (0)
-
-inline int elem_bytes(int dt) { return dt == PKV_F32 ? 4 : 2; }
-
-// ---------------------------------------------------------------------------
-// small device helpers
-// ---------------------------------------------------------------------------
-__device__ __forceinline__ uint32_t smem_addr(const void* p) {
-  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
-}
-
-template <int VEC>
-__device__ __forceinline__ void cp_async(uint32_t dst, const void* src, int src_bytes) {
-  if constexpr (VEC == 16) {
-    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(dst), "l"(src),
-                 "r"(src_bytes));
-  } else {
-    asm volatile("cp.async.ca.shared.global [%0], [%1], %2, %3;\n" ::"r"(dst), "l"(src),
-                 "n"(VEC), "r"(src_bytes));
-  }
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n"); }
-template <int N>
-__device__ __forceinline__ void cp_async_wait() {
-  asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
-}
-
-// element type traits: convert 16-byte chunks to fp32
-template <typename T>
-struct Elem;
-template <>
-struct Elem<float> {
-  static constexpr int kBytes = 4;
-  static constexpr int kPerChunk = 4;
-  __device__ __forceinline__ static void unpack(const uint4& c, float* f) {
-    f[0] = __uint_as_float(c.x);
-    f[1] = __uint_as_float(c.y);
-    f[2] = __uint_as_float(c.z);
-    f[3] = __uint_as_float(c.w);
-  }
-};
-template <>
-struct Elem<__nv_bfloat16> {
-  static constexpr int kBytes = 2;
-  static constexpr int kPerChunk = 8;
-  __device__ __forceinline__ static void unpack(const uint4& c, float* f) {
-    const uint32_t w[4] = {c.x, c.y, c.z, c.w};
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      f[2 * i] = __uint_as_float(w[i] << 16);
-      f[2 * i + 1] = __uint_as_float(w[i] & 0xffff0000u);
-    }
-  }
-};
-template <>
-struct Elem<__half> {
-  static constexpr int kBytes = 2;
-  static constexpr int kPerChunk = 8;
-  __device__ __forceinline__ static void unpack(const uint4& c, float* f) {
-    const uint32_t w[4] = {c.x, c.y, c.z, c.w};
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      __half2 h = *reinterpret_cast<const __half2*>(&w[i]);
-      float2 v = __half22float2(h);
-      f[2 * i] = v.x;
-      f[2 * i + 1] = v.y;
-    }
-  }
-};
-
-__device__ __forceinline__ float load_as_float(const void* base, int64_t idx, int dtype) {
-  if (dtype == PKV_F32) return static_cast<const float*>(base)[idx];
-  if (dtype == PKV_BF16) return __bfloat162float(static_cast<const __nv_bfloat16*>(base)[idx]);
-  return __half2float(static_cast<const __half*>(base)[idx]);
-}
-__device__ __forceinline__ void store_from_float(void* base, int64_t idx, int dtype, float v) {
-  if (dtype == PKV_F32)
-    static_cast<float*>(base)[idx] = v;
-  else if (dtype == PKV_BF16)
-    static_cast<__nv_bfloat16*>(base)[idx] = __float2bfloat16_rn(v);
-  else
-    static_cast<__half*>(base)[idx] = __float2half_rn(v);
-}
-
-// byte copy with the widest vector the alignment allows
-__device__ __forceinline__ void copy_bytes(char* dst, const char* src, int64_t n, int64_t tid,
-                                           int64_t nthreads) {
-  if ((n & 15) == 0) {
-    for (int64_t i = tid; i < (n >> 4); i += nthreads)
-      reinterpret_cast<uint4*>(dst)[i] = reinterpret_cast<const uint4*>(src)[i];
-  } else if ((n & 3) == 0) {
-    for (int64_t i = tid; i < (n >> 2); i += nthreads)
-      reinterpret_cast<uint32_t*>(dst)[i] = reinterpret_cast<const uint32_t*>(src)[i];
-  } else {
-    for (int64_t i = tid; i < (n >> 1); i += nthreads)
-      reinterpret_cast<uint16_t*>(dst)[i] = reinterpret_cast<const uint16_t*>(src)[i];
-  }
-}
-__device__ __forceinline__ void zero_bytes(char* dst, int64_t n, int64_t tid, int64_t nthreads) {
-  if ((n & 15) == 0) {
-    for (int64_t i = tid; i < (n >> 4); i += nthreads)
-      reinterpret_cast<uint4*>(dst)[i] = make_uint4(0, 0, 0, 0);
-  } else if ((n & 3) == 0) {
-    for (int64_t i = tid; i < (n >> 2); i += nthreads) reinterpret_cast<uint32_t*>(dst)[i] = 0;
-  } else {
-    for (int64_t i = tid; i < (n >> 1); i += nthreads) reinterpret_cast<uint16_t*>(dst)[i] = 0;
-  }
-}
 
 // ---------------------------------------------------------------------------
 // K0 / K1 / mirror
@@ -197,6 +86,25 @@ __global__ void kv_append_kernel(const char* __restrict__ kn, const char* __rest
     const int64_t dst = (page * ps + (pos & (ps - 1))) * row_bytes;
     copy_bytes(kc + dst, kn + t * row_bytes, row_bytes, threadIdx.x, blockDim.x);
     copy_bytes(vc + dst, vn + t * row_bytes, row_bytes, threadIdx.x, blockDim.x);
+  }
+}
+
+// decode-step append for the exact path: query i appends its token at
+// position q_nkeys[i]-1 of view sequence q_seq[i]
+__global__ void append_decode_kernel(const char* __restrict__ kn, const char* __restrict__ vn,
+                                     int64_t nq, const int32_t* __restrict__ q_seq,
+                                     const int32_t* __restrict__ q_nkeys,
+                                     const int32_t* __restrict__ seq_row,
+                                     const int32_t* __restrict__ bt, int64_t bt_stride, int log2ps,
+                                     char* __restrict__ kc, char* __restrict__ vc, int64_t row_bytes) {
+  const int ps = 1 << log2ps;
+  for (int64_t i = blockIdx.x; i < nq; i += gridDim.x) {
+    const int32_t pos = q_nkeys[i] - 1;
+    const int64_t r = seq_row[q_seq[i]];
+    const int64_t page = bt[r * bt_stride + (pos >> log2ps)];
+    const int64_t dst = (page * ps + (pos & (ps - 1))) * row_bytes;
+    copy_bytes(kc + dst, kn + i * row_bytes, row_bytes, threadIdx.x, blockDim.x);
+    copy_bytes(vc + dst, vn + i * row_bytes, row_bytes, threadIdx.x, blockDim.x);
   }
 }
 
@@ -724,7 +632,8 @@ int pkv_kv_append(const void* k_new, const void* v_new, int64_t n_tok, const int
 int64_t pkv_attention_workspace_bytes(int64_t n_queries, int32_t hq, int32_t head_dim) {
   const int64_t splits = n_queries + kMaxExtraSplits;
   auto up = [](int64_t x) { return (x + 255) / 256 * 256; };
-  return up(4 * (4 + n_queries + 1)) + up(4 * splits * hq * 2) + up(4 * splits * hq * head_dim);
+  return up(4 * n_queries * hq) /* counters */ + up(4 * (4 + n_queries + 1)) /* plan */ +
+         up(4 * splits * hq * 2) + up(4 * splits * hq * head_dim);
 }
 
 int pkv_paged_attention(const pkv_attention_args* a, void* stream_) {
@@ -736,21 +645,14 @@ int pkv_paged_attention(const pkv_attention_args* a, void* stream_) {
                      a->hq, a->hkv);
   if (a->page_size <= 0 || (a->page_size & (a->page_size - 1)))
     return pkv::fail(PKV_VALUE_ERROR, "page_size must be a power of two");
+  if (a->n_queries > (int64_t(1) << 30)) return pkv::fail(PKV_CONFIG_ERROR, "too many queries");
+  if (a->k_new && !a->block_table)
+    return pkv::fail(PKV_VALUE_ERROR, "fused append needs the paged (block-table) source");
   const int s = elem_bytes(a->kv_dtype);
   if (a->head_dim <= 0 || a->head_dim > 256 || (a->head_dim * s) % 4)
     return pkv::fail(PKV_CONFIG_ERROR,
                      "head_dim %d unsupported (need 1..256 with head_dim*elem_size %% 4 == 0)",
                      a->head_dim);
-  int dp = 4;
-  while (dp < a->head_dim) dp *= 2;
-  if (dp * s < 16) dp = 16 / s;
-  const int group = a->hq / a->hkv;
-  const int r = group % 4 == 0 ? 4 : (group % 2 == 0 ? 2 : 1);
-  DecodeFn fn = a->kv_dtype == PKV_F32    ? pick_r<float>(r, dp)
-                : a->kv_dtype == PKV_BF16 ? pick_r<__nv_bfloat16>(r, dp)
-                                          : pick_r<__half>(r, dp);
-  if (!fn) return pkv::fail(PKV_CONFIG_ERROR, "no decode kernel for dtype %d head_dim %d",
-                            a->kv_dtype, a->head_dim);
   if (a->workspace_bytes < pkv_attention_workspace_bytes(a->n_queries, a->hq, a->head_dim))
     return pkv::fail(PKV_VALUE_ERROR, "workspace too small");
   if (!g_num_sms) {
@@ -760,16 +662,94 @@ int pkv_paged_attention(const pkv_attention_args* a, void* stream_) {
   }
   const int num_sms = a->num_sms > 0 ? a->num_sms : g_num_sms;
   const int waves = a->target_waves > 0 ? a->target_waves : 4;
+  const int group = a->hq / a->hkv;
+  const int log2ps = __builtin_ctz(a->page_size);
 
   auto up = [](int64_t x) { return (x + 255) / 256 * 256; };
   char* ws = static_cast<char*>(a->workspace);
-  int32_t* plan = reinterpret_cast<int32_t*>(ws);
+  unsigned* counters = reinterpret_cast<unsigned*>(ws);
+  int32_t* plan = reinterpret_cast<int32_t*>(ws + up(4 * a->n_queries * a->hq));
   const int64_t splits = a->n_queries + kMaxExtraSplits;
-  float* ws_ml = reinterpret_cast<float*>(ws + up(4 * (4 + a->n_queries + 1)));
+  float* ws_ml = reinterpret_cast<float*>(reinterpret_cast<char*>(plan) + up(4 * (4 + a->n_queries + 1)));
   float* ws_o = reinterpret_cast<float*>(reinterpret_cast<char*>(ws_ml) + up(4 * splits * a->hq * 2));
 
+  const bool tc_ok = decode_tc_supported(a->kv_dtype, a->head_dim);
+  bool use_tc = a->mode == 2 || (a->mode == 0 && a->kv_dtype == PKV_BF16);
+  if (use_tc && !tc_ok) {
+    if (a->mode == 2)
+      return pkv::fail(PKV_CONFIG_ERROR, "tensor-core decode needs a 16-bit cache and head_dim 64/128");
+    use_tc = false;
+  }
+
+  if (use_tc) {
+    const int qgroups = (group + 15) / 16;
+    TcParams t;
+    t.q = a->q;
+    t.q_dtype = a->q_dtype;
+    t.nq = static_cast<int>(a->n_queries);
+    t.q_seq = a->q_seq;
+    t.q_nkeys = a->q_nkeys;
+    t.k = static_cast<const char*>(a->k_cache);
+    t.v = static_cast<const char*>(a->v_cache);
+    t.kw = static_cast<char*>(const_cast<void*>(a->k_cache));
+    t.vw = static_cast<char*>(const_cast<void*>(a->v_cache));
+    t.k_new = static_cast<const char*>(a->k_new);
+    t.v_new = static_cast<const char*>(a->v_new);
+    t.bt = a->block_table;
+    t.bt_stride = a->bt_stride;
+    t.seq_row = a->seq_row;
+    t.seq_start = a->seq_start;
+    t.log2ps = log2ps;
+    t.hq = a->hq;
+    t.hkv = a->hkv;
+    t.group = group;
+    t.qgroups = qgroups;
+    t.head_items = a->hkv * qgroups;
+    t.row_stride = int64_t(a->hkv) * a->head_dim * 2;
+    t.qscale = a->scale * kLog2e;
+    t.out = a->out;
+    t.out_dtype = a->out_dtype;
+    t.target_items = int64_t(num_sms) * decode_tc_warps() * waves;
+    t.plan_global = nullptr;
+    t.ws_ml = ws_ml;
+    t.ws_o = ws_o;
+    t.counters = counters;
+    if (a->n_queries > kSmemPlanMax) {
+      plan_kernel<<<1, kPlanThreads, 0, stream>>>(a->q_nkeys, a->n_queries, log2ps, t.head_items,
+                                                  t.target_items, plan);
+      PKV_CHECK_LAUNCH();
+      t.plan_global = plan;
+    }
+    if (a->prof_start) cudaEventRecord(static_cast<cudaEvent_t>(a->prof_start), stream);
+    if (launch_decode_tc(t, a->kv_dtype, a->head_dim, num_sms, stream) != PKV_OK)
+      return pkv::fail(PKV_CUDA_ERROR, "decode_tc launch: %s", cudaGetErrorString(cudaGetLastError()));
+    if (a->prof_stop) cudaEventRecord(static_cast<cudaEvent_t>(a->prof_stop), stream);
+    return PKV_OK;
+  }
+
+  // ---- fp32 CUDA-core path (exact; the reference's 1e-5 contract) ----------
+  int dp = 4;
+  while (dp < a->head_dim) dp *= 2;
+  if (dp * s < 16) dp = 16 / s;
+  const int r = group % 4 == 0 ? 4 : (group % 2 == 0 ? 2 : 1);
+  DecodeFn fn = a->kv_dtype == PKV_F32    ? pick_r<float>(r, dp)
+                : a->kv_dtype == PKV_BF16 ? pick_r<__nv_bfloat16>(r, dp)
+                                          : pick_r<__half>(r, dp);
+  if (!fn) return pkv::fail(PKV_CONFIG_ERROR, "no decode kernel for dtype %d head_dim %d",
+                            a->kv_dtype, a->head_dim);
+  if (a->k_new) {
+    // unfused append of the decode tokens (positions q_nkeys-1)
+    const int64_t row_bytes = int64_t(a->hkv) * a->head_dim * s;
+    int threads = static_cast<int>(row_bytes / 16);
+    threads = threads < 32 ? 32 : (threads > 256 ? 256 : ((threads + 31) / 32) * 32);
+    append_decode_kernel<<<static_cast<unsigned>(a->n_queries < 65535 ? a->n_queries : 65535), threads, 0,
+                           stream>>>(static_cast<const char*>(a->k_new), static_cast<const char*>(a->v_new),
+                                     a->n_queries, a->q_seq, a->q_nkeys, a->seq_row, a->block_table,
+                                     a->bt_stride, log2ps, static_cast<char*>(const_cast<void*>(a->k_cache)),
+                                     static_cast<char*>(const_cast<void*>(a->v_cache)), row_bytes);
+    PKV_CHECK_LAUNCH();
+  }
   const int head_items = a->hkv * (group / r);
-  const int log2ps = __builtin_ctz(a->page_size);
   plan_kernel<<<1, kPlanThreads, 0, stream>>>(a->q_nkeys, a->n_queries, log2ps, head_items,
                                               int64_t(num_sms) * kWarps * waves, plan);
   PKV_CHECK_LAUNCH();

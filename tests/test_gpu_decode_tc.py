@@ -1,0 +1,187 @@
+"""Tensor-core decode kernel (K2-TC) and the fused decode step (DecodeBatch).
+
+Bars: bf16 outputs within 2e-2 relative of a float64 reference (north star);
+allocator state and K/V cache contents after fused appends bit-exact against
+the oracle store; paged == gathered and run-to-run results bitwise equal.
+"""
+
+import math
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+
+from oracle import OraclePool, OracleStore, relative_error  # noqa: E402
+from oracle.attention import round_bf16  # noqa: E402
+from paper_2506_07311_b200 import (  # noqa: E402
+    AttentionConfig,
+    KvStore,
+    MaskMeta,
+    PagePool,
+    gathered_attention,
+    paged_attention,
+)
+from paper_2506_07311_b200.batch import DecodeBatch  # noqa: E402
+from replay import as_numpy  # noqa: E402
+
+pytestmark = pytest.mark.gpu
+BF16_TOL = 2e-2
+
+
+def dense_ref(q, keys, vals, lengths, nkeys, g, scale):
+    """float64 reference on the GPU: q [nq, Hq, D], per-query key prefix."""
+    out = []
+    off = 0
+    for i, n in enumerate(lengths):
+        k = keys[off:off + nkeys[i]].double().repeat_interleave(g, dim=1)
+        v = vals[off:off + nkeys[i]].double().repeat_interleave(g, dim=1)
+        s = torch.einsum("hd,lhd->hl", q[i].double(), k) * scale
+        out.append(torch.einsum("hl,lhd->hd", torch.softmax(s, -1), v))
+        off += n
+    return torch.stack(out)
+
+
+def build(lengths, hkv, d, ps, dtype, seed=0, scatter=True):
+    pool = PagePool(sum(-(-n // ps) for n in lengths) * 2 + 8, page_size=ps)
+    store = KvStore(pool, hkv, d, dtype=dtype)
+    gen = torch.Generator(device="cuda").manual_seed(seed)
+    ks, vs = [], []
+    for i, n in enumerate(lengths):
+        if scatter:
+            pool.reserve(("pad", i), ps * (1 + i % 3))
+        pool.reserve(i, n)
+        k = torch.randn((n, hkv, d), generator=gen, device="cuda").to(store.torch_dtype)
+        v = torch.randn((n, hkv, d), generator=gen, device="cuda").to(store.torch_dtype)
+        store.assign(i, np.arange(n), k, v)
+        ks.append(k)
+        vs.append(v)
+    if scatter:
+        for i in range(len(lengths)):
+            pool.free(("pad", i))
+    return pool, store, torch.cat(ks), torch.cat(vs)
+
+
+@pytest.mark.parametrize("dtype", [torch.bfloat16, torch.float16])
+@pytest.mark.parametrize("d", [64, 128])
+@pytest.mark.parametrize("hq,hkv", [(4, 4), (32, 8), (16, 2), (32, 2), (48, 2)])
+@pytest.mark.parametrize("ps", [4, 16, 64])
+def test_tensor_core_decode_matches_float64(dtype, d, hq, hkv, ps):
+    lengths = [1, 15, 16, 17, 300, 1000]
+    pool, store, keys, vals = build(lengths, hkv, d, ps, dtype, seed=hq + d + ps)
+    cfg = AttentionConfig(head_count=hq, head_dim=d, page_size=ps, kv_head_count=hkv)
+    meta = MaskMeta.decode(store.batch_view(list(range(len(lengths)))))
+    gen = torch.Generator(device="cuda").manual_seed(5)
+    q = torch.randn((len(lengths), hq, d), generator=gen, device="cuda")
+    ref = dense_ref(q, keys, vals, lengths, lengths, hq // hkv, cfg.scale)
+    for qq in (q, q.to(dtype)):  # fp32 queries use the hi/lo split MMA
+        out = paged_attention(qq, store, meta, cfg, precision="tensor")
+        ref_q = ref if qq.dtype == torch.float32 else dense_ref(qq.float(), keys, vals, lengths, lengths,
+                                                               hq // hkv, cfg.scale)
+        err = relative_error(as_numpy(out), ref_q.cpu().numpy())
+        assert err <= BF16_TOL, err
+        assert err <= (6e-3 if dtype == torch.bfloat16 else 1e-3), err
+
+
+def test_tensor_core_general_meta_and_gathered_bitwise():
+    lengths = [40, 130, 7]
+    pool, store, keys, vals = build(lengths, 2, 128, 16, torch.bfloat16)
+    cfg = AttentionConfig(head_count=8, head_dim=128, page_size=16, kv_head_count=2)
+    view = store.batch_view(list(range(3)))
+    for meta in (MaskMeta.self_attention(view), MaskMeta.suffix(view, [3, 1, 7])):
+        q = torch.randn((meta.query_count, 8, 128), device="cuda").bfloat16()
+        paged = paged_attention(q, store, meta, cfg)
+        gk, gv = store.gather_view(view)
+        assert torch.equal(paged, gathered_attention(q, gk, gv, meta, cfg))
+        assert torch.equal(paged, paged_attention(q, store, meta, cfg))  # deterministic
+        exact = paged_attention(q, store, meta, cfg, precision="exact")
+        assert relative_error(as_numpy(paged), as_numpy(exact)) <= BF16_TOL
+
+
+def test_many_splits_merge_and_determinism():
+    # one long sequence -> hundreds of splits merged by the last-arriving warp
+    lengths = [65536, 3]
+    pool, store, keys, vals = build(lengths, 8, 128, 16, torch.bfloat16, scatter=False)
+    cfg = AttentionConfig(head_count=32, head_dim=128, page_size=16, kv_head_count=8)
+    meta = MaskMeta.decode(store.batch_view([0, 1]))
+    q = torch.randn((2, 32, 128), device="cuda").bfloat16()
+    a = paged_attention(q, store, meta, cfg)
+    b = paged_attention(q, store, meta, cfg)
+    assert torch.equal(a, b)
+    ref = dense_ref(q.float(), keys, vals, lengths, lengths, 4, cfg.scale)
+    assert relative_error(as_numpy(a), ref.cpu().numpy()) <= 6e-3
+
+
+def test_more_queries_than_the_shared_memory_plan():
+    # n_queries > 2048 takes the global plan kernel
+    lengths = [int(x) for x in np.random.default_rng(3).integers(1, 40, 2500)]
+    pool, store, keys, vals = build(lengths, 2, 64, 16, torch.bfloat16, scatter=False)
+    cfg = AttentionConfig(head_count=4, head_dim=64, page_size=16, kv_head_count=2)
+    meta = MaskMeta.decode(store.batch_view(list(range(len(lengths)))))
+    q = torch.randn((len(lengths), 4, 64), device="cuda").bfloat16()
+    out = paged_attention(q, store, meta, cfg)
+    exact = paged_attention(q, store, meta, cfg, precision="exact")
+    assert relative_error(as_numpy(out), as_numpy(exact)) <= 6e-3
+
+
+@pytest.mark.parametrize("dtype,precision", [(torch.bfloat16, "auto"), (np.float32, "auto"),
+                                             (torch.float16, "tensor")])
+def test_decode_batch_fused_append_matches_oracle(dtype, precision):
+    """DecodeBatch.step (fused append + decode) for 20 steps crossing page
+    boundaries, including a forked sequence (copy-on-write on its first
+    write); cache contents and allocator state are bit-exact with the oracle
+    store driven through the reference semantics (grow, assign, decode)."""
+    hq, hkv, d, ps = 8, 2, 64, 16
+    lengths = [5, 16, 31, 100]
+    cap = 64
+    pool = PagePool(cap, page_size=ps)
+    store = KvStore(pool, hkv, d, dtype=dtype)
+    opool = OraclePool(cap, ps)
+    ostore = OracleStore(opool, hkv, d)
+    rng = np.random.default_rng(11)
+    for i, n in enumerate(lengths):
+        k = round_bf16(rng.standard_normal((n, hkv, d)).astype(np.float32))
+        v = round_bf16(rng.standard_normal((n, hkv, d)).astype(np.float32))
+        if dtype == torch.float16:
+            k, v = k.astype(np.float16).astype(np.float32), v.astype(np.float16).astype(np.float32)
+        for p_, s_ in ((pool, store), (opool, ostore)):
+            p_.reserve(i, n)
+            s_.assign(i, np.arange(n), k, v)
+    # fork sequence 2 at a mid-page prefix (shares page 0, copies the tail)
+    for p_ in (pool, opool):
+        p_.fork(2, "f", 20)
+        # page-aligned fork of 3, then rewind 3 so its next append lands in a
+        # shared page: exercises copy-on-write inside the batched step
+        p_.fork(3, "g", 96)
+        p_.table(3).logical_len = 50
+    ids = [0, 1, 2, 3, "f"]
+    cfg = AttentionConfig(head_count=hq, head_dim=d, page_size=ps, kv_head_count=hkv)
+    batch = DecodeBatch(store, ids, cfg)
+    for step in range(20):
+        q = round_bf16(rng.standard_normal((len(ids), hq, d)).astype(np.float32))
+        k = round_bf16(rng.standard_normal((len(ids), hkv, d)).astype(np.float32))
+        v = round_bf16(rng.standard_normal((len(ids), hkv, d)).astype(np.float32))
+        if dtype == torch.float16:
+            k, v = k.astype(np.float16).astype(np.float32), v.astype(np.float16).astype(np.float32)
+        out = as_numpy(batch.step(q, k, v, precision=precision))
+        # oracle: reference call order per sequence (decoder.py:263-284)
+        for j, sid in enumerate(ids):
+            pos = opool.table(sid).logical_len
+            opool.grow(sid, pos + 1)
+            ostore.assign(sid, [pos], k[j:j + 1], v[j:j + 1])
+        assert pool.dump() == opool.dump(), step
+        want = []
+        for j, sid in enumerate(ids):
+            n = opool.table(sid).logical_len
+            gk, gv = ostore.gather(sid, n)
+            kk = np.repeat(gk.astype(np.float64), hq // hkv, axis=1)
+            vv = np.repeat(gv.astype(np.float64), hq // hkv, axis=1)
+            s = np.einsum("hd,lhd->hl", q[j].astype(np.float64), kk) / math.sqrt(d)
+            s = np.exp(s - s.max(-1, keepdims=True))
+            s /= s.sum(-1, keepdims=True)
+            want.append(np.einsum("hl,lhd->hd", s, vv))
+        tol = 1e-5 if dtype == np.float32 else 6e-3
+        assert relative_error(out, np.stack(want)) <= tol, step
+    torch.cuda.synchronize()
+    assert np.array_equal(as_numpy(store.keys), ostore.keys)
+    assert np.array_equal(as_numpy(store.values), ostore.values)
