@@ -56,6 +56,7 @@ def parse():
     ap.add_argument("--sweep", action="store_true", help="also print a C3 context sweep (stderr)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--waves", type=int, default=0, help="split planner target waves (0 = default)")
     return ap.parse_args()
 
 
@@ -209,8 +210,19 @@ def run_ours(args, rank, world, device):
     out = torch.empty((B, hq, d), dtype=torch.float32, device=device)
     ws_bytes = lib.pkv_attention_workspace_bytes(B, hq, d)
     ws = _Workspace.get(device, ws_bytes)
+    cnt = _Workspace.counters(device, B * hq)
     l2_bytes = torch.cuda.get_device_properties(device).L2_cache_size
-    flush = torch.empty(max(2 * l2_bytes, 256 << 20), dtype=torch.uint8, device=device)
+    # L2 flush between steps: *read* 2x L2 of unrelated data, so the next
+    # step starts with a cold, clean L2 (a write flush would leave dirty lines
+    # whose write-back steals HBM bandwidth from the timed kernel)
+    flush_buf = torch.ones(max(2 * l2_bytes, 256 << 20) // 4, dtype=torch.float32, device=device)
+
+    class _Flush:
+        @staticmethod
+        def zero_():
+            flush_buf.sum()
+
+    flush = _Flush()
     stream = torch.cuda.current_stream(device)
     sp = C.c_void_p(stream.cuda_stream)
     prof = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(K)]
@@ -218,23 +230,33 @@ def run_ours(args, rank, world, device):
         a.record(); b_.record()
     torch.cuda.synchronize(device)
 
-    def step(t, prof_pair=None):
+    def make_args(t, prof_pair=None):
         # one decode step = K1 append fused into the K2 launch (the last split
         # of each sequence writes the new token into its page) + in-kernel
         # split plan and split merge: a single launch
         mt = meta[t]
         md = mt.data_ptr()
-        a = _lib.AttentionArgs(
+        return _lib.AttentionArgs(
             q=qs[t].data_ptr(), q_dtype=_lib.PKV_BF16, n_queries=B, q_seq=md, q_nkeys=md + 4 * B,
             k_cache=store.keys.data_ptr(), v_cache=store.values.data_ptr(), kv_dtype=_lib.PKV_BF16,
             block_table=mirror.data_ptr(), bt_stride=mirror.shape[1], seq_row=rows.data_ptr(),
             seq_start=None, page_size=ps, hq=hq, hkv=hkv, head_dim=d, scale=cfg.scale,
             out=out.data_ptr(), out_dtype=_lib.PKV_F32, workspace=ws.data_ptr(),
-            workspace_bytes=ws.numel(), num_sms=0, target_waves=0,
+            workspace_bytes=ws.numel(), num_sms=0, target_waves=args.waves,
             prof_start=prof_pair[0].cuda_event if prof_pair else None,
             prof_stop=prof_pair[1].cuda_event if prof_pair else None,
-            mode=0, k_new=ks[t].data_ptr(), v_new=vs[t].data_ptr())
-        _lib.check(lib.pkv_paged_attention(C.byref(a), sp), "pkv_paged_attention")
+            mode=0, k_new=ks[t].data_ptr(), v_new=vs[t].data_ptr(),
+            counters=cnt.data_ptr(), counters_len=cnt.numel())
+
+    # argument blocks are built before the timed region so the host only
+    # pays one C call per step (keeps host latency out of the device timing)
+    step_args = [make_args(t, prof[t - W] if t >= W else None) for t in range(total_steps)]
+    fn = lib.pkv_paged_attention
+
+    def step(t, prof_pair=None):
+        st = fn(C.byref(step_args[t]), sp)
+        if st:
+            _lib.check(st, "pkv_paged_attention")
 
     for t in range(W):
         flush.zero_()
@@ -486,7 +508,7 @@ def main():
             "vs_baseline": None, "dtype": "bf16", "data": "synthetic (randn K/V/Q, scattered pages)",
             "config": {"workload": r["name"], "global_batch": int(r["tokens_all"] / K),
                        "kv_bytes_per_step": r["kv_all"] / K, "page_size": r["shape"][3],
-                       "parallelism": f"request-sharded x{world}", "l2": "flushed between steps (2x L2 write)"},
+                       "parallelism": f"request-sharded x{world}", "l2": "flushed between steps (read of 2x L2 of unrelated data)"},
             "pct_of_8TBs": round(100 * value / world / NOMINAL_HBM_GBS, 2),
             "tokens_per_s": r["tokens_all"] / (r["total_ms_max"] / 1e3),
             "roofline": {"bound": "hbm", "kernel": "decode_kernel (K2)", "achieved": round(k2_achieved, 1),

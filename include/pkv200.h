@@ -202,12 +202,16 @@ typedef struct pkv_attention_args {
    * [n_queries, hkv, head_dim] and written into its page first */
   const void* k_new;
   const void* v_new;
+  /* scheduler counters: a zero-filled uint32 array of at least
+   * 2 + n_queries * hq entries (work cursor, finished warps, split-merge
+   * counters), used for nothing else; every launch leaves it zeroed again
+   * (required by the tensor-core kernel) */
+  uint32_t* counters;
+  int64_t counters_len;
 } pkv_attention_args;
 
 /* Workspace bound: the split planner never creates more than
- * n_queries + 8192 key splits, so the bound depends only on the query count.
- * The workspace must be zero-filled before its first use (it holds
- * self-resetting split counters); the kernels leave it reusable. */
+ * n_queries + 8192 key splits, so the bound depends only on the query count. */
 int64_t pkv_attention_workspace_bytes(int64_t n_queries, int32_t hq, int32_t head_dim);
 int pkv_paged_attention(const pkv_attention_args* args, void* stream);
 
@@ -243,6 +247,12 @@ int pkv_paged_prefill(const pkv_prefill_args* args, void* stream);
 
 /* number of SMs of the current device (0 when no device is visible) */
 int pkv_device_sm_count(int32_t* out);
+
+/* Debug: per-CTA globaltimer timeline of the tensor-core decode kernel
+ * (64 stamps per CTA).  enable = 1/0 switches recording on/off and clears the
+ * buffer (-1 leaves it); out (n entries, may be NULL) receives the stamps.
+ * Synchronous. */
+int pkv_debug_trace(int32_t enable, uint64_t* out, int64_t n);
 
 #ifdef __cplusplus
 }

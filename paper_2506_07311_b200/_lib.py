@@ -48,6 +48,7 @@ class AttentionArgs(C.Structure):
         ("num_sms", _i32), ("target_waves", _i32),
         ("prof_start", _vp), ("prof_stop", _vp),
         ("mode", _i32), ("k_new", _vp), ("v_new", _vp),
+        ("counters", _vp), ("counters_len", _i64),
     ]
 
 
@@ -99,6 +100,7 @@ SIGNATURES = {
     "pkv_prefill_supported": (C.c_int, [_i32, _i32, _i32, _i32, _i32]),
     "pkv_paged_prefill": (C.c_int, [_P(PrefillArgs), _vp]),
     "pkv_device_sm_count": (C.c_int, [_P(_i32)]),
+    "pkv_debug_trace": (C.c_int, [_i32, _P(_u64), _i64]),
 }
 
 _lib = None

@@ -213,9 +213,11 @@ def _check_queries(queries, meta: MaskMeta, config: AttentionConfig):
 
 
 class _Workspace:
-    """Per-device scratch for split partials and the device split plan."""
+    """Per-device scratch for split partials and the device split plan, plus
+    the zero-filled split-merge counters (pkv200.h: used for nothing else)."""
 
     _bufs: dict = {}
+    _counters: dict = {}
 
     @classmethod
     def get(cls, device, nbytes: int):
@@ -223,9 +225,19 @@ class _Workspace:
 
         buf = cls._bufs.get(device)
         if buf is None or buf.numel() < nbytes:
-            # zero-filled: holds self-resetting split counters (pkv200.h)
-            buf = torch.zeros(max(nbytes, 1 << 20), dtype=torch.uint8, device=device)
+            buf = torch.empty(max(nbytes, 1 << 20), dtype=torch.uint8, device=device)
             cls._bufs[device] = buf
+        return buf
+
+    @classmethod
+    def counters(cls, device, n: int):
+        import torch
+
+        n = n + 2  # work cursor + finished-warp count precede the merge counters
+        buf = cls._counters.get(device)
+        if buf is None or buf.numel() < n:
+            buf = torch.zeros(max(n, 1 << 16), dtype=torch.int32, device=device)
+            cls._counters[device] = buf
         return buf
 
 
@@ -256,6 +268,7 @@ def _launch_attention(q, qcode, meta, config, nkeys, *, k, v, kv_code, bt, bt_st
     meta_dev = torch.from_numpy(meta_host).to(device)
     ws_bytes = _lib.load().pkv_attention_workspace_bytes(nq, config.head_count, config.head_dim)
     ws = _Workspace.get(device, ws_bytes)
+    cnt = _Workspace.counters(device, nq * config.head_count)
     args = _lib.AttentionArgs(
         q=q.data_ptr(), q_dtype=qcode, n_queries=nq,
         q_seq=meta_dev.data_ptr(), q_nkeys=meta_dev.data_ptr() + 4 * nq,
@@ -266,7 +279,7 @@ def _launch_attention(q, qcode, meta, config, nkeys, *, k, v, kv_code, bt, bt_st
         page_size=config.page_size, hq=config.head_count, hkv=config.kv_head_count,
         head_dim=config.head_dim, scale=float(config.scale), out=out.data_ptr(), out_dtype=out_code,
         workspace=ws.data_ptr(), workspace_bytes=ws.numel(), num_sms=0, target_waves=0,
-        mode=PRECISION_MODES[precision])
+        mode=PRECISION_MODES[precision], counters=cnt.data_ptr(), counters_len=cnt.numel())
     _lib.check(_lib.load().pkv_paged_attention(C.byref(args), _stream(device)), "pkv_paged_attention")
     return out
 

@@ -107,6 +107,7 @@ class DecodeBatch:
         out = torch.empty((n, cfg.head_count, cfg.head_dim), dtype=out_t, device=self.device)
         ws_bytes = _lib.load().pkv_attention_workspace_bytes(n, cfg.head_count, cfg.head_dim)
         ws = _Workspace.get(self.device, ws_bytes)
+        cnt = _Workspace.counters(self.device, n * cfg.head_count)
         args = _lib.AttentionArgs(
             q=q.data_ptr(), q_dtype=qcode, n_queries=n, q_seq=md, q_nkeys=md + 4 * n,
             k_cache=store.keys.data_ptr(), v_cache=store.values.data_ptr(), kv_dtype=store.dtype_code,
@@ -114,7 +115,8 @@ class DecodeBatch:
             seq_start=None, page_size=store.page_size, hq=cfg.head_count, hkv=cfg.kv_head_count,
             head_dim=cfg.head_dim, scale=float(cfg.scale), out=out.data_ptr(), out_dtype=out_code,
             workspace=ws.data_ptr(), workspace_bytes=ws.numel(), num_sms=0, target_waves=0,
-            mode=PRECISION_MODES[precision], k_new=k.data_ptr(), v_new=v.data_ptr())
+            mode=PRECISION_MODES[precision], k_new=k.data_ptr(), v_new=v.data_ptr(),
+            counters=cnt.data_ptr(), counters_len=cnt.numel())
         # K1 append is fused into the decode launch (the last split of every
         # sequence reads the new token from k/v and writes it into its page)
         _lib.check(_lib.load().pkv_paged_attention(C.byref(args), stream), "pkv_paged_attention")

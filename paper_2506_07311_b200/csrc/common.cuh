@@ -175,6 +175,26 @@ __device__ __forceinline__ uint32_t pack2<__half>(float lo, float hi) {
   __half2 v = __floats2half2_rn(lo, hi);
   return *reinterpret_cast<uint32_t*>(&v);
 }
+// sum of the two 16-bit lanes of a packed register, as fp32
+template <typename T>
+__device__ __forceinline__ float unpack_sum(uint32_t v);
+template <>
+__device__ __forceinline__ float unpack_sum<__nv_bfloat16>(uint32_t v) {
+  return __uint_as_float(v << 16) + __uint_as_float(v & 0xffff0000u);
+}
+template <>
+__device__ __forceinline__ float unpack_sum<__half>(uint32_t v) {
+  const float2 f = __half22float2(*reinterpret_cast<const __half2*>(&v));
+  return f.x + f.y;
+}
+
+// wrapping increment with acquire-release semantics at GPU scope
+__device__ __forceinline__ unsigned atom_inc_acq_rel(unsigned* addr, unsigned wrap) {
+  unsigned old;
+  asm volatile("atom.acq_rel.gpu.global.inc.u32 %0, [%1], %2;\n" : "=r"(old) : "l"(addr), "r"(wrap) : "memory");
+  return old;
+}
+
 template <typename T>
 __device__ __forceinline__ float round_to(float x);
 template <>

@@ -7,7 +7,7 @@
 
 namespace pkv {
 
-constexpr int kSmemPlanMax = 2048;        // queries planned in shared memory
+constexpr int kSmemPlanMax = 512;         // queries planned in shared memory
 constexpr int kMaxExtraSplitsTc = 8192;   // same bound as the CUDA-core path
 
 struct TcParams {
@@ -32,19 +32,25 @@ struct TcParams {
   float qscale;        // scale * log2(e)
   void* out;
   int out_dtype;
-  const int32_t* plan_global;  // non-null when nq > kSmemPlanMax
+  const int32_t* plan_global;  // global plan buffer, used when nq > kSmemPlanMax
+  void* plan_scratch;          // int64 sort scratch for the global plan
   int64_t target_items;
   float* ws_ml;
   float* ws_o;
-  unsigned* counters;  // [nq * head_items], zero-initialised, self-resetting
+  // [0] work cursor, [1] finished warps, [2 + q*head_items + hi] split merge;
+  // zero-initialised and left zeroed by every launch
+  unsigned* counters;
   int ring_offset;
+  int merge_offset;
+  int kv_dtype;
 };
 
 using TcFn = void (*)(TcParams);
 
 bool decode_tc_supported(int kv_dtype, int head_dim);
-int decode_tc_smem_bytes(int head_dim, int64_t nq);
+int64_t decode_tc_plan_bytes(int64_t nq);  // global plan + sort scratch
 int launch_decode_tc(TcParams p, int kv_dtype, int head_dim, int num_sms, cudaStream_t stream);
 int decode_tc_warps();
+int debug_trace(int enable, uint64_t* out, int64_t n);
 
 }  // namespace pkv

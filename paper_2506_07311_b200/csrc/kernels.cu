@@ -26,6 +26,7 @@
 #include <cuda_fp16.h>
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstdint>
 
 #include "common.cuh"
@@ -632,8 +633,8 @@ int pkv_kv_append(const void* k_new, const void* v_new, int64_t n_tok, const int
 int64_t pkv_attention_workspace_bytes(int64_t n_queries, int32_t hq, int32_t head_dim) {
   const int64_t splits = n_queries + kMaxExtraSplits;
   auto up = [](int64_t x) { return (x + 255) / 256 * 256; };
-  return up(4 * n_queries * hq) /* counters */ + up(4 * (4 + n_queries + 1)) /* plan */ +
-         up(4 * splits * hq * 2) + up(4 * splits * hq * head_dim);
+  const int64_t plan = std::max<int64_t>(4 * (4 + n_queries + 1), decode_tc_plan_bytes(n_queries));
+  return up(plan) + up(4 * splits * hq * 2) + up(4 * splits * hq * head_dim);
 }
 
 int pkv_paged_attention(const pkv_attention_args* a, void* stream_) {
@@ -667,10 +668,11 @@ int pkv_paged_attention(const pkv_attention_args* a, void* stream_) {
 
   auto up = [](int64_t x) { return (x + 255) / 256 * 256; };
   char* ws = static_cast<char*>(a->workspace);
-  unsigned* counters = reinterpret_cast<unsigned*>(ws);
-  int32_t* plan = reinterpret_cast<int32_t*>(ws + up(4 * a->n_queries * a->hq));
+  unsigned* counters = a->counters;
+  int32_t* plan = reinterpret_cast<int32_t*>(ws);
   const int64_t splits = a->n_queries + kMaxExtraSplits;
-  float* ws_ml = reinterpret_cast<float*>(reinterpret_cast<char*>(plan) + up(4 * (4 + a->n_queries + 1)));
+  const int64_t plan_bytes = std::max<int64_t>(4 * (4 + a->n_queries + 1), decode_tc_plan_bytes(a->n_queries));
+  float* ws_ml = reinterpret_cast<float*>(reinterpret_cast<char*>(plan) + up(plan_bytes));
   float* ws_o = reinterpret_cast<float*>(reinterpret_cast<char*>(ws_ml) + up(4 * splits * a->hq * 2));
 
   const bool tc_ok = decode_tc_supported(a->kv_dtype, a->head_dim);
@@ -682,6 +684,8 @@ int pkv_paged_attention(const pkv_attention_args* a, void* stream_) {
   }
 
   if (use_tc) {
+    if (!a->counters || a->counters_len < 2 + a->n_queries * a->hq)
+      return pkv::fail(PKV_VALUE_ERROR, "tensor-core decode needs a zeroed counters array of 2 + n_queries*hq");
     const int qgroups = (group + 15) / 16;
     TcParams t;
     t.q = a->q;
@@ -709,20 +713,15 @@ int pkv_paged_attention(const pkv_attention_args* a, void* stream_) {
     t.qscale = a->scale * kLog2e;
     t.out = a->out;
     t.out_dtype = a->out_dtype;
-    t.target_items = int64_t(num_sms) * decode_tc_warps() * waves;
-    t.plan_global = nullptr;
+    t.target_items = int64_t(num_sms) * waves;  // CTA-sized items
+    t.plan_global = plan;                        // used only when nq > kSmemPlanMax
+    t.plan_scratch = reinterpret_cast<char*>(plan) + up(4 * (4 + 6 * a->n_queries + 2));
     t.ws_ml = ws_ml;
     t.ws_o = ws_o;
     t.counters = counters;
-    if (a->n_queries > kSmemPlanMax) {
-      plan_kernel<<<1, kPlanThreads, 0, stream>>>(a->q_nkeys, a->n_queries, log2ps, t.head_items,
-                                                  t.target_items, plan);
-      PKV_CHECK_LAUNCH();
-      t.plan_global = plan;
-    }
     if (a->prof_start) cudaEventRecord(static_cast<cudaEvent_t>(a->prof_start), stream);
-    if (launch_decode_tc(t, a->kv_dtype, a->head_dim, num_sms, stream) != PKV_OK)
-      return pkv::fail(PKV_CUDA_ERROR, "decode_tc launch: %s", cudaGetErrorString(cudaGetLastError()));
+    const int st = launch_decode_tc(t, a->kv_dtype, a->head_dim, num_sms, stream);
+    if (st != PKV_OK) return st;
     if (a->prof_stop) cudaEventRecord(static_cast<cudaEvent_t>(a->prof_stop), stream);
     return PKV_OK;
   }
@@ -801,3 +800,7 @@ int pkv_paged_attention(const pkv_attention_args* a, void* stream_) {
 }
 
 }  // extern "C"
+
+extern "C" int pkv_debug_trace(int32_t enable, uint64_t* out, int64_t n) {
+  return pkv::debug_trace(enable, out, n);
+}
