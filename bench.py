@@ -57,6 +57,7 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--waves", type=int, default=0, help="split planner target waves (0 = default)")
+    ap.add_argument("--heads", default="", help="experiment: override query:kv heads, e.g. 32:32")
     return ap.parse_args()
 
 
@@ -79,6 +80,9 @@ def workload(args, rank: int, world: int):
         lengths = config_lengths("c2")
         name = "C2 LLaMA-7B MHA 32x128 bf16 decode, batch 32, mixed contexts 128-2048 (seed 0), page 16"
     hq, hkv, d, ps, _ = CONFIG_SHAPES[args.config]
+    if args.heads:  # experiment override "HQ:HKV" (not a BASELINE config)
+        hq, hkv = (int(x) for x in args.heads.split(":"))
+        name += f" [heads overridden to {hq}q/{hkv}kv]"
     return name, lengths, hq, hkv, d, ps
 
 
@@ -198,19 +202,25 @@ def run_ours(args, rank, world, device):
     for b, n in enumerate(lengths):
         pool.grow(b, n + total_steps)
     mirror = pool.device_table(device)
-    rows = torch.tensor([pool.table(b).mirror_row for b in range(B)], dtype=torch.int32, device=device)
+    rows_np = np.asarray([pool.table(b).mirror_row for b in range(B)], dtype=np.int32)
     base = np.asarray(lengths, dtype=np.int32)
     gen = torch.Generator(device=device).manual_seed(1234 + rank)
     qs = torch.randn((total_steps, B, hq, d), generator=gen, device=device, dtype=torch.bfloat16)
     ks = torch.randn((total_steps, B, hkv, d), generator=gen, device=device, dtype=torch.bfloat16)
     vs = torch.randn((total_steps, B, hkv, d), generator=gen, device=device, dtype=torch.bfloat16)
-    # per-step metadata (positions / key counts grow by one per step)
-    meta = torch.from_numpy(np.stack([np.concatenate([np.arange(B, dtype=np.int32), base + t + 1, base + t])
-                                      for t in range(total_steps)])).to(device)
+    # per-step metadata [q_seq | key counts | mirror rows | host work plan];
+    # key counts grow by one per step (the appended token is attended)
+    plans = [_lib.attention_plan(base + t + 1, rows_np, ps, hq, hkv, args.waves)
+             for t in range(total_steps)]
+    width = 3 * B + max(pl.size for pl in plans)
+    meta_np = np.zeros((total_steps, width), dtype=np.int32)
+    for t in range(total_steps):
+        row_t = np.concatenate([np.arange(B, dtype=np.int32), base + t + 1, rows_np, plans[t]])
+        meta_np[t, :row_t.size] = row_t
+    meta = torch.from_numpy(meta_np).to(device)
     out = torch.empty((B, hq, d), dtype=torch.float32, device=device)
     ws_bytes = lib.pkv_attention_workspace_bytes(B, hq, d)
     ws = _Workspace.get(device, ws_bytes)
-    cnt = _Workspace.counters(device, B * hq)
     l2_bytes = torch.cuda.get_device_properties(device).L2_cache_size
     # L2 flush between steps: *read* 2x L2 of unrelated data, so the next
     # step starts with a cold, clean L2 (a write flush would leave dirty lines
@@ -232,21 +242,21 @@ def run_ours(args, rank, world, device):
 
     def make_args(t, prof_pair=None):
         # one decode step = K1 append fused into the K2 launch (the last split
-        # of each sequence writes the new token into its page) + in-kernel
-        # split plan and split merge: a single launch
+        # of each sequence writes the new token into its page) + the split
+        # combine (programmatic dependent launch) when a sequence is split
         mt = meta[t]
         md = mt.data_ptr()
         return _lib.AttentionArgs(
             q=qs[t].data_ptr(), q_dtype=_lib.PKV_BF16, n_queries=B, q_seq=md, q_nkeys=md + 4 * B,
             k_cache=store.keys.data_ptr(), v_cache=store.values.data_ptr(), kv_dtype=_lib.PKV_BF16,
-            block_table=mirror.data_ptr(), bt_stride=mirror.shape[1], seq_row=rows.data_ptr(),
+            block_table=mirror.data_ptr(), bt_stride=mirror.shape[1], seq_row=md + 8 * B,
             seq_start=None, page_size=ps, hq=hq, hkv=hkv, head_dim=d, scale=cfg.scale,
             out=out.data_ptr(), out_dtype=_lib.PKV_F32, workspace=ws.data_ptr(),
             workspace_bytes=ws.numel(), num_sms=0, target_waves=args.waves,
             prof_start=prof_pair[0].cuda_event if prof_pair else None,
             prof_stop=prof_pair[1].cuda_event if prof_pair else None,
             mode=0, k_new=ks[t].data_ptr(), v_new=vs[t].data_ptr(),
-            counters=cnt.data_ptr(), counters_len=cnt.numel())
+            plan=md + 12 * B, plan_host=plans[t].ctypes.data)
 
     # argument blocks are built before the timed region so the host only
     # pays one C call per step (keeps host latency out of the device timing)
@@ -305,6 +315,8 @@ def run_ours(args, rank, world, device):
         "tokens_all": tokens_all, "kv_all": kv_all, "alg_all": alg_all,
         "k2_ms_mean": sum(k2_ms) / K, "k2_alg_bytes_mean": alg_bytes / K,
         "clocks": clocks.summary(), "lengths": lengths, "shape": (hq, hkv, d, ps),
+        # decode launch + split combine (plan header word 6: split queries)
+        "launches": sum(1 + int(plans[W + i][6] > 0) for i in range(K)),
     }
     if not args.no_e2e:
         result["e2e"] = run_e2e(args, pool, store, cfg, lengths, device, flush, world)
@@ -518,7 +530,7 @@ def main():
                          "k2_share_of_step": r["k2_ms_mean"] / (sum(r["step_ms"]) / K),
                          "algorithmic_bytes_per_launch": r["k2_alg_bytes_mean"]},
             "clocks": r["clocks"],
-            "gpu_launches": K * (1 if r["B"] <= 2048 else 2),
+            "gpu_launches": r["launches"],
         }
         if "e2e" in r:
             e = r["e2e"]

@@ -202,13 +202,23 @@ typedef struct pkv_attention_args {
    * [n_queries, hkv, head_dim] and written into its page first */
   const void* k_new;
   const void* v_new;
-  /* scheduler counters: a zero-filled uint32 array of at least
-   * 2 + n_queries * hq entries (work cursor, finished warps, split-merge
-   * counters), used for nothing else; every launch leaves it zeroed again
-   * (required by the tensor-core kernel) */
-  uint32_t* counters;
-  int64_t counters_len;
+  /* tensor-core path only: the work plan from pkv_attention_plan(), both the
+   * host copy (read by the launcher) and an identical device copy */
+  const int32_t* plan;
+  const int32_t* plan_host;
 } pkv_attention_args;
+
+/* Host planner of the tensor-core decode (a serving scheduler's job: the
+ * per-query key counts are host metadata).  q_row[i] is the mirror row of
+ * query i's sequence (paged) or its first K/V row (gathered).  Chooses the
+ * head blocking, even page splits, a size-sorted item order and a greedy
+ * LPT assignment of items to CTAs; writes at most
+ * pkv_attention_plan_ints(n_queries, hq) int32 into plan_out (*n_out = used).
+ * num_sms <= 0 queries the device; target_waves <= 0 uses the default. */
+int64_t pkv_attention_plan_ints(int64_t n_queries, int32_t hq);
+int pkv_attention_plan(const int32_t* q_nkeys, const int32_t* q_row, int64_t n_queries,
+                       int32_t page_size, int32_t hq, int32_t hkv, int32_t num_sms,
+                       int32_t target_waves, int32_t* plan_out, int64_t cap, int64_t* n_out);
 
 /* Workspace bound: the split planner never creates more than
  * n_queries + 8192 key splits, so the bound depends only on the query count. */

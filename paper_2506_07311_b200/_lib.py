@@ -48,7 +48,7 @@ class AttentionArgs(C.Structure):
         ("num_sms", _i32), ("target_waves", _i32),
         ("prof_start", _vp), ("prof_stop", _vp),
         ("mode", _i32), ("k_new", _vp), ("v_new", _vp),
-        ("counters", _vp), ("counters_len", _i64),
+        ("plan", _vp), ("plan_host", _vp),
     ]
 
 
@@ -96,6 +96,8 @@ SIGNATURES = {
     "pkv_page_copy": (C.c_int, [_vp, _vp, _vp, _i64, _i64, _i32, _vp]),
     "pkv_kv_append": (C.c_int, [_vp, _vp, _i64, _vp, _i32, _vp, _vp, _i64, _i32, _vp, _vp, _i64, _vp]),
     "pkv_attention_workspace_bytes": (_i64, [_i64, _i32, _i32]),
+    "pkv_attention_plan_ints": (_i64, [_i64, _i32]),
+    "pkv_attention_plan": (C.c_int, [_vp, _vp, _i64, _i32, _i32, _i32, _i32, _i32, _vp, _i64, _P(_i64)]),
     "pkv_paged_attention": (C.c_int, [_P(AttentionArgs), _vp]),
     "pkv_prefill_supported": (C.c_int, [_i32, _i32, _i32, _i32, _i32]),
     "pkv_paged_prefill": (C.c_int, [_P(PrefillArgs), _vp]),
@@ -134,3 +136,19 @@ def check(status: int, what: str = "") -> None:
 
 def call(name: str, *args) -> None:
     check(getattr(load(), name)(*args), name)
+
+
+def attention_plan(q_nkeys, q_row, page_size: int, hq: int, hkv: int, target_waves: int = 0):
+    """Host plan of the tensor-core decode (pkv_attention_plan) as int32 numpy."""
+    import numpy as np
+
+    nk = np.ascontiguousarray(q_nkeys, dtype=np.int32)
+    rows = np.ascontiguousarray(q_row, dtype=np.int32)
+    n = nk.size
+    lib = load()
+    out = np.empty(lib.pkv_attention_plan_ints(n, hq), dtype=np.int32)
+    got = C.c_int64()
+    check(lib.pkv_attention_plan(nk.ctypes.data, rows.ctypes.data, n, page_size, hq, hkv, 0,
+                                 target_waves, out.ctypes.data, out.size, C.byref(got)),
+          "pkv_attention_plan")
+    return out[: got.value].copy()

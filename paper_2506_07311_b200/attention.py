@@ -213,11 +213,9 @@ def _check_queries(queries, meta: MaskMeta, config: AttentionConfig):
 
 
 class _Workspace:
-    """Per-device scratch for split partials and the device split plan, plus
-    the zero-filled split-merge counters (pkv200.h: used for nothing else)."""
+    """Per-device scratch for split partials (and the CUDA-core device plan)."""
 
     _bufs: dict = {}
-    _counters: dict = {}
 
     @classmethod
     def get(cls, device, nbytes: int):
@@ -227,17 +225,6 @@ class _Workspace:
         if buf is None or buf.numel() < nbytes:
             buf = torch.empty(max(nbytes, 1 << 20), dtype=torch.uint8, device=device)
             cls._bufs[device] = buf
-        return buf
-
-    @classmethod
-    def counters(cls, device, n: int):
-        import torch
-
-        n = n + 2  # work cursor + finished-warp count precede the merge counters
-        buf = cls._counters.get(device)
-        if buf is None or buf.numel() < n:
-            buf = torch.zeros(max(n, 1 << 16), dtype=torch.int32, device=device)
-            cls._counters[device] = buf
         return buf
 
 
@@ -264,22 +251,34 @@ def _launch_attention(q, qcode, meta, config, nkeys, *, k, v, kv_code, bt, bt_st
     out = torch.empty((nq, config.head_count, config.head_dim), dtype=out_t, device=device)
     if nq == 0:
         return out
-    meta_host = np.concatenate([meta.q_seq.astype(np.int32), nkeys.astype(np.int32)])
-    meta_dev = torch.from_numpy(meta_host).to(device)
+    # one packed upload: [q_seq | q_nkeys | seq_row (or seq_start as int64) | plan]
+    q_seq = meta.q_seq.astype(np.int32)
+    rows_by_seq = seq_row if bt is not None else seq_start
+    q_row = np.asarray(rows_by_seq, dtype=np.int64)[meta.q_seq]
+    if q_row.size and (q_row.max() >= 2 ** 31):
+        raise OutOfRange("K/V rows beyond 2^31 are not addressable")
+    plan = _lib.attention_plan(nkeys, q_row, config.page_size, config.head_count,
+                               config.kv_head_count)
+    seq_part = (np.asarray(seq_row, dtype=np.int32) if bt is not None
+                else np.asarray(seq_start, dtype=np.int64).view(np.int32))
+    nseq = seq_part.size
+    # 2*nq int32 precede seq_part, so an int64 seq_start stays 8-byte aligned
+    host = np.concatenate([q_seq, nkeys.astype(np.int32), seq_part, plan])
+    dev = torch.from_numpy(host).to(device)
+    base = dev.data_ptr()
+    seq_ptr = base + 4 * (2 * nq)
+    plan_ptr = seq_ptr + 4 * nseq
     ws_bytes = _lib.load().pkv_attention_workspace_bytes(nq, config.head_count, config.head_dim)
     ws = _Workspace.get(device, ws_bytes)
-    cnt = _Workspace.counters(device, nq * config.head_count)
     args = _lib.AttentionArgs(
-        q=q.data_ptr(), q_dtype=qcode, n_queries=nq,
-        q_seq=meta_dev.data_ptr(), q_nkeys=meta_dev.data_ptr() + 4 * nq,
+        q=q.data_ptr(), q_dtype=qcode, n_queries=nq, q_seq=base, q_nkeys=base + 4 * nq,
         k_cache=k.data_ptr(), v_cache=v.data_ptr(), kv_dtype=kv_code,
         block_table=bt.data_ptr() if bt is not None else None, bt_stride=bt_stride,
-        seq_row=seq_row.data_ptr() if seq_row is not None else None,
-        seq_start=seq_start.data_ptr() if seq_start is not None else None,
+        seq_row=seq_ptr if bt is not None else None, seq_start=seq_ptr if bt is None else None,
         page_size=config.page_size, hq=config.head_count, hkv=config.kv_head_count,
         head_dim=config.head_dim, scale=float(config.scale), out=out.data_ptr(), out_dtype=out_code,
         workspace=ws.data_ptr(), workspace_bytes=ws.numel(), num_sms=0, target_waves=0,
-        mode=PRECISION_MODES[precision], counters=cnt.data_ptr(), counters_len=cnt.numel())
+        mode=PRECISION_MODES[precision], plan=plan_ptr, plan_host=plan.ctypes.data)
     _lib.check(_lib.load().pkv_paged_attention(C.byref(args), _stream(device)), "pkv_paged_attention")
     return out
 
@@ -315,7 +314,7 @@ def paged_attention(queries, store: KvStore, meta: MaskMeta, config: AttentionCo
         _fill_stats(stats, meta, config, nkeys, block_mask)
     device = store.device
     q, qcode = _q_tensor(queries, device)
-    seq_row = torch.from_numpy(np.asarray([t.mirror_row for t in tables], dtype=np.int32)).to(device)
+    seq_row = np.asarray([t.mirror_row for t in tables], dtype=np.int32)
     mirror = store.pool.device_table(device)
     return _launch_attention(q, qcode, meta, config, nkeys, k=store.keys, v=store.values,
                              kv_code=store.dtype_code, bt=mirror, bt_stride=mirror.shape[1],
@@ -349,7 +348,7 @@ def gathered_attention(queries, keys, values, meta: MaskMeta, config: AttentionC
     v = to_device(values, device, k.dtype)
     _, kv_code = torch_dtype(k.dtype)
     q, qcode = _q_tensor(queries, device)
-    seq_start = torch.from_numpy(meta.view.prefix_sums.astype(np.int64)).to(device)
+    seq_start = meta.view.prefix_sums.astype(np.int64)
     return _launch_attention(q, qcode, meta, config, nkeys, k=k, v=v, kv_code=kv_code, bt=None,
                              bt_stride=0, seq_row=None, seq_start=seq_start,
                              out_dtype=out_dtype or torch.float32, device=device,

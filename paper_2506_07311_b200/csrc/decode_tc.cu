@@ -1,236 +1,114 @@
 // K2-TC: split-K paged decode on the tensor cores (mma.sync m16n8k16, bf16 /
-// fp16 operands, fp32 accumulation) for 16-bit KV caches.
+// fp16 operands, fp32 accumulation) for 16-bit KV caches, plus its split
+// combine (K2c) and the host-side planner.
 //
 // Replaces the reference streaming kernel (attention.py:259-329) for bf16
 // stores.  Decode is HBM bound (GQA-4 bf16: 4 flop/B, far below the ridge), so
-// the tensor cores are used to cut *issue* cost, not for FLOPs: the CUDA-core
-// kernel spends ~1200 instructions per 8 KiB chunk on unpacking, FMA chains
-// and shuffles; here a 16-key chunk costs 16 HMMA + 16 LDSM + the softmax.
-// tcgen05 is not used: M = G <= 16 query rows is not a dense contraction and
-// the TMEM round trip would cost more than it saves.
+// the tensor cores are used to cut *issue* cost, not for FLOPs: a 16-key chunk
+// costs 16 HMMA + 16 LDSM + the softmax instead of ~1200 CUDA-core
+// instructions.  tcgen05 is not used: M = G <= 16 query rows is not a dense
+// contraction and the TMEM round trip would cost more than it saves
+// (SURVEY.md §2.3).
 //
-// Work decomposition.  A work item is (query, kv head, group of <= 16 query
-// heads, key split) and is processed by a whole CTA (8 warps, one CTA per SM):
-// warp w takes the item's 16-key chunks w, w+8, w+16, ...  and the 8 partial
-// softmax states are merged through shared memory at the end of the item, so
-// the number of *global* splits per query is 8x smaller than with warp items
-// and small batches do not drown in split merges.  The item list is planned
-// on the device from the per-query key counts (even page ranges per split,
-// at least kMinSplitChunks chunks per split), sorted by item size and dealt
-// to CTAs in snake order (LPT-style balance), so each CTA knows its whole item
-// sequence up front.  That lets every warp run a *producer* that streams its
-// chunks through a private 3-stage cp.async ring (16-byte XOR swizzle ->
-// conflict-free LDSM; zero-fill past the valid keys) straight across item
-// boundaries: the next item's pages are in flight while the current one
-// merges.  The G grouped query heads are the M rows of the MMA, so every K/V
-// byte is read from HBM once per group.
+// Work decomposition (planned on the host, like any serving scheduler: the
+// per-query key counts are host metadata).  A work item is (query, key split,
+// block of HB kv heads, group of query heads) and is processed by one CTA of 8
+// warps, one CTA per SM.  Each kv head of the block gets WPH = 8/HB warps:
+//   * large batches: HB = 8, WPH = 1 — one warp streams one kv head over the
+//     whole split, no intra-CTA merging at all;
+//   * small batches: HB < 8, WPH > 1 — the warps of a head take its 16-key
+//     chunks round-robin and merge through shared memory (asynchronously: the
+//     last warp to arrive merges in warp order), which keeps the number of
+//     global splits per query small.
+// Items are sorted by size and dealt to CTAs in snake order (LPT balance), so
+// every CTA knows its item sequence up front and every warp runs a producer
+// that streams its chunks through a private 3-stage cp.async ring (16-byte
+// XOR swizzle -> conflict-free LDSM; zero-fill past the valid keys) straight
+// across item boundaries.  The G grouped query heads are the M rows of the
+// MMA, so every K/V byte is read from HBM once per query-head group.
 //
 // Numerics: scores accumulate unscaled in fp32 and the softmax scale (times
 // log2 e) is folded into the exp2 argument; P is rounded to the operand type
 // for the P@V MMA and the denominator sums the *rounded* P.  fp32 queries are
 // split hi+lo into two MMAs (fp32-accurate scores).
 //
-// Splits of one query are merged by the last CTA to finish (acq_rel atomic
-// counters that self-reset), in ascending split order: deterministic, and no
-// combine launch.  Optional fused append: with k_new/v_new the last split of
-// each query reads the new token from the input and writes it into its page
+// Splits of a query write (m, l, O) partials; the combine kernel (launched
+// with programmatic dependent launch, so its launch overlaps the decode tail)
+// merges them in ascending split order: deterministic, no atomics in the hot
+// loop.  Optional fused append: with k_new/v_new the last split of each query
+// reads the new token from the input and writes it into its page
 // (reshape-and-cache folded into the decode launch).
+#include <algorithm>
+#include <functional>
+#include <numeric>
+#include <queue>
+#include <vector>
+
 #include "common.cuh"
 #include "decode_tc.h"
 
 namespace pkv {
+
+// Debug timeline (pkv_debug_trace): per CTA, globaltimer stamps of
+// [start, plan loaded, item k consumer start..., chunks done, published, end].
+__device__ unsigned long long g_trace[1024 * 64];
+__device__ volatile int g_trace_on;
+
 namespace {
 
 constexpr int kWarpsTc = 8;
 constexpr int kThreadsTc = kWarpsTc * 32;
 constexpr int kStagesTc = 3;
-constexpr int kCh = 16;              // keys per chunk
-constexpr int kMinSplitChunks = 16;  // >= 2 chunks per warp per item
-constexpr int kMergeRows = 4;        // rows per CTA-merge pass
-constexpr int kMaxPending = 128;     // queued split merges per CTA
-
-struct Item {
-  int qi, hi, kvh, qh0, rows, split, nsplit, kb, ke, nchunks, nk, row, slot;
-  bool valid;
-};
-
-// Debug timeline (pkv_debug_trace): per CTA, globaltimer stamps of
-// [start, plan done, item k consumer start..., item k merged..., end].
+constexpr int kCh = 16;        // keys per chunk
+constexpr int kMergeRows = 4;  // rows per warp slot of the intra-CTA merge
+// planner cost of an item: head-pages streamed + a fixed per-item overhead
+// (pipeline refill, query load, merge), in head-page units (~2 us)
+constexpr int64_t kItemOverhead = 12;
 constexpr int kTraceSlots = 64;
-}  // namespace
-// external linkage + volatile reads: the flag is only ever written by the host
-__device__ unsigned long long g_trace[1024 * 64];
-__device__ volatile int g_trace_on;
-namespace {
 
 __device__ __forceinline__ unsigned long long gtimer() {
   unsigned long long t;
   asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
   return t;
 }
+// per warp: 32 slots [start, plan, (item start, first data, chunks done,
+// stored) x 7, end]; lane 0 of every warp of CTAs < 256 records
 __device__ __forceinline__ void trace(int slot) {
-  if (g_trace_on && threadIdx.x == 0 && slot < kTraceSlots && blockIdx.x < 1024)
-    g_trace[blockIdx.x * kTraceSlots + slot] = gtimer();
+  if (g_trace_on && (threadIdx.x & 31) == 0 && slot < 32 && blockIdx.x < 256)
+    g_trace[(blockIdx.x * 8 + (threadIdx.x >> 5)) * 32 + slot] = gtimer();
 }
 
-// Plan arrays (shared memory, or global for large query counts).
+// plan layout (int32), see plan_decode()
+enum {
+  H_HB = 0, H_WPH, H_QGS, H_QGROUPS, H_HEAD_ITEMS, H_TOTAL_ITEMS, H_NSPLIT_Q, H_NQ,
+  H_GRID, H_CTA_OFF, H_CTA_ITEMS, kHdr = 12
+};
+constexpr int kCtaItemsSmem = 64;  // per-CTA item list staged in shared memory
+__host__ __device__ constexpr int64_t o_order(int64_t) { return kHdr; }
+__host__ __device__ constexpr int64_t o_ioff(int64_t nq) { return kHdr + nq; }
+__host__ __device__ constexpr int64_t o_nsplit(int64_t nq) { return kHdr + 2 * nq + 1; }
+__host__ __device__ constexpr int64_t o_soff(int64_t nq) { return kHdr + 3 * nq + 1; }
+__host__ __device__ constexpr int64_t o_nk(int64_t nq) { return kHdr + 4 * nq + 2; }
+__host__ __device__ constexpr int64_t o_row(int64_t nq) { return kHdr + 5 * nq + 2; }
+__host__ __device__ constexpr int64_t o_cq(int64_t nq) { return kHdr + 6 * nq + 2; }
+
 struct PlanView {
-  const int32_t* nk;      // [nq] key counts
-  const int32_t* row;     // [nq] mirror row (paged) / first row (gathered)
-  const int32_t* order;   // [nq] queries sorted by split size (desc)
-  const int32_t* nsplit;  // [nq]
-  const int32_t* ioff;    // [nq + 1] item offsets over the sorted queries
-  const int32_t* soff;    // [nq + 1] split-slot offsets by query index
-  int64_t total_items;
+  const int32_t *order, *ioff, *nsplit, *soff, *nk, *row;
+  int hb, wph, qgs, qgroups, head_items, total_items, nq;
 };
 
-// ---------------------------------------------------------------------------
-// Block-wide planner (used in-CTA for small query counts and by the plan
-// kernel otherwise).  `keys` is scratch for the sort: 2 * nq_pow2 int64.
-// ---------------------------------------------------------------------------
-__device__ void plan_block(const TcParams& p, int32_t* nk, int32_t* row, int32_t* order,
-                           int32_t* nsplit, int32_t* ioff, int32_t* soff, long long* keys,
-                           int nq_pow2, long long* red, int* hdr) {
-  const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, warp = tid >> 5, nw = nt >> 5;
-  const int ps = 1 << p.log2ps;
-  long long pages = 0;
-  for (int i = tid; i < p.nq; i += nt) {
-    const int n = p.q_nkeys[i];
-    const int sv = p.q_seq[i];
-    nk[i] = n;
-    row[i] = p.bt ? p.seq_row[sv] : static_cast<int>(p.seq_start[sv]);
-    pages += (n + ps - 1) >> p.log2ps;
-  }
-#pragma unroll
-  for (int o = 16; o; o >>= 1) pages += __shfl_xor_sync(0xffffffffu, pages, o);
-  if (lane == 0) red[warp] = pages;
-  __syncthreads();
-  if (tid == 0) {
-    long long tot = 0;
-    for (int w = 0; w < nw; ++w) tot += red[w];
-    long long sp = (tot * p.head_items + p.target_items - 1) / p.target_items;
-    const long long min_sp = (int64_t(kMinSplitChunks) * kCh + ps - 1) / ps;
-    const long long cap = (tot + kMaxExtraSplitsTc - 1) / kMaxExtraSplitsTc;
-    sp = sp < min_sp ? min_sp : sp;
-    sp = sp < cap ? cap : sp;
-    red[0] = sp;
-  }
-  __syncthreads();
-  const long long sp = red[0];
-  // sort key: (split size desc, query asc); padding sorts last
-  for (int i = tid; i < nq_pow2; i += nt) {
-    long long key = 0x7fffffffffffffffLL;
-    if (i < p.nq) {
-      const long long pg = (nk[i] + ps - 1) >> p.log2ps;
-      const long long ns = (pg + sp - 1) / sp;
-      nsplit[i] = static_cast<int32_t>(ns);
-      const long long size = (pg + ns - 1) / ns;
-      key = ((0x7fffffffLL - size) << 32) | i;
-    }
-    keys[i] = key;
-  }
-  __syncthreads();
-  if (nq_pow2 <= 32) {
-    // small batches: bitonic sort inside warp 0 with shuffles (no barriers)
-    if (warp == 0) {
-      long long x = lane < nq_pow2 ? keys[lane] : 0x7fffffffffffffffLL;
-      for (int k = 2; k <= 32; k <<= 1) {
-        for (int j = k >> 1; j > 0; j >>= 1) {
-          const long long y = __shfl_xor_sync(0xffffffffu, x, j);
-          const bool up = (lane & k) == 0;
-          const bool lower = (lane & j) == 0;
-          x = (lower == up) ? (x < y ? x : y) : (x < y ? y : x);
-        }
-      }
-      if (lane < nq_pow2) keys[lane] = x;
-    }
-    __syncthreads();
-  }
-  for (int k = 2; nq_pow2 > 32 && k <= nq_pow2; k <<= 1) {
-    for (int j = k >> 1; j > 0; j >>= 1) {
-      for (int i = tid; i < nq_pow2; i += nt) {
-        const int ixj = i ^ j;
-        if (ixj > i) {
-          const long long a = keys[i], b = keys[ixj];
-          const bool up = (i & k) == 0;
-          if ((a > b) == up) {
-            keys[i] = b;
-            keys[ixj] = a;
-          }
-        }
-      }
-      __syncthreads();
-    }
-  }
-  for (int i = tid; i < p.nq; i += nt) order[i] = static_cast<int32_t>(keys[i] & 0xffffffff);
-  __syncthreads();
-  // two exclusive scans: items over the sorted order, split slots by index
-  int carry_i = 0, carry_s = 0;
-  int* scan = reinterpret_cast<int*>(red);  // 2 * nw ints
-  for (int base = 0; base < p.nq; base += nt) {
-    const int i = base + tid;
-    int ci = 0, cs = 0;
-    if (i < p.nq) {
-      ci = nsplit[order[i]] * p.head_items;
-      cs = nsplit[i];
-    }
-    int xi = ci, xs = cs;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const int yi = __shfl_up_sync(0xffffffffu, xi, o);
-      const int ys = __shfl_up_sync(0xffffffffu, xs, o);
-      if (lane >= o) {
-        xi += yi;
-        xs += ys;
-      }
-    }
-    if (lane == 31) {
-      scan[warp] = xi;
-      scan[nw + warp] = xs;
-    }
-    __syncthreads();
-    int bi = 0, bs = 0, ai = 0, as = 0;
-    for (int w = 0; w < nw; ++w) {
-      const int vi = scan[w], vs = scan[nw + w];
-      if (w < warp) {
-        bi += vi;
-        bs += vs;
-      }
-      ai += vi;
-      as += vs;
-    }
-    if (i < p.nq) {
-      ioff[i] = carry_i + bi + xi - ci;
-      soff[i] = carry_s + bs + xs - cs;
-    }
-    carry_i += ai;
-    carry_s += as;
-    __syncthreads();
-  }
-  if (tid == 0) {
-    ioff[p.nq] = carry_i;
-    soff[p.nq] = carry_s;
-    hdr[0] = carry_i;
-  }
-  __syncthreads();
-}
+// one warp's view of a work item
+struct Item {
+  int qi, kvh, sub, qh0, rows, split, nsplit, kb, ke, nchunks, nk, row, slot;
+  bool valid;
+};
 
-__global__ void __launch_bounds__(1024) plan_tc_kernel(const __grid_constant__ TcParams p, int32_t* g,
-                                                        long long* keys, int nq_pow2) {
-  __shared__ long long red[32];
-  __shared__ int hdr[1];
-  const int nq = p.nq;
-  plan_block(p, g + 4, g + 4 + nq, g + 4 + 2 * nq, g + 4 + 3 * nq, g + 4 + 4 * nq,
-             g + 4 + 5 * nq + 1, keys, nq_pow2, red, hdr);
-  if (threadIdx.x == 0) g[0] = hdr[0];
-}
-
-__device__ __forceinline__ Item make_item(int64_t gidx, const PlanView& pv, const TcParams& p) {
+__device__ __forceinline__ Item make_item(int64_t gidx, const PlanView& pv, const TcParams& p, int warp) {
   Item it;
   it.valid = gidx < pv.total_items;
   if (!it.valid) return it;
   const int gi = static_cast<int>(gidx);
-  int lo = 0, hi = p.nq;  // sorted position j with ioff[j] <= gi < ioff[j+1]
+  int lo = 0, hi = pv.nq;  // sorted position j with ioff[j] <= gi < ioff[j+1]
   while (hi - lo > 1) {
     const int mid = (lo + hi) >> 1;
     if (pv.ioff[mid] <= gi) lo = mid; else hi = mid;
@@ -238,12 +116,14 @@ __device__ __forceinline__ Item make_item(int64_t gidx, const PlanView& pv, cons
   const int q = pv.order[lo];
   const int rem = gi - pv.ioff[lo];
   it.qi = q;
-  it.split = rem / p.head_items;
-  it.hi = rem - it.split * p.head_items;
-  it.kvh = it.hi / p.qgroups;
-  const int qg = it.hi - it.kvh * p.qgroups;
-  it.qh0 = it.kvh * p.group + qg * 16;
-  it.rows = min(16, p.group - qg * 16);
+  it.split = rem / pv.head_items;
+  const int hix = rem - it.split * pv.head_items;
+  const int hb = hix / pv.qgroups;
+  const int qg = hix - hb * pv.qgroups;
+  it.kvh = hb * pv.hb + warp / pv.wph;
+  it.sub = warp % pv.wph;
+  it.qh0 = it.kvh * p.group + qg * pv.qgs;
+  it.rows = min(pv.qgs, p.group - qg * pv.qgs);
   it.nsplit = pv.nsplit[q];
   it.nk = pv.nk[q];
   it.row = pv.row[q];
@@ -267,179 +147,17 @@ __device__ __forceinline__ Item make_item(int64_t gidx, const PlanView& pv, cons
   return it;
 }
 
-// Merge the nsplit partials (m, l, unnormalised O) of one (query, head group)
-// by the whole CTA, in ascending split order.  Split weights are computed once
-// into shared memory (`scratch`, >= 2*rows*nsplit + rows floats when it fits;
-// otherwise recomputed per element), then every thread accumulates float4
-// slices of O with 8 independent loads in flight.
-template <int D>
-__device__ void merge_global(const TcParams& p, const Item& C, int64_t out_base, float* scratch) {
-  const int ns = C.nsplit, rows = C.rows, s0 = C.slot - C.split;
-  const float2* ml = reinterpret_cast<const float2*>(p.ws_ml);
-  const bool staged = rows * ns * 2 + rows <= kWarpsTc * kMergeRows * D;
-  float* s_w = scratch;                // [rows][ns] weights
-  float* s_inv = scratch + rows * ns;  // [rows] 1 / denominator
-  if (staged) {
-    for (int e = threadIdx.x; e < rows * ns; e += kThreadsTc) {
-      const int r = e / ns, s = e - r * ns;
-      const float2 v = __ldcg(ml + (int64_t(s0 + s) * p.hq + C.qh0 + r));
-      s_w[e] = v.x;
-      s_w[rows * ns + rows + e] = v.y;
-    }
-    __syncthreads();
-    for (int r = threadIdx.x >> 5; r < rows; r += kWarpsTc) {  // one warp per row
-      const int lane = threadIdx.x & 31;
-      float mx = -INFINITY;
-      for (int s = lane; s < ns; s += 32) mx = fmaxf(mx, s_w[r * ns + s]);
-#pragma unroll
-      for (int o = 16; o; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-      float den = 0.f;
-      for (int s = lane; s < ns; s += 32) {
-        const float w = exp2f(s_w[r * ns + s] - mx);
-        den += w * s_w[rows * ns + rows + r * ns + s];
-        s_w[r * ns + s] = w;
-      }
-#pragma unroll
-      for (int o = 16; o; o >>= 1) den += __shfl_xor_sync(0xffffffffu, den, o);
-      if (lane == 0) s_inv[r] = 1.f / den;
-    }
-    __syncthreads();
+// k-th item of this CTA (host LPT assignment; staged list, global beyond it)
+struct CtaItems {
+  const int32_t* smem_list;
+  const int32_t* global_list;
+  int count;
+  int total;
+  __device__ __forceinline__ int64_t operator()(int64_t k) const {
+    if (k >= count) return total;  // invalid item: end of this CTA's work
+    return k < kCtaItemsSmem ? smem_list[k] : global_list[k];
   }
-  constexpr int V = D / 4;  // float4 slices per row
-  for (int e = threadIdx.x; e < rows * V; e += kThreadsTc) {
-    const int r = e / V, dv = e - r * V;
-    const int64_t col = C.qh0 + r;
-    float mx = 0.f, inv = 0.f;
-    if (!staged) {
-      mx = -INFINITY;
-      for (int s = 0; s < ns; ++s) mx = fmaxf(mx, __ldcg(ml + (int64_t(s0 + s) * p.hq + col)).x);
-      float den = 0.f;
-      for (int s = 0; s < ns; ++s) {
-        const float2 v = __ldcg(ml + (int64_t(s0 + s) * p.hq + col));
-        den += exp2f(v.x - mx) * v.y;
-      }
-      inv = 1.f / den;
-    } else {
-      inv = s_inv[r];
-    }
-    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-    for (int sb = 0; sb < ns; sb += 8) {
-      float4 ov[8];
-#pragma unroll
-      for (int u = 0; u < 8; ++u)
-        ov[u] = sb + u < ns ? __ldcg(reinterpret_cast<const float4*>(p.ws_o + (int64_t(s0 + sb + u) * p.hq + col) * D) + dv)
-                            : make_float4(0.f, 0.f, 0.f, 0.f);
-#pragma unroll
-      for (int u = 0; u < 8; ++u) {
-        if (sb + u >= ns) break;
-        const float w = staged ? s_w[r * ns + sb + u]
-                               : exp2f(__ldcg(ml + (int64_t(s0 + sb + u) * p.hq + col)).x - mx);
-        acc.x += w * ov[u].x;
-        acc.y += w * ov[u].y;
-        acc.z += w * ov[u].z;
-        acc.w += w * ov[u].w;
-      }
-    }
-    const int64_t off = out_base + int64_t(r) * D + 4 * dv;
-    store_from_float(p.out, off, p.out_dtype, acc.x * inv);
-    store_from_float(p.out, off + 1, p.out_dtype, acc.y * inv);
-    store_from_float(p.out, off + 2, p.out_dtype, acc.z * inv);
-    store_from_float(p.out, off + 3, p.out_dtype, acc.w * inv);
-  }
-}
-
-// One warp merges the 8 per-warp states of an item (rows <= kMergeRows) from
-// shared memory, in warp order, and writes the output row (single split) or
-// the item's global split partial.
-template <int D>
-__device__ void warp_merge_item(const TcParams& p, const Item& C, int64_t out_base, const float* s_mo,
-                                const float* s_ml, int lane, int* s_sync, int k) {
-  constexpr int E = D / 32;  // elements per lane per row
-  float acc[kMergeRows][E];
-  float rmx[kMergeRows], rden[kMergeRows];
-  // 1) read all slots into registers (warp order: deterministic)
-#pragma unroll
-  for (int r = 0; r < kMergeRows; ++r) {
-    if (r >= C.rows) break;
-    float mw[kWarpsTc];
-    float mx = -INFINITY;
-#pragma unroll
-    for (int w = 0; w < kWarpsTc; ++w) {
-      mw[w] = s_ml[(w * kMergeRows + r) * 2];
-      mx = fmaxf(mx, mw[w]);
-    }
-    float den = 0.f;
-#pragma unroll
-    for (int w = 0; w < kWarpsTc; ++w) {
-      mw[w] = mw[w] == -INFINITY ? 0.f : exp2f(mw[w] - mx);
-      den += mw[w] * s_ml[(w * kMergeRows + r) * 2 + 1];
-    }
-#pragma unroll
-    for (int e = 0; e < E; ++e) {
-      float a = 0.f;
-#pragma unroll
-      for (int w = 0; w < kWarpsTc; ++w) a += mw[w] * s_mo[(w * kMergeRows + r) * D + lane + 32 * e];
-      acc[r][e] = a;
-    }
-    rmx[r] = mx;
-    rden[r] = den;
-  }
-  // 2) release the slots before touching global memory
-  __syncwarp();
-  if (lane == 0) {
-    s_sync[0] = 0;
-    *reinterpret_cast<volatile int*>(&s_sync[1]) = k + 1;
-  }
-  // 3) output row (single split) or the item's global split partial
-#pragma unroll
-  for (int r = 0; r < kMergeRows; ++r) {
-    if (r >= C.rows) break;
-    const int64_t slot = int64_t(C.slot) * p.hq + C.qh0 + r;
-#pragma unroll
-    for (int e = 0; e < E; ++e) {
-      const int d = lane + 32 * e;
-      if (C.nsplit == 1)
-        store_from_float(p.out, out_base + int64_t(r) * D + d, p.out_dtype, acc[r][e] / rden[r]);
-      else
-        __stcg(p.ws_o + slot * D + d, acc[r][e]);
-    }
-    if (C.nsplit > 1 && lane == 0) __stcg(reinterpret_cast<float2*>(p.ws_ml) + slot, make_float2(rmx[r], rden[r]));
-  }
-}
-
-// Single-warp split merge (overflow fallback of the queued CTA merges).
-template <int D>
-__device__ void merge_global_warp(const TcParams& p, const Item& C, int64_t out_base, int lane) {
-  const int s0 = C.slot - C.split;
-  const float2* ml = reinterpret_cast<const float2*>(p.ws_ml);
-  for (int r = 0; r < C.rows; ++r) {
-    const int64_t col = C.qh0 + r;
-    float mx = -INFINITY;
-    for (int s = lane; s < C.nsplit; s += 32) mx = fmaxf(mx, __ldcg(ml + (int64_t(s0 + s) * p.hq + col)).x);
-#pragma unroll
-    for (int o = 16; o; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-    float den = 0.f;
-    for (int s = lane; s < C.nsplit; s += 32) {
-      const float2 v = __ldcg(ml + (int64_t(s0 + s) * p.hq + col));
-      den += exp2f(v.x - mx) * v.y;
-    }
-#pragma unroll
-    for (int o = 16; o; o >>= 1) den += __shfl_xor_sync(0xffffffffu, den, o);
-    for (int d = lane; d < D; d += 32) {
-      float acc = 0.f;
-      for (int s = 0; s < C.nsplit; ++s) {
-        const int64_t slot = int64_t(s0 + s) * p.hq + col;
-        acc += exp2f(__ldcg(ml + slot).x - mx) * __ldcg(p.ws_o + slot * D + d);
-      }
-      store_from_float(p.out, out_base + int64_t(r) * D + d, p.out_dtype, acc / den);
-    }
-  }
-}
-
-// k-th item of CTA b in snake order over the size-sorted item list
-__device__ __forceinline__ int64_t item_of(int b, int64_t k, int G) {
-  return k * G + ((k & 1) ? (G - 1 - b) : b);
-}
+};
 
 template <typename T, int D, bool SPLITQ, bool ROWS16>
 __global__ void __launch_bounds__(kThreadsTc, 1) decode_tc_kernel(const __grid_constant__ TcParams p) {
@@ -452,91 +170,99 @@ __global__ void __launch_bounds__(kThreadsTc, 1) decode_tc_kernel(const __grid_c
   constexpr int NT = D / 8;              // n-tiles of P V
   static_assert(CPR >= 8 && CPR <= 32, "D must be 64 or 128");
 
-  extern __shared__ __align__(1024) unsigned char smem[];
-  __shared__ long long s_red[32];
-  __shared__ int s_hdr[2];
-  __shared__ int s_sync[3];  // arrivals of the current item, items merged, queued merges
-  __shared__ long long s_pend[kMaxPending];
-  if (threadIdx.x < 3) s_sync[threadIdx.x] = 0;
+  // dependents (the split combine) may launch now and wait for our completion
+  asm volatile("griddepcontrol.launch_dependents;");
 
+  extern __shared__ __align__(1024) unsigned char smem[];
+  __shared__ int s_arr[kWarpsTc];   // per head: arrivals at the current item
+  __shared__ int s_done[kWarpsTc];  // per head: items merged
+  __shared__ int32_t s_cta_items[kCtaItemsSmem];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   trace(0);
-  const int ps = 1 << p.log2ps;
-  float* s_mo = reinterpret_cast<float*>(smem + p.merge_offset);             // [W][4][D]
-  float* s_ml = s_mo + kWarpsTc * kMergeRows * D;                            // [W][4][2]
-
-  // ---------------- plan -------------------------------------------------
-  PlanView pv;
-  if (p.plan_global) {
-    const int nq = p.nq;
-    const int32_t* g = p.plan_global;
-    pv.nk = g + 4;
-    pv.row = g + 4 + nq;
-    pv.order = g + 4 + 2 * nq;
-    pv.nsplit = g + 4 + 3 * nq;
-    pv.ioff = g + 4 + 4 * nq;
-    pv.soff = g + 4 + 5 * nq + 1;
-    pv.total_items = g[0];
-  } else {
-    int32_t* base = reinterpret_cast<int32_t*>(smem);
-    const int nq = p.nq;
-    int32_t *nk = base, *row = nk + nq, *order = row + nq, *ns = order + nq, *ioff = ns + nq,
-            *soff = ioff + nq + 1;
-    int nq_pow2 = 1;
-    while (nq_pow2 < nq) nq_pow2 <<= 1;
-    // the sort scratch lives in the (not yet used) merge buffer
-    plan_block(p, nk, row, order, ns, ioff, soff, reinterpret_cast<long long*>(s_mo), nq_pow2, s_red,
-               s_hdr);
-    pv.nk = nk;
-    pv.row = row;
-    pv.order = order;
-    pv.nsplit = ns;
-    pv.ioff = ioff;
-    pv.soff = soff;
-    pv.total_items = s_hdr[0];
+  if (threadIdx.x < kWarpsTc) {
+    s_arr[threadIdx.x] = 0;
+    s_done[threadIdx.x] = 0;
   }
-  __syncthreads();
-  trace(1);
-  const int G = gridDim.x;
-  const int b = blockIdx.x;
+  CtaItems items;
+  {
+    const int32_t* off = p.plan + p.plan[H_CTA_OFF];
+    const int32_t* list = p.plan + p.plan[H_CTA_ITEMS];
+    const int first = __ldg(off + blockIdx.x);
+    items.count = __ldg(off + blockIdx.x + 1) - first;
+    items.global_list = list + first;
+    items.smem_list = s_cta_items;
+    items.total = __ldg(p.plan + H_TOTAL_ITEMS);
+    if (threadIdx.x < kCtaItemsSmem && threadIdx.x < items.count) s_cta_items[threadIdx.x] = __ldg(list + first + threadIdx.x);
+  }
 
+  // ---------------- plan (host-computed; staged into shared memory) ---------
+  PlanView pv;
+  {
+    const int32_t* g = p.plan;
+    const int nq = p.nq;
+    const int32_t* src = g;
+    if (p.plan_in_smem) {
+      int32_t* s = reinterpret_cast<int32_t*>(smem);
+      const int n = static_cast<int>(o_cq(nq));
+      for (int i = threadIdx.x; i < n; i += kThreadsTc) s[i] = __ldg(g + i);
+      __syncthreads();
+      src = s;
+    } else {
+      __syncthreads();
+    }
+    pv.order = src + o_order(nq);
+    pv.ioff = src + o_ioff(nq);
+    pv.nsplit = src + o_nsplit(nq);
+    pv.soff = src + o_soff(nq);
+    pv.nk = src + o_nk(nq);
+    pv.row = src + o_row(nq);
+    pv.hb = src[H_HB];
+    pv.wph = src[H_WPH];
+    pv.qgs = src[H_QGS];
+    pv.qgroups = src[H_QGROUPS];
+    pv.head_items = src[H_HEAD_ITEMS];
+    pv.total_items = src[H_TOTAL_ITEMS];
+    pv.nq = nq;
+  }
+  trace(1);
+  float* s_mo = reinterpret_cast<float*>(smem + p.merge_offset);  // [W][4][D]
+  float* s_ml = s_mo + kWarpsTc * kMergeRows * D;                 // [W][4][2]
   unsigned char* ring = smem + p.ring_offset + warp * (kStagesTc * STAGE);
   const uint32_t ring_addr = static_cast<uint32_t>(__cvta_generic_to_shared(ring));
   const int t4 = lane & 3, g = lane >> 2;
-  unsigned* merge_cnt = p.counters + 2;
+  const int ps = 1 << p.log2ps;
 
   // ======================= producer (per warp) ===========================
   const int cc = lane % CPR, r0 = lane / CPR;  // copy geometry of this lane
   Item P;
   int64_t pk = 0;  // producer item counter (within this CTA's sequence)
-  int pc = 0;      // next chunk of P to issue (warp-strided)
+  int pc = 0;      // next chunk of P to issue
   int win = -1, win_val = 0;
   auto start_item = [&]() {
     for (;;) {
-      P = make_item(item_of(b, pk, G), pv, p);
-      pc = warp;
+      P = make_item(items(pk), pv, p, warp);
+      pc = P.sub;
       win = -1;
       if (!P.valid) return;
-      if (warp == 0) {
-        // warm L2 with the item's query rows: every warp's consumer loads them
-        // at item start, after this warp's prefetched pages
+      if (P.sub == 0) {
+        // warm L2 with the query rows the consumer loads at item start
         const int qe = p.q_dtype == PKV_F32 ? 4 : 2;
         const char* qrow = static_cast<const char*>(p.q) + (int64_t(P.qi) * p.hq + P.qh0) * D * qe;
         if (lane * 128 < P.rows * D * qe) asm volatile("prefetch.global.L2 [%0];" ::"l"(qrow + lane * 128));
-      }
-      if (warp == 0 && p.k_new != nullptr && P.split == P.nsplit - 1) {
-        // fused append: write the new token's head slice into its page
-        const int pos = P.nk - 1;
-        const int64_t page = p.bt[int64_t(P.row) * p.bt_stride + (pos >> p.log2ps)];
-        const int64_t dst = (page * ps + (pos & (ps - 1))) * p.row_stride + int64_t(P.kvh) * ROWB;
-        const int64_t src = (int64_t(P.qi) * p.hkv + P.kvh) * ROWB;
-        if (lane < CPR) {
-          reinterpret_cast<uint4*>(p.kw + dst)[lane] = reinterpret_cast<const uint4*>(p.k_new + src)[lane];
-          reinterpret_cast<uint4*>(p.vw + dst)[lane] = reinterpret_cast<const uint4*>(p.v_new + src)[lane];
+        if (p.k_new != nullptr && P.split == P.nsplit - 1) {
+          // fused append: write the new token's head slice into its page
+          const int pos = P.nk - 1;
+          const int64_t page = p.bt[int64_t(P.row) * p.bt_stride + (pos >> p.log2ps)];
+          const int64_t dst = (page * ps + (pos & (ps - 1))) * p.row_stride + int64_t(P.kvh) * ROWB;
+          const int64_t srcb = (int64_t(P.qi) * p.hkv + P.kvh) * ROWB;
+          if (lane < CPR) {
+            reinterpret_cast<uint4*>(p.kw + dst)[lane] = reinterpret_cast<const uint4*>(p.k_new + srcb)[lane];
+            reinterpret_cast<uint4*>(p.vw + dst)[lane] = reinterpret_cast<const uint4*>(p.v_new + srcb)[lane];
+          }
         }
       }
       if (pc < P.nchunks) return;
-      ++pk;  // this warp has no chunk in the item: skip it
+      ++pk;  // no chunk of this item for this warp
     }
   };
 
@@ -584,7 +310,7 @@ __global__ void __launch_bounds__(kThreadsTc, 1) decode_tc_kernel(const __grid_c
         cp_async<16>(vdst + soff, ok ? vs_ : p.v, ok ? 16 : 0);
       }
       ++gissue;
-      pc += kWarpsTc;
+      pc += pv.wph;
       if (pc >= P.nchunks) {
         ++pk;
         start_item();
@@ -600,17 +326,18 @@ __global__ void __launch_bounds__(kThreadsTc, 1) decode_tc_kernel(const __grid_c
   // ======================= consumer ======================================
   long long gcons = 0;
   const float qscale = p.qscale;
+  const int head_local = warp / pv.wph;
   for (int64_t k = 0;; ++k) {
-    const Item C = make_item(item_of(b, k, G), pv, p);
+    const Item C = make_item(items(k), pv, p, warp);
     if (!C.valid) break;
-    trace(2 + 3 * int(k));
+    trace(2 + 4 * int(k));
 
     float o[NT][4];
 #pragma unroll
     for (int n = 0; n < NT; ++n) o[n][0] = o[n][1] = o[n][2] = o[n][3] = 0.f;
     float m0 = -INFINITY, m1 = -INFINITY, l0 = 0.f, l1 = 0.f;
 
-    if (warp < C.nchunks) {
+    if (C.sub < C.nchunks) {
       // Q fragments (A operand), unscaled
       uint32_t qa[KS][4];
       uint32_t qb[SPLITQ ? KS : 1][4];
@@ -642,9 +369,10 @@ __global__ void __launch_bounds__(kThreadsTc, 1) decode_tc_kernel(const __grid_c
         }
       }
 
-      for (int c = warp; c < C.nchunks; c += kWarpsTc) {
+      for (int c = C.sub; c < C.nchunks; c += pv.wph) {
         cp_async_wait<kStagesTc - 2>();
         __syncwarp();
+        if (c == C.sub) trace(3 + 4 * int(k));
         issue_next();
         const uint32_t kbase = ring_addr + static_cast<int>(gcons % kStagesTc) * STAGE;
         const uint32_t vbase = kbase + kCh * ROWB;
@@ -750,132 +478,153 @@ __global__ void __launch_bounds__(kThreadsTc, 1) decode_tc_kernel(const __grid_c
         l1 += __shfl_xor_sync(0xffffffffu, l1, 2);
       }
     }
-
-    trace(3 + 3 * int(k));
+    trace(4 + 4 * int(k));
     const int64_t out_base = (int64_t(C.qi) * p.hq + C.qh0) * D;
+    const int64_t pslot = int64_t(C.slot) * p.hq + C.qh0;  // split partial rows
 
-    if (C.rows <= kMergeRows) {
-      // ---- asynchronous CTA merge: each warp publishes its state into its
-      // shared-memory slot and moves on to its next item; the last warp to
-      // arrive merges the 8 slots in warp order (deterministic).  A warp only
-      // overwrites its slot after the previous item's merge released it.
-      if (k > 0) {
-        if (lane == 0)
-          while (*reinterpret_cast<volatile int*>(&s_sync[1]) < static_cast<int>(k)) __nanosleep(32);
-        __syncwarp();
-      }
-      if (g < C.rows) {
-        float* dst = s_mo + (warp * kMergeRows + g) * D;
+    if (pv.wph == 1) {
+      // ---- one warp owns this head: output rows or the split partial
 #pragma unroll
-        for (int n = 0; n < NT; ++n) *reinterpret_cast<float2*>(dst + n * 8 + 2 * t4) = make_float2(o[n][0], o[n][1]);
-        if (t4 == 0) {
-          s_ml[(warp * kMergeRows + g) * 2] = m0;
-          s_ml[(warp * kMergeRows + g) * 2 + 1] = l0;
-        }
-      }
-      // the warp barrier orders the lanes' shared stores before lane 0's
-      // shared atomic; shared memory is coherent within the SM, and no
-      // __threadfence_block here: MEMBAR would also wait for this warp's
-      // in-flight cp.async prefetches of the next item
-      __syncwarp();
-      int last = 0;
-      if (lane == 0) last = atomicAdd(&s_sync[0], 1) == kWarpsTc - 1;
-      last = __shfl_sync(0xffffffffu, last, 0);
-      trace(4 + 3 * int(k));
-      if (last) {
-        warp_merge_item<D>(p, C, out_base, s_mo, s_ml, lane, s_sync, static_cast<int>(k));
-        if (C.nsplit > 1) {
-          // publish the global partial; the last CTA of this (query, head
-          // group) queues the split merge for the end of the kernel
-          __syncwarp();
-          int overflow = 0;
-          if (lane == 0) {
-            const unsigned prev =
-                atom_inc_acq_rel(merge_cnt + (int64_t(C.qi) * p.head_items + C.hi), C.nsplit - 1);
-            if (prev == static_cast<unsigned>(C.nsplit - 1)) {
-              const int idx = atomicAdd(&s_sync[2], 1);
-              if (idx < kMaxPending) s_pend[idx] = item_of(b, k, G); else overflow = 1;
-            }
+      for (int n = 0; n < NT; ++n) {
+        const int d = n * 8 + 2 * t4;
+        if (C.nsplit == 1) {
+          if (g < C.rows) {
+            store_from_float(p.out, out_base + int64_t(g) * D + d, p.out_dtype, o[n][0] / l0);
+            store_from_float(p.out, out_base + int64_t(g) * D + d + 1, p.out_dtype, o[n][1] / l0);
           }
-          overflow = __shfl_sync(0xffffffffu, overflow, 0);
-          if (overflow) merge_global_warp<D>(p, C, out_base, lane);
+          if (ROWS16 && g + 8 < C.rows) {
+            store_from_float(p.out, out_base + int64_t(g + 8) * D + d, p.out_dtype, o[n][2] / l1);
+            store_from_float(p.out, out_base + int64_t(g + 8) * D + d + 1, p.out_dtype, o[n][3] / l1);
+          }
+        } else {
+          if (g < C.rows) __stcg(reinterpret_cast<float2*>(p.ws_o + (pslot + g) * D + d), make_float2(o[n][0], o[n][1]));
+          if (ROWS16 && g + 8 < C.rows)
+            __stcg(reinterpret_cast<float2*>(p.ws_o + (pslot + g + 8) * D + d), make_float2(o[n][2], o[n][3]));
         }
       }
+      if (C.nsplit > 1 && t4 == 0) {
+        if (g < C.rows) __stcg(reinterpret_cast<float2*>(p.ws_ml) + pslot + g, make_float2(m0, l0));
+        if (ROWS16 && g + 8 < C.rows) __stcg(reinterpret_cast<float2*>(p.ws_ml) + pslot + g + 8, make_float2(m1, l1));
+      }
+      trace(5 + 4 * int(k));
       continue;
     }
 
-    // ---- synchronous CTA merge (more than kMergeRows rows), kMergeRows per pass
-    for (int rb = 0; rb < C.rows; rb += kMergeRows) {
-      // publish this warp's rows [rb, rb + 4)
-      {
-        const int rl = (rb < 8 ? g : g + 8) - rb;  // local row of this lane's fragment
-        const bool mine = rl >= 0 && rl < kMergeRows;
-        if (mine) {
-          float* dst = s_mo + (warp * kMergeRows + rl) * D;
-#pragma unroll
-          for (int n = 0; n < NT; ++n) {
-            const float x0 = rb < 8 ? o[n][0] : o[n][2];
-            const float x1 = rb < 8 ? o[n][1] : o[n][3];
-            *reinterpret_cast<float2*>(dst + n * 8 + 2 * t4) = make_float2(x0, x1);
-          }
-          if (t4 == 0) {
-            s_ml[(warp * kMergeRows + rl) * 2] = rb < 8 ? m0 : m1;
-            s_ml[(warp * kMergeRows + rl) * 2 + 1] = rb < 8 ? l0 : l1;
-          }
-        }
-      }
-      __syncthreads();
-      const int nrows = min(kMergeRows, C.rows - rb);
-      for (int e = threadIdx.x; e < nrows * D; e += kThreadsTc) {
-        const int rl = e / D, d = e - rl * D;
-        float mx = -INFINITY;
-#pragma unroll
-        for (int w = 0; w < kWarpsTc; ++w) mx = fmaxf(mx, s_ml[(w * kMergeRows + rl) * 2]);
-        float den = 0.f, acc = 0.f;
-#pragma unroll
-        for (int w = 0; w < kWarpsTc; ++w) {
-          const float mw = s_ml[(w * kMergeRows + rl) * 2];
-          const float wgt = mw == -INFINITY ? 0.f : exp2f(mw - mx);
-          den += wgt * s_ml[(w * kMergeRows + rl) * 2 + 1];
-          acc += wgt * s_mo[(w * kMergeRows + rl) * D + d];
-        }
-        if (C.nsplit == 1) {
-          store_from_float(p.out, out_base + int64_t(rb + rl) * D + d, p.out_dtype, acc / den);
-        } else {
-          const int64_t slot = int64_t(C.slot) * p.hq + C.qh0 + rb + rl;
-          __stcg(p.ws_o + slot * D + d, acc);
-          if (d == 0) __stcg(reinterpret_cast<float2*>(p.ws_ml) + slot, make_float2(mx, den));
-        }
-      }
-      __syncthreads();
+    // ---- WPH warps share this head: asynchronous shared-memory merge.  A
+    // warp overwrites its slot only after the head's previous item merged;
+    // the last of the head's warps to arrive merges in warp order.
+    if (k > 0) {
+      if (lane == 0)
+        while (*reinterpret_cast<volatile int*>(&s_done[head_local]) < static_cast<int>(k)) __nanosleep(32);
+      __syncwarp();
     }
-    trace(4 + 3 * int(k));
-    if (C.nsplit == 1) continue;
-
-    // ---- split partial published by every thread (ordered by the barrier
-    // above); the last CTA of this (query, head group) queues the merge
-    if (threadIdx.x == 0) {
-      s_hdr[1] = 0;
-      const unsigned prev = atom_inc_acq_rel(merge_cnt + (int64_t(C.qi) * p.head_items + C.hi), C.nsplit - 1);
-      if (prev == static_cast<unsigned>(C.nsplit - 1)) {
-        const int idx = s_sync[2]++;
-        if (idx < kMaxPending) s_pend[idx] = item_of(b, k, G); else s_hdr[1] = 1;
+    if (g < C.rows) {  // rows <= kMergeRows when wph > 1 (planner)
+      float* dst = s_mo + (warp * kMergeRows + g) * D;
+#pragma unroll
+      for (int n = 0; n < NT; ++n) *reinterpret_cast<float2*>(dst + n * 8 + 2 * t4) = make_float2(o[n][0], o[n][1]);
+      if (t4 == 0) {
+        s_ml[(warp * kMergeRows + g) * 2] = m0;
+        s_ml[(warp * kMergeRows + g) * 2 + 1] = l0;
       }
     }
-    __syncthreads();
-    if (s_hdr[1]) merge_global<D>(p, C, out_base, s_mo);  // queue overflow: merge now
-    __syncthreads();
+    __syncwarp();
+    int last = 0;
+    if (lane == 0) last = atomicAdd(&s_arr[head_local], 1) == pv.wph - 1;
+    last = __shfl_sync(0xffffffffu, last, 0);
+    trace(5 + 4 * int(k));
+    if (!last) continue;
+    constexpr int E = D / 32;
+    float acc[kMergeRows][E], rmx[kMergeRows], rden[kMergeRows];
+    const int w0 = head_local * pv.wph;
+#pragma unroll
+    for (int r = 0; r < kMergeRows; ++r) {
+      if (r >= C.rows) break;
+      float mx = -INFINITY;
+      for (int w = w0; w < w0 + pv.wph; ++w) mx = fmaxf(mx, s_ml[(w * kMergeRows + r) * 2]);
+      float den = 0.f;
+#pragma unroll
+      for (int e = 0; e < E; ++e) acc[r][e] = 0.f;
+      for (int w = w0; w < w0 + pv.wph; ++w) {
+        const float mw = s_ml[(w * kMergeRows + r) * 2];
+        const float wgt = mw == -INFINITY ? 0.f : exp2f(mw - mx);
+        den += wgt * s_ml[(w * kMergeRows + r) * 2 + 1];
+#pragma unroll
+        for (int e = 0; e < E; ++e) acc[r][e] += wgt * s_mo[(w * kMergeRows + r) * D + lane + 32 * e];
+      }
+      rmx[r] = mx;
+      rden[r] = den;
+    }
+    __syncwarp();
+    if (lane == 0) {  // release the head's slots before touching global memory
+      s_arr[head_local] = 0;
+      *reinterpret_cast<volatile int*>(&s_done[head_local]) = static_cast<int>(k) + 1;
+    }
+#pragma unroll
+    for (int r = 0; r < kMergeRows; ++r) {
+      if (r >= C.rows) break;
+#pragma unroll
+      for (int e = 0; e < E; ++e) {
+        const int d = lane + 32 * e;
+        if (C.nsplit == 1)
+          store_from_float(p.out, out_base + int64_t(r) * D + d, p.out_dtype, acc[r][e] / rden[r]);
+        else
+          __stcg(p.ws_o + (pslot + r) * D + d, acc[r][e]);
+      }
+      if (C.nsplit > 1 && lane == 0) __stcg(reinterpret_cast<float2*>(p.ws_ml) + pslot + r, make_float2(rmx[r], rden[r]));
+    }
   }
-  // ---- queued split merges, cooperatively by the whole CTA
   cp_async_wait<0>();
-  __syncthreads();
-  const int npend = s_sync[2];
-  for (int i = 0; i < npend && i < kMaxPending; ++i) {
-    const Item M = make_item(s_pend[i], pv, p);
-    merge_global<D>(p, M, (int64_t(M.qi) * p.hq + M.qh0) * D, s_mo);
-    __syncthreads();
+  trace(31);
+}
+
+// K2c: merge the split partials of every (query with > 1 split, query head).
+// One warp per (query, head, 32-wide slice of D); ascending split order.
+template <int D>
+__global__ void __launch_bounds__(256) combine_tc_kernel(const __grid_constant__ TcParams p) {
+  asm volatile("griddepcontrol.wait;" ::: "memory");  // decode grid done + flushed
+  const int nq = p.nq;
+  const int32_t* plan = p.plan;
+  const int nsq = plan[H_NSPLIT_Q];
+  const int32_t* cq = plan + o_cq(nq);
+  const int32_t* nsplit = plan + o_nsplit(nq);
+  const int32_t* soff = plan + o_soff(nq);
+  const int lane = threadIdx.x & 31;
+  constexpr int SL = D / 32;
+  const int64_t tasks = int64_t(nsq) * p.hq * SL;
+  const float2* ml = reinterpret_cast<const float2*>(p.ws_ml);
+  for (int64_t t = int64_t(blockIdx.x) * 8 + (threadIdx.x >> 5); t < tasks; t += int64_t(gridDim.x) * 8) {
+    const int sl = static_cast<int>(t % SL);
+    const int64_t r = t / SL;
+    const int qh = static_cast<int>(r % p.hq);
+    const int q = cq[r / p.hq];
+    const int ns = nsplit[q], s0 = soff[q];
+    float mx = -INFINITY;
+    for (int s = lane; s < ns; s += 32) mx = fmaxf(mx, __ldcg(ml + (int64_t(s0 + s) * p.hq + qh)).x);
+#pragma unroll
+    for (int o = 16; o; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    float den = 0.f;
+    for (int s = lane; s < ns; s += 32) {
+      const float2 v = __ldcg(ml + (int64_t(s0 + s) * p.hq + qh));
+      den += exp2f(v.x - mx) * v.y;
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) den += __shfl_xor_sync(0xffffffffu, den, o);
+    const int d = sl * 32 + lane;
+    float acc = 0.f;
+    for (int sb = 0; sb < ns; sb += 8) {
+      float wv[8], ov[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int64_t slot = int64_t(s0 + sb + u) * p.hq + qh;
+        const bool in = sb + u < ns;
+        wv[u] = in ? __ldcg(ml + slot).x : -INFINITY;
+        ov[u] = in ? __ldcg(p.ws_o + slot * D + d) : 0.f;
+      }
+#pragma unroll
+      for (int u = 0; u < 8; ++u) acc += (wv[u] == -INFINITY ? 0.f : exp2f(wv[u] - mx)) * ov[u];
+    }
+    store_from_float(p.out, (int64_t(q) * p.hq + qh) * D + d, p.out_dtype, acc / den);
   }
-  trace(kTraceSlots - 1);
 }
 
 template <typename T, int D>
@@ -884,28 +633,180 @@ TcFn pick_rows(bool splitq, bool rows16) {
   return rows16 ? decode_tc_kernel<T, D, false, true> : decode_tc_kernel<T, D, false, false>;
 }
 
-int pow2_at_least(int n) {
-  int x = 1;
-  while (x < n) x <<= 1;
-  return x;
-}
-
 }  // namespace
 
 bool decode_tc_supported(int kv_dtype, int head_dim) {
   return (kv_dtype == PKV_BF16 || kv_dtype == PKV_F16) && (head_dim == 64 || head_dim == 128);
 }
 
-int64_t decode_tc_plan_bytes(int64_t nq) {
-  // int32 header + 6 arrays, then the int64 sort scratch
-  const int64_t ints = 4 + 6 * nq + 2;
-  const int64_t al = (ints * 4 + 255) / 256 * 256;
-  return al + 8 * int64_t(pow2_at_least(static_cast<int>(nq)));
+constexpr int kMaxGrid = 1024;
+constexpr int kMaxWaves = 8;
+int64_t decode_plan_ints(int64_t nq, int hq) {
+  // cq[nq] + cta_off[grid+1] + cta_items[<= waves*grid + nq*hq]
+  return o_cq(nq) + nq + (kMaxGrid + 1) + (int64_t(kMaxWaves) * kMaxGrid + nq * hq);
 }
 
-int launch_decode_tc(TcParams p, int kv_dtype, int head_dim, int num_sms, cudaStream_t stream) {
+// Host planner: head blocking, even page splits, size-sorted item order.
+int plan_decode(const int32_t* nk, const int32_t* row, int64_t nq, int page_size, int hq, int hkv,
+                int num_sms, int waves, int32_t* out, int64_t cap, int64_t* n_out) {
+  if (cap < decode_plan_ints(nq, hq)) return fail(PKV_VALUE_ERROR, "plan buffer too small");
+  num_sms = std::min(num_sms, kMaxGrid);
+  waves = std::min(waves, kMaxWaves);  // <= 0: search
+  const int G = hq / hkv;
+  const int ps = page_size;
+  std::vector<int64_t> pages(nq);
+  int64_t total_pages = 0, max_pages = 0;
+  for (int64_t i = 0; i < nq; ++i) {
+    pages[i] = (int64_t(nk[i]) + ps - 1) / ps;
+    total_pages += pages[i];
+    max_pages = std::max(max_pages, pages[i]);
+  }
+  // head block: one warp per kv head when there are enough (query, head
+  // block) units to fill the GPU, otherwise several warps per head
+  int hb = 1;
+  for (int cand : {8, 4, 2, 1}) {
+    if (hkv % cand) continue;
+    const int wph = kWarpsTc / cand;
+    const int qgs = wph == 1 ? 16 : kMergeRows;
+    const int64_t units = nq * (hkv / cand) * ((G + qgs - 1) / qgs);
+    hb = cand;
+    if (units * 2 >= num_sms) break;
+  }
+  const int wph = kWarpsTc / hb;
+  const int qgs = wph == 1 ? 16 : kMergeRows;
+  const int qgroups = (G + qgs - 1) / qgs;
+  const int head_items = (hkv / hb) * qgroups;
+  const int64_t min_sp = (int64_t(2) * kCh * wph + ps - 1) / ps;  // >= 2 chunks per warp
+  std::vector<int32_t> ns(nq), order(nq);
+  std::vector<int64_t> size(nq);
+  // split size for `w` waves; the item cost model (head-pages plus a fixed
+  // per-item overhead) drives both the choice and the LPT assignment
+  auto split_for = [&](int w) {
+    const int64_t target = int64_t(num_sms) * w;
+    const int64_t sp = (total_pages * head_items + target - 1) / target;
+    return std::max<int64_t>({sp, min_sp, (max_pages + 255) / 256, 1});
+  };
+  auto build = [&](int64_t sp) {
+    for (int64_t i = 0; i < nq; ++i) {
+      ns[i] = static_cast<int32_t>(std::max<int64_t>(1, (pages[i] + sp - 1) / sp));
+      size[i] = (pages[i] + ns[i] - 1) / ns[i];
+    }
+    std::iota(order.begin(), order.end(), 0);
+    std::stable_sort(order.begin(), order.end(), [&](int32_t a, int32_t b) { return size[a] > size[b]; });
+  };
+  auto makespan = [&](int grid) {
+    std::vector<int64_t> load(grid, 0);
+    std::priority_queue<std::pair<int64_t, int>, std::vector<std::pair<int64_t, int>>, std::greater<>> heap;
+    for (int c = 0; c < grid; ++c) heap.emplace(0, c);
+    int64_t worst = 0;
+    for (int64_t j = 0; j < nq; ++j) {
+      const int32_t q = order[j];
+      const int64_t cost = size[q] * hb + kItemOverhead;
+      for (int64_t t = 0; t < int64_t(ns[q]) * head_items; ++t) {
+        auto top = heap.top();
+        heap.pop();
+        top.first += cost;
+        worst = std::max(worst, top.first);
+        heap.push(top);
+      }
+    }
+    return worst;
+  };
+  int64_t best_sp = split_for(std::max(1, waves));
+  if (waves <= 0) {  // search the wave count with the smallest predicted makespan
+    int64_t best = -1;
+    for (int w : {1, 2, 3, 4, 5, 6, 8}) {
+      const int64_t sp = split_for(w);
+      build(sp);
+      int64_t items = 0;
+      for (int64_t i = 0; i < nq; ++i) items += int64_t(ns[i]) * head_items;
+      const int grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(num_sms, items)));
+      const int64_t m = makespan(grid);
+      if (best < 0 || m < best) {
+        best = m;
+        best_sp = sp;
+      }
+    }
+  }
+  build(best_sp);
+  int32_t* o = out;
+  o[H_HB] = hb;
+  o[H_WPH] = wph;
+  o[H_QGS] = qgs;
+  o[H_QGROUPS] = qgroups;
+  o[H_HEAD_ITEMS] = head_items;
+  o[H_NQ] = static_cast<int32_t>(nq);
+  for (int h = H_GRID; h < kHdr; ++h) o[h] = 0;
+  int64_t acc = 0;
+  for (int64_t j = 0; j < nq; ++j) {
+    o[o_order(nq) + j] = order[j];
+    o[o_ioff(nq) + j] = static_cast<int32_t>(acc);
+    acc += int64_t(ns[order[j]]) * head_items;
+  }
+  if (acc > (int64_t(1) << 31) - 1) return fail(PKV_CONFIG_ERROR, "too many work items");
+  o[o_ioff(nq) + nq] = static_cast<int32_t>(acc);
+  o[H_TOTAL_ITEMS] = static_cast<int32_t>(acc);
+  int64_t s = 0, nsq = 0;
+  for (int64_t i = 0; i < nq; ++i) {
+    o[o_nsplit(nq) + i] = ns[i];
+    o[o_soff(nq) + i] = static_cast<int32_t>(s);
+    s += ns[i];
+    o[o_nk(nq) + i] = nk[i];
+    o[o_row(nq) + i] = row[i];
+    if (ns[i] > 1) o[o_cq(nq) + nsq++] = static_cast<int32_t>(i);
+  }
+  o[o_soff(nq) + nq] = static_cast<int32_t>(s);
+  o[H_NSPLIT_Q] = static_cast<int32_t>(nsq);
+
+  // greedy LPT: items in size order (largest first) to the least-loaded CTA;
+  // cost = pages of the split plus a fixed per-item overhead
+  const int64_t total_items = acc;
+  const int grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(num_sms, total_items)));
+  std::vector<std::vector<int32_t>> lists(grid);
+  {
+    using Load = std::pair<int64_t, int32_t>;  // (load, cta)
+    std::vector<Load> heap;
+    heap.reserve(grid);
+    for (int c = 0; c < grid; ++c) heap.emplace_back(0, c);
+    auto cmp = [](const Load& a, const Load& b) { return a > b; };  // min-heap
+    std::make_heap(heap.begin(), heap.end(), cmp);
+    int64_t gi = 0;
+    for (int64_t j = 0; j < nq; ++j) {
+      const int32_t q = order[j];
+      const int64_t cost = size[q] * hb + kItemOverhead;
+      const int64_t n_items = int64_t(ns[q]) * head_items;
+      for (int64_t t = 0; t < n_items; ++t, ++gi) {
+        std::pop_heap(heap.begin(), heap.end(), cmp);
+        Load& l = heap.back();
+        lists[l.second].push_back(static_cast<int32_t>(gi));
+        l.first += cost;
+        std::push_heap(heap.begin(), heap.end(), cmp);
+      }
+    }
+  }
+  const int64_t off_pos = o_cq(nq) + nq;
+  const int64_t items_pos = off_pos + grid + 1;
+  if (items_pos + total_items > cap) return fail(PKV_VALUE_ERROR, "plan buffer too small for %lld items",
+                                                  static_cast<long long>(total_items));
+  int64_t cur = 0;
+  for (int c = 0; c < grid; ++c) {
+    o[off_pos + c] = static_cast<int32_t>(cur);
+    for (int32_t it : lists[c]) o[items_pos + cur++] = it;
+  }
+  o[off_pos + grid] = static_cast<int32_t>(cur);
+  o[H_GRID] = grid;
+  o[H_CTA_OFF] = static_cast<int32_t>(off_pos);
+  o[H_CTA_ITEMS] = static_cast<int32_t>(items_pos);
+  if (n_out) *n_out = items_pos + total_items;
+  return PKV_OK;
+}
+
+int64_t decode_plan_max_splits(int64_t nq) { return nq * 256 + nq; }
+
+int launch_decode_tc(TcParams p, const int32_t* plan_host, int kv_dtype, int head_dim, int num_sms,
+                     cudaStream_t stream) {
   const bool splitq = p.q_dtype == PKV_F32;
-  const bool rows16 = p.group > 8;
+  const bool rows16 = plan_host[H_QGS] > 8 && p.group > 8;
   p.kv_dtype = kv_dtype;
   TcFn fn = nullptr;
   if (kv_dtype == PKV_BF16)
@@ -913,23 +814,10 @@ int launch_decode_tc(TcParams p, int kv_dtype, int head_dim, int num_sms, cudaSt
   else
     fn = head_dim == 64 ? pick_rows<__half, 64>(splitq, rows16) : pick_rows<__half, 128>(splitq, rows16);
   const int merge_bytes = kWarpsTc * kMergeRows * head_dim * 4 + kWarpsTc * kMergeRows * 2 * 4;
-  if (p.nq <= kSmemPlanMax) {
-    p.plan_global = nullptr;
-    const int plan_bytes = (6 * p.nq + 2) * 4;
-    p.merge_offset = (plan_bytes + 127) / 128 * 128;
-    // the in-CTA sort borrows the merge buffer as scratch
-    const int sort_bytes = 8 * pow2_at_least(p.nq);
-    const int merge_span = merge_bytes > sort_bytes ? merge_bytes : sort_bytes;
-    p.ring_offset = (p.merge_offset + merge_span + 1023) / 1024 * 1024;
-  } else {
-    p.merge_offset = 0;
-    p.ring_offset = (merge_bytes + 1023) / 1024 * 1024;
-    plan_tc_kernel<<<1, 1024, 0, stream>>>(p, const_cast<int32_t*>(p.plan_global),
-                                           reinterpret_cast<long long*>(p.plan_scratch),
-                                           pow2_at_least(p.nq));
-    cudaError_t e = cudaGetLastError();
-    if (e != cudaSuccess) return fail(PKV_CUDA_ERROR, "decode_tc plan launch: %s", cudaGetErrorString(e));
-  }
+  const int64_t plan_bytes = o_cq(p.nq) * 4;
+  p.plan_in_smem = p.nq <= kSmemPlanMax;
+  p.merge_offset = p.plan_in_smem ? static_cast<int>((plan_bytes + 127) / 128 * 128) : 0;
+  p.ring_offset = (p.merge_offset + merge_bytes + 1023) / 1024 * 1024;
   const int smem = p.ring_offset + kWarpsTc * kStagesTc * 2 * kCh * head_dim * 2;
   static int configured[16] = {0};
   const int key = (kv_dtype == PKV_BF16) * 8 + (head_dim == 128) * 4 + splitq * 2 + rows16;
@@ -940,9 +828,27 @@ int launch_decode_tc(TcParams p, int kv_dtype, int head_dim, int num_sms, cudaSt
       return fail(PKV_CUDA_ERROR, "decode_tc smem attribute (%d B): %s", smem, cudaGetErrorString(e));
     configured[key] = smem;
   }
-  fn<<<num_sms, kThreadsTc, smem, stream>>>(p);
+  const int grid = plan_host[H_GRID];  // the planner's LPT assignment is per CTA
+  fn<<<grid, kThreadsTc, smem, stream>>>(p);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return fail(PKV_CUDA_ERROR, "decode_tc launch: %s", cudaGetErrorString(e));
+  const int nsq = plan_host[H_NSPLIT_Q];
+  if (nsq > 0) {
+    const int64_t tasks = int64_t(nsq) * p.hq * (head_dim / 32);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(static_cast<unsigned>(std::min<int64_t>((tasks + 7) / 8, int64_t(num_sms) * 8)));
+    cfg.blockDim = dim3(256);
+    cfg.dynamicSmemBytes = 0;
+    cfg.stream = stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    e = head_dim == 64 ? cudaLaunchKernelEx(&cfg, combine_tc_kernel<64>, p)
+                       : cudaLaunchKernelEx(&cfg, combine_tc_kernel<128>, p);
+    if (e != cudaSuccess) return fail(PKV_CUDA_ERROR, "combine launch: %s", cudaGetErrorString(e));
+  }
   return PKV_OK;
 }
 

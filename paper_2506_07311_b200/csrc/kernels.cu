@@ -633,7 +633,7 @@ int pkv_kv_append(const void* k_new, const void* v_new, int64_t n_tok, const int
 int64_t pkv_attention_workspace_bytes(int64_t n_queries, int32_t hq, int32_t head_dim) {
   const int64_t splits = n_queries + kMaxExtraSplits;
   auto up = [](int64_t x) { return (x + 255) / 256 * 256; };
-  const int64_t plan = std::max<int64_t>(4 * (4 + n_queries + 1), decode_tc_plan_bytes(n_queries));
+  const int64_t plan = 4 * (4 + n_queries + 1);
   return up(plan) + up(4 * splits * hq * 2) + up(4 * splits * hq * head_dim);
 }
 
@@ -668,10 +668,9 @@ int pkv_paged_attention(const pkv_attention_args* a, void* stream_) {
 
   auto up = [](int64_t x) { return (x + 255) / 256 * 256; };
   char* ws = static_cast<char*>(a->workspace);
-  unsigned* counters = a->counters;
   int32_t* plan = reinterpret_cast<int32_t*>(ws);
   const int64_t splits = a->n_queries + kMaxExtraSplits;
-  const int64_t plan_bytes = std::max<int64_t>(4 * (4 + a->n_queries + 1), decode_tc_plan_bytes(a->n_queries));
+  const int64_t plan_bytes = 4 * (4 + a->n_queries + 1);
   float* ws_ml = reinterpret_cast<float*>(reinterpret_cast<char*>(plan) + up(plan_bytes));
   float* ws_o = reinterpret_cast<float*>(reinterpret_cast<char*>(ws_ml) + up(4 * splits * a->hq * 2));
 
@@ -684,15 +683,15 @@ int pkv_paged_attention(const pkv_attention_args* a, void* stream_) {
   }
 
   if (use_tc) {
-    if (!a->counters || a->counters_len < 2 + a->n_queries * a->hq)
-      return pkv::fail(PKV_VALUE_ERROR, "tensor-core decode needs a zeroed counters array of 2 + n_queries*hq");
-    const int qgroups = (group + 15) / 16;
+    if (!a->plan || !a->plan_host)
+      return pkv::fail(PKV_VALUE_ERROR, "tensor-core decode needs the pkv_attention_plan() plan");
+    if (a->plan_host[7] != a->n_queries)
+      return pkv::fail(PKV_VALUE_ERROR, "plan was built for %d queries, call has %lld", a->plan_host[7],
+                       static_cast<long long>(a->n_queries));
     TcParams t;
     t.q = a->q;
     t.q_dtype = a->q_dtype;
     t.nq = static_cast<int>(a->n_queries);
-    t.q_seq = a->q_seq;
-    t.q_nkeys = a->q_nkeys;
     t.k = static_cast<const char*>(a->k_cache);
     t.v = static_cast<const char*>(a->v_cache);
     t.kw = static_cast<char*>(const_cast<void*>(a->k_cache));
@@ -701,26 +700,19 @@ int pkv_paged_attention(const pkv_attention_args* a, void* stream_) {
     t.v_new = static_cast<const char*>(a->v_new);
     t.bt = a->block_table;
     t.bt_stride = a->bt_stride;
-    t.seq_row = a->seq_row;
-    t.seq_start = a->seq_start;
     t.log2ps = log2ps;
     t.hq = a->hq;
     t.hkv = a->hkv;
     t.group = group;
-    t.qgroups = qgroups;
-    t.head_items = a->hkv * qgroups;
     t.row_stride = int64_t(a->hkv) * a->head_dim * 2;
     t.qscale = a->scale * kLog2e;
     t.out = a->out;
     t.out_dtype = a->out_dtype;
-    t.target_items = int64_t(num_sms) * waves;  // CTA-sized items
-    t.plan_global = plan;                        // used only when nq > kSmemPlanMax
-    t.plan_scratch = reinterpret_cast<char*>(plan) + up(4 * (4 + 6 * a->n_queries + 2));
+    t.plan = a->plan;
     t.ws_ml = ws_ml;
     t.ws_o = ws_o;
-    t.counters = counters;
     if (a->prof_start) cudaEventRecord(static_cast<cudaEvent_t>(a->prof_start), stream);
-    const int st = launch_decode_tc(t, a->kv_dtype, a->head_dim, num_sms, stream);
+    const int st = launch_decode_tc(t, a->plan_host, a->kv_dtype, a->head_dim, num_sms, stream);
     if (st != PKV_OK) return st;
     if (a->prof_stop) cudaEventRecord(static_cast<cudaEvent_t>(a->prof_stop), stream);
     return PKV_OK;
@@ -800,6 +792,29 @@ int pkv_paged_attention(const pkv_attention_args* a, void* stream_) {
 }
 
 }  // extern "C"
+
+extern "C" int64_t pkv_attention_plan_ints(int64_t n_queries, int32_t hq) {
+  return pkv::decode_plan_ints(n_queries, hq);
+}
+
+extern "C" int pkv_attention_plan(const int32_t* q_nkeys, const int32_t* q_row, int64_t n_queries,
+                                  int32_t page_size, int32_t hq, int32_t hkv, int32_t num_sms,
+                                  int32_t target_waves, int32_t* plan_out, int64_t cap, int64_t* n_out) {
+  if (n_queries <= 0) return pkv::fail(PKV_VALUE_ERROR, "no queries");
+  if (hq <= 0 || hkv <= 0 || hq % hkv) return pkv::fail(PKV_SHAPE_MISMATCH, "bad head counts");
+  if (page_size <= 0 || (page_size & (page_size - 1)))
+    return pkv::fail(PKV_VALUE_ERROR, "page_size must be a power of two");
+  if (num_sms <= 0) {
+    if (!g_num_sms) {
+      int32_t n = 0;
+      pkv_device_sm_count(&n);
+      g_num_sms = n > 0 ? n : 148;
+    }
+    num_sms = g_num_sms;
+  }
+  return pkv::plan_decode(q_nkeys, q_row, n_queries, page_size, hq, hkv, num_sms,
+                          target_waves, plan_out, cap, n_out);
+}
 
 extern "C" int pkv_debug_trace(int32_t enable, uint64_t* out, int64_t n) {
   return pkv::debug_trace(enable, out, n);

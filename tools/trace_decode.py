@@ -1,14 +1,22 @@
-"""Per-CTA timeline of one tensor-core decode launch (debug)."""
-import ctypes as C, sys, numpy as np, torch
+"""Per-warp timeline of one tensor-core decode launch (debug).
+
+    python tools/trace_decode.py B CTX     # C3 GQA shape, B sequences of CTX
+    python tools/trace_decode.py 0         # C2 (MHA 32x128, 32 mixed lengths)
+"""
+import ctypes as C
+import sys
+
+import numpy as np
+import torch
+
 sys.path.insert(0, '.')
-import bench
-from paper_2506_07311_b200 import _lib, MaskMeta, paged_attention
-from paper_2506_07311_b200.batch import DecodeBatch
+import bench  # noqa: E402
+from paper_2506_07311_b200 import MaskMeta, _lib, paged_attention  # noqa: E402
 
 B = int(sys.argv[1]) if len(sys.argv) > 1 else 1
 ctx = int(sys.argv[2]) if len(sys.argv) > 2 else 8192
 dev = torch.device('cuda', 0)
-if B == 0:  # C2: MHA 32x128, 32 mixed lengths
+if B == 0:
     from oracle.workloads import config_lengths
     lens = config_lengths("c2")
     B = len(lens)
@@ -16,44 +24,52 @@ if B == 0:  # C2: MHA 32x128, 32 mixed lengths
 else:
     pool, store, cfg = bench.build_cache([ctx] * B, 32, 8, 128, 16, 4, dev)
 meta = MaskMeta.decode(store.batch_view(list(range(B))))
-q = torch.randn((B, 32, 128), device=dev).bfloat16()
-ends = []
+q = torch.randn((B, cfg.head_count, 128), device=dev).bfloat16()
 lib = _lib.load()
 for _ in range(3):
     paged_attention(q, store, meta, cfg)
 flush = torch.ones(64 << 20, device=dev)
-flush.sum(); torch.cuda.synchronize()
-print("trace on:", lib.pkv_debug_trace(1, None, 0), lib.pkv_last_error())
+flush.sum()
+torch.cuda.synchronize()
+lib.pkv_debug_trace(1, None, 0)
 paged_attention(q, store, meta, cfg)
 torch.cuda.synchronize()
-buf = (C.c_uint64 * (148 * 64))()
-print("trace read:", lib.pkv_debug_trace(-1, buf, 148 * 64), lib.pkv_last_error(), buf[0], buf[1], buf[63])
+n = 256 * 8 * 32
+buf = (C.c_uint64 * n)()
+lib.pkv_debug_trace(-1, buf, n)
 lib.pkv_debug_trace(0, None, 0)
-t = np.array(buf, dtype=np.float64).reshape(148, 64)
-t0 = t[:, 0][t[:, 0] > 0].min()
+t = np.array(buf, dtype=np.float64).reshape(256, 8, 32)[:148]
+t0 = t[:, :, 0][t[:, :, 0] > 0].min()
 rel = np.where(t > 0, (t - t0) / 1000.0, np.nan)
-print("start spread (us): %.2f..%.2f" % (np.nanmin(rel[:, 0]), np.nanmax(rel[:, 0])))
-print("plan done: median %.2f max %.2f" % (np.nanmedian(rel[:, 1]), np.nanmax(rel[:, 1])))
-print("end: median %.2f max %.2f" % (np.nanmedian(rel[:, 63]), np.nanmax(rel[:, 63])))
-busy = []
-for b in range(148):
-    tot = 0.0
-    for k in range(20):
-        s, c = rel[b, 2 + 3 * k], rel[b, 3 + 3 * k]
-        if np.isnan(s):
-            break
-        tot += c - s
-    busy.append(tot)
-print("streaming time per CTA: mean %.1f min %.1f max %.1f; items per CTA: %s" % (
-    np.mean(busy), np.min(busy), np.max(busy),
-    np.bincount([sum(1 for k in range(20) if not np.isnan(rel[b, 2 + 3 * k])) for b in range(148)])))
-ends = np.sort(rel[:, 63])
-print("end-time deciles:", np.round(ends[::15], 1))
-for b in [0, 1, 40, 100, 147]:
-    items = []
-    for k in range(20):
-        s, c, m = rel[b, 2 + 3 * k], rel[b, 3 + 3 * k], rel[b, 4 + 3 * k]
-        if np.isnan(s):
-            break
-        items.append("[%.1f chunks-done %.1f merged %.1f]" % (s, c, m))
-    print("cta", b, "start %.1f plan %.1f" % (rel[b, 0], rel[b, 1]), " ".join(items), "end %.1f" % rel[b, 63])
+print("kernel span (us): %.1f   plan done median %.2f" % (np.nanmax(rel[:, :, 31]), np.nanmedian(rel[:, :, 1])))
+gaps = {"start->first data": [], "first data->chunks done": [], "chunks done->stored": [],
+        "stored->next start": []}
+for c in range(148):
+    for w in range(8):
+        for k in range(7):
+            s, f, d, st = rel[c, w, 2 + 4 * k: 6 + 4 * k]
+            if np.isnan(s):
+                break
+            if not np.isnan(f):
+                gaps["start->first data"].append(f - s)
+                gaps["first data->chunks done"].append(d - f)
+            gaps["chunks done->stored"].append(st - d)
+            nxt = rel[c, w, 2 + 4 * (k + 1)] if k < 6 else np.nan
+            if not np.isnan(nxt):
+                gaps["stored->next start"].append(nxt - st)
+for k_, v in gaps.items():
+    v = np.array(v)
+    print("%-26s n=%5d mean %6.2f  p50 %6.2f  p90 %6.2f  max %6.2f  sum/warp %6.2f" % (
+        k_, v.size, v.mean(), np.median(v), np.percentile(v, 90), v.max(), v.sum() / (148 * 8)))
+ends = np.nanmax(rel[:, :, 31], axis=1)
+print("CTA end deciles:", np.round(np.sort(ends)[::15], 1))
+for c in [0, int(np.nanargmax(ends))]:
+    print("cta", c)
+    for w in range(8):
+        items = []
+        for k in range(7):
+            s, f, d, st = rel[c, w, 2 + 4 * k: 6 + 4 * k]
+            if np.isnan(s):
+                break
+            items.append("[%.1f f%.1f d%.1f s%.1f]" % (s, f, d, st))
+        print("  w%d" % w, " ".join(items), "end %.1f" % rel[c, w, 31])
