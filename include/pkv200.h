@@ -225,34 +225,44 @@ int pkv_attention_plan(const int32_t* q_nkeys, const int32_t* q_row, int64_t n_q
 int64_t pkv_attention_workspace_bytes(int64_t n_queries, int32_t hq, int32_t head_dim);
 int pkv_paged_attention(const pkv_attention_args* args, void* stream);
 
-/* K3   causal / suffix prefill on tcgen05 tensor cores (bf16 only).
- * Queries of sequence s are the q_len[s] consecutive positions ending at
- * seq_len[s]-1 (MaskMeta.suffix / self_attention, attention.py:81-110),
- * stored contiguously from q_start[s]. */
+/* K3   causal / suffix prefill on tcgen05 tensor cores (16-bit caches).
+ * Replaces _streaming_attention (attention.py:259-329) under the
+ * self-attention and suffix metas (attention.py:81-84, 98-110): the queries
+ * of view sequence s are the q_len[s] consecutive positions ending at
+ * seq_len[s]-1, stored contiguously from row q_start[s] of q.  The host
+ * planner cuts them into work items (one kv head x 128/G query positions,
+ * longest first); the caller uploads the plan and passes both copies. */
 typedef struct pkv_prefill_args {
-  const void* q;             /* [total_q, hq, head_dim] bf16 */
-  int32_t n_seqs;
-  const int32_t* q_start;    /* [n_seqs] */
-  const int32_t* q_len;      /* [n_seqs] */
-  const int32_t* seq_len;    /* [n_seqs] keys of each sequence */
-  const int32_t* seq_row;    /* [n_seqs] mirror rows */
-  const void* k_cache;       /* bf16 [rows, hkv, head_dim] */
+  const void* q;             /* [total_q, hq, head_dim], same dtype as the cache */
+  int64_t total_q;
+  const void* k_cache;       /* [cache_rows, hkv, head_dim] */
   const void* v_cache;
-  const int32_t* block_table;
+  int32_t kv_dtype;          /* PKV_BF16 or PKV_F16 */
+  int64_t cache_rows;
+  const int32_t* block_table; /* device mirror */
   int64_t bt_stride;
-  int32_t page_size;
+  int32_t page_size;         /* power of two >= 8 */
   int32_t hq;
   int32_t hkv;
-  int32_t head_dim;
+  int32_t head_dim;          /* 64 or 128 */
   float scale;
   int32_t causal;
-  void* out;                 /* [total_q, hq, head_dim] */
+  void* out;                 /* [total_q, hq, head_dim], fp32 or the cache dtype */
   int32_t out_dtype;
-  int32_t max_q_len;
+  const int32_t* plan;       /* device copy of the pkv_prefill_plan() items */
+  int64_t n_items;
+  void* prof_start;          /* optional cudaEvent_t pair around the launch */
+  void* prof_stop;
 } pkv_prefill_args;
 
 int pkv_prefill_supported(int32_t hq, int32_t hkv, int32_t head_dim, int32_t page_size,
                           int32_t kv_dtype);
+/* int32 entries the plan of these sequences needs (8 per work item) */
+int64_t pkv_prefill_plan_ints(const int32_t* q_len, int64_t n_seqs, int32_t hq, int32_t hkv);
+/* host planner: q_start (int64), q_len, seq_len, seq_row per view sequence */
+int pkv_prefill_plan(const int64_t* q_start, const int32_t* q_len, const int32_t* seq_len,
+                     const int32_t* seq_row, int64_t n_seqs, int32_t hq, int32_t hkv,
+                     int32_t causal, int32_t* plan_out, int64_t cap, int64_t* n_items_out);
 int pkv_paged_prefill(const pkv_prefill_args* args, void* stream);
 
 /* number of SMs of the current device (0 when no device is visible) */

@@ -54,10 +54,11 @@ class AttentionArgs(C.Structure):
 
 class PrefillArgs(C.Structure):
     _fields_ = [
-        ("q", _vp), ("n_seqs", _i32), ("q_start", _vp), ("q_len", _vp), ("seq_len", _vp),
-        ("seq_row", _vp), ("k_cache", _vp), ("v_cache", _vp), ("block_table", _vp),
-        ("bt_stride", _i64), ("page_size", _i32), ("hq", _i32), ("hkv", _i32), ("head_dim", _i32),
-        ("scale", _f32), ("causal", _i32), ("out", _vp), ("out_dtype", _i32), ("max_q_len", _i32),
+        ("q", _vp), ("total_q", _i64), ("k_cache", _vp), ("v_cache", _vp), ("kv_dtype", _i32),
+        ("cache_rows", _i64), ("block_table", _vp), ("bt_stride", _i64), ("page_size", _i32),
+        ("hq", _i32), ("hkv", _i32), ("head_dim", _i32), ("scale", _f32), ("causal", _i32),
+        ("out", _vp), ("out_dtype", _i32), ("plan", _vp), ("n_items", _i64),
+        ("prof_start", _vp), ("prof_stop", _vp),
     ]
 
 
@@ -100,6 +101,8 @@ SIGNATURES = {
     "pkv_attention_plan": (C.c_int, [_vp, _vp, _i64, _i32, _i32, _i32, _i32, _i32, _vp, _i64, _P(_i64)]),
     "pkv_paged_attention": (C.c_int, [_P(AttentionArgs), _vp]),
     "pkv_prefill_supported": (C.c_int, [_i32, _i32, _i32, _i32, _i32]),
+    "pkv_prefill_plan_ints": (_i64, [_vp, _i64, _i32, _i32]),
+    "pkv_prefill_plan": (C.c_int, [_vp, _vp, _vp, _vp, _i64, _i32, _i32, _i32, _vp, _i64, _P(_i64)]),
     "pkv_paged_prefill": (C.c_int, [_P(PrefillArgs), _vp]),
     "pkv_device_sm_count": (C.c_int, [_P(_i32)]),
     "pkv_debug_trace": (C.c_int, [_i32, _P(_u64), _i64]),
@@ -152,3 +155,22 @@ def attention_plan(q_nkeys, q_row, page_size: int, hq: int, hkv: int, target_wav
                                  target_waves, out.ctypes.data, out.size, C.byref(got)),
           "pkv_attention_plan")
     return out[: got.value].copy()
+
+
+def prefill_plan(q_start, q_len, seq_len, seq_row, hq: int, hkv: int, causal: bool):
+    """Host work plan of the tcgen05 prefill (pkv_prefill_plan) as int32 numpy
+    [n_items, 8]."""
+    import numpy as np
+
+    qs = np.ascontiguousarray(q_start, dtype=np.int64)
+    ql = np.ascontiguousarray(q_len, dtype=np.int32)
+    sl = np.ascontiguousarray(seq_len, dtype=np.int32)
+    sr = np.ascontiguousarray(seq_row, dtype=np.int32)
+    lib = load()
+    cap = int(lib.pkv_prefill_plan_ints(ql.ctypes.data, ql.size, hq, hkv))
+    out = np.empty(max(cap, 8), dtype=np.int32)
+    got = C.c_int64()
+    check(lib.pkv_prefill_plan(qs.ctypes.data, ql.ctypes.data, sl.ctypes.data, sr.ctypes.data, ql.size,
+                               hq, hkv, int(bool(causal)), out.ctypes.data, out.size, C.byref(got)),
+          "pkv_prefill_plan")
+    return out[: 8 * got.value].reshape(-1, 8).copy()

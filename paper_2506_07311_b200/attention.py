@@ -28,7 +28,7 @@ from enum import IntEnum
 import numpy as np
 
 from . import _lib
-from .errors import NoAllowedKeys, OutOfRange, ShapeMismatch
+from .errors import ConfigError, NoAllowedKeys, OutOfRange, ShapeMismatch
 from .store import BatchView, KvStore, _ptr, _stream, to_device, torch_dtype
 
 
@@ -239,7 +239,7 @@ def _q_tensor(queries, device):
     return q, code
 
 
-PRECISION_MODES = {"auto": 0, "exact": 1, "tensor": 2}
+PRECISION_MODES = {"auto": 0, "exact": 1, "tensor": 2, "prefill": 2}
 
 
 def _launch_attention(q, qcode, meta, config, nkeys, *, k, v, kv_code, bt, bt_stride, seq_row,
@@ -283,6 +283,84 @@ def _launch_attention(q, qcode, meta, config, nkeys, *, k, v, kv_code, bt, bt_st
     return out
 
 
+PREFILL_MIN_RUN = 16  # longest per-sequence query run that makes the K3 tile worthwhile
+
+
+def suffix_runs(meta: MaskMeta):
+    """(q_start, q_len) per view sequence when the queries of every sequence
+    are one run of consecutive positions ending at its last key — the shape
+    of MaskMeta.self_attention / .suffix (attention.py:81-84, 98-110) that K3
+    executes — else None."""
+    n_seq = len(meta.view.lengths)
+    q_len = np.bincount(meta.q_seq, minlength=n_seq).astype(np.int64)
+    q_start = np.zeros(n_seq, dtype=np.int64)
+    if n_seq > 1:
+        q_start[1:] = np.cumsum(q_len)[:-1]
+    if meta.query_count == 0:
+        return q_start, q_len
+    lens = meta.view.lengths.astype(np.int64)
+    first = lens - q_len
+    idx = np.arange(meta.query_count, dtype=np.int64)
+    want = first[meta.q_seq] + idx - q_start[meta.q_seq]
+    if not np.array_equal(want, meta.q_pos):
+        return None
+    return q_start, q_len
+
+
+def _prefill_route(meta, config, kv_code, precision):
+    """Query runs for K3, or None to use K2.  "auto" sends bf16 caches with
+    runs of >= PREFILL_MIN_RUN positions (fp16 stays on the fp32 CUDA-core
+    kernel and its 1e-5 contract, like the decode dispatch); "tensor" also
+    takes fp16; "prefill" forces K3 for any suffix-shaped meta."""
+    if precision == "exact":
+        return None
+    supported = kv_code in (_lib.PKV_BF16, _lib.PKV_F16) and _lib.load().pkv_prefill_supported(
+        config.head_count, config.kv_head_count, config.head_dim, config.page_size, kv_code)
+    runs = suffix_runs(meta) if supported else None
+    if precision == "prefill":
+        if runs is None:
+            raise ConfigError("the tcgen05 prefill needs a suffix-shaped meta over a 16-bit cache with "
+                              "head_dim 64/128, page_size >= 8 and 128 % (hq/hkv) == 0")
+        return runs
+    if runs is None or (precision == "auto" and kv_code != _lib.PKV_BF16):
+        return None
+    return runs if runs[1].max(initial=0) >= PREFILL_MIN_RUN else None
+
+
+def _launch_prefill(q, meta, config, runs, *, k, v, kv_code, bt, rows, out_dtype, device, prof=None):
+    """K3: one tcgen05 launch over every sequence's query run.  Paged mode:
+    `bt` is the device block-table mirror and `rows` the mirror row of each
+    view sequence; gathered mode (bt None): `rows` is each sequence's first
+    row in the contiguous K/V."""
+    import torch
+
+    q_start, q_len = runs
+    nq = meta.query_count
+    out_t, out_code = torch_dtype(out_dtype)
+    if out_code not in (_lib.PKV_F32, kv_code):
+        out_t, out_code = torch.float32, _lib.PKV_F32
+    out = torch.empty((nq, config.head_count, config.head_dim), dtype=out_t, device=device)
+    if nq == 0:
+        return out
+    q = q.to(k.dtype).contiguous()
+    rows = np.asarray(rows, dtype=np.int64)
+    if rows.size and rows.max() >= 2 ** 31:
+        raise OutOfRange("K/V rows beyond 2^31 are not addressable")
+    plan = _lib.prefill_plan(q_start, q_len, meta.view.lengths, rows, config.head_count,
+                             config.kv_head_count, config.causal)
+    dev_plan = torch.from_numpy(plan).to(device)
+    args = _lib.PrefillArgs(
+        q=q.data_ptr(), total_q=nq, k_cache=k.data_ptr(), v_cache=v.data_ptr(),
+        kv_dtype=kv_code, cache_rows=k.shape[0], block_table=bt.data_ptr() if bt is not None else None,
+        bt_stride=bt.shape[1] if bt is not None else 0, page_size=config.page_size,
+        hq=config.head_count, hkv=config.kv_head_count, head_dim=config.head_dim,
+        scale=float(config.scale), causal=int(bool(config.causal)), out=out.data_ptr(),
+        out_dtype=out_code, plan=dev_plan.data_ptr(), n_items=plan.shape[0],
+        prof_start=prof[0] if prof else None, prof_stop=prof[1] if prof else None)
+    _lib.check(_lib.load().pkv_paged_prefill(C.byref(args), _stream(device)), "pkv_paged_prefill")
+    return out
+
+
 def paged_attention(queries, store: KvStore, meta: MaskMeta, config: AttentionConfig, *,
                     stats: KernelStats | None = None, block_mask: BlockMask | None = None,
                     skip_empty: bool = True, out_dtype=None, precision: str = "auto"):
@@ -293,7 +371,9 @@ def paged_attention(queries, store: KvStore, meta: MaskMeta, config: AttentionCo
     `precision`: "auto" runs bf16 caches on the tensor-core kernel (P rounded
     to bf16; 2e-2 contract) and fp32/fp16 caches on the fp32 CUDA-core kernel
     (1e-5 contract); "exact" forces the CUDA-core kernel, "tensor" the
-    tensor-core one."""
+    tensor-core ones, "prefill" the K3 tcgen05 prefill kernel.  Suffix /
+    self-attention metas over bf16 caches (fp16 under "tensor") with query
+    runs of >= PREFILL_MIN_RUN positions go to K3."""
     import torch
 
     _check_queries(queries, meta, config)
@@ -315,7 +395,12 @@ def paged_attention(queries, store: KvStore, meta: MaskMeta, config: AttentionCo
     device = store.device
     q, qcode = _q_tensor(queries, device)
     seq_row = np.asarray([t.mirror_row for t in tables], dtype=np.int32)
+    runs = _prefill_route(meta, config, store.dtype_code, precision)
     mirror = store.pool.device_table(device)
+    if runs is not None:
+        return _launch_prefill(q, meta, config, runs, k=store.keys, v=store.values,
+                               kv_code=store.dtype_code, bt=mirror, rows=seq_row,
+                               out_dtype=out_dtype or torch.float32, device=device)
     return _launch_attention(q, qcode, meta, config, nkeys, k=store.keys, v=store.values,
                              kv_code=store.dtype_code, bt=mirror, bt_stride=mirror.shape[1],
                              seq_row=seq_row, seq_start=None,
@@ -349,6 +434,10 @@ def gathered_attention(queries, keys, values, meta: MaskMeta, config: AttentionC
     _, kv_code = torch_dtype(k.dtype)
     q, qcode = _q_tensor(queries, device)
     seq_start = meta.view.prefix_sums.astype(np.int64)
+    runs = _prefill_route(meta, config, kv_code, precision)
+    if runs is not None:
+        return _launch_prefill(q, meta, config, runs, k=k, v=v, kv_code=kv_code, bt=None,
+                               rows=seq_start, out_dtype=out_dtype or torch.float32, device=device)
     return _launch_attention(q, qcode, meta, config, nkeys, k=k, v=v, kv_code=kv_code, bt=None,
                              bt_stride=0, seq_row=None, seq_start=seq_start,
                              out_dtype=out_dtype or torch.float32, device=device,

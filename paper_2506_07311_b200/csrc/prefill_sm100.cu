@@ -1,9 +1,598 @@
-// K3 placeholder: the tcgen05 prefill kernel lands in a later commit; until
-// then pkv_prefill_supported() reports no support and callers use K2.
-#include "pkv200.h"
-#include "status.h"
+// K3: paged causal / suffix prefill attention on the 5th-generation tensor
+// cores (tcgen05.mma, accumulators in TMEM, operands staged by TMA).
+//
+// Replaces the reference streaming kernel (attention.py:259-329) for the
+// self-attention and suffix metas (attention.py:81-84, 98-110) of 16-bit
+// caches: there the query tile times the key page really is a dense
+// contraction.
+//
+// Work item (planned on the host, pkv_prefill_plan): one kv head of one tile
+// of QT = 128 / G consecutive query positions of one sequence.  The item's
+// 128 query rows are the M dimension of the MMAs: row r = i * G + g is query
+// position q0 + i of query head kvh * G + g, so every K/V byte staged in
+// shared memory serves all G grouped query heads.  Keys stream in tiles of
+// 128 (N); each tile is gathered page by page from the paged cache with 3-D
+// TMA boxes (64 head-dim elements x 1 head x min(ps, 128) rows, 128-byte
+// swizzle) straight into the canonical K-major layout the MMA descriptors
+// describe.  Pages past the end of the block table are fetched with an
+// out-of-range row coordinate, which TMA fills with zeros.
+//
+// Warp roles (256 threads, one CTA per SM):
+//   warp 0     TMA producer: Q once, then K/V tiles through a 2-stage ring;
+//   warp 1     MMA issuer (one thread): S_j = Q K_j^T into TMEM (double
+//              buffered), then O += P_{j-1} V_{j-1} (P from shared memory,
+//              V as an MN-major operand) — QK of the next tile is in flight
+//              while the softmax works on the current one;
+//   warp 2     TMEM allocator (512 columns: S0, S1, O);
+//   warps 4-7  softmax + epilogue: thread t owns query row t (TMEM lane t),
+//              so row max / sum need no shuffles.  Online softmax in base 2
+//              with a lazily updated running max: O and l are rescaled only
+//              when the row max grows by more than 2^8 (exact — numerator
+//              and denominator share the stale max — and rare after the
+//              first tiles).  P is rounded to the operand type and written
+//              to shared memory in the swizzled K-major layout.
+//
+// Causal masking is applied only on tiles that reach past a row's last
+// allowed key; tiles entirely above the diagonal are never visited (the
+// host plan sizes each item's key range).
+#include <cuda.h>
 
-extern "C" int pkv_prefill_supported(int32_t, int32_t, int32_t, int32_t, int32_t) { return 0; }
-extern "C" int pkv_paged_prefill(const pkv_prefill_args*, void*) {
-  return pkv::fail(PKV_CONFIG_ERROR, "tcgen05 prefill not built");
+#include <algorithm>
+#include <cstring>
+#include <numeric>
+#include <vector>
+
+#include "common.cuh"
+
+namespace pkv {
+namespace {
+
+constexpr int kThreads = 256;
+constexpr int kM = 128;          // query rows per item (MMA M)
+constexpr int kN = 128;          // keys per tile (MMA N of QK^T, K of PV)
+constexpr int kRowB = 128;       // bytes per swizzled row (64 x 16-bit)
+constexpr int kChunkB = kM * kRowB;  // one 64-column chunk of a 128-row tile: 16 KB
+constexpr int kItemInts = 8;
+constexpr float kLog2eP = 1.4426950408889634f;
+constexpr float kRescaleThreshold = 8.0f;  // log2 units
+
+// ---- PTX wrappers -----------------------------------------------------------
+__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(bar), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(bar), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint32_t bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(bar) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+  uint32_t done = 0;
+  do {
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+        " selp.u32 %0, 1, 0, p;\n}\n"
+        : "=r"(done)
+        : "r"(bar), "r"(parity)
+        : "memory");
+  } while (!done);
+}
+__device__ __forceinline__ void tma_load_3d(uint32_t dst, const CUtensorMap* map, uint32_t bar, int c0,
+                                            int c1, int c2) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5}], "
+      "[%2];\n" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(bar), "r"(c0), "r"(c1), "r"(c2)
+      : "memory");
+}
+__device__ __forceinline__ void tc_fence_before() {
+  asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+}
+__device__ __forceinline__ void tc_fence_after() {
+  asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+}
+__device__ __forceinline__ void tc_commit(uint32_t bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(bar)
+               : "memory");
+}
+__device__ __forceinline__ void tc_mma(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc, uint32_t idesc,
+                                       uint32_t accumulate) {
+  asm volatile(
+      "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
+      " tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(d_tmem),
+      "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+// 32 consecutive 32-bit TMEM columns of this thread's lane
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t* v) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, "
+      "%13, %14, %15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31}, "
+      "[%32];\n"
+      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+        "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]),
+        "=r"(v[15]), "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]),
+        "=r"(v[22]), "=r"(v[23]), "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]),
+        "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
+      : "r"(taddr));
+}
+__device__ __forceinline__ void tmem_st32(uint32_t taddr, const uint32_t* v) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, "
+      "%13, %14, %15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31, "
+      "%32};\n" ::"r"(taddr),
+      "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]), "r"(v[8]),
+      "r"(v[9]), "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]), "r"(v[15]), "r"(v[16]),
+      "r"(v[17]), "r"(v[18]), "r"(v[19]), "r"(v[20]), "r"(v[21]), "r"(v[22]), "r"(v[23]), "r"(v[24]),
+      "r"(v[25]), "r"(v[26]), "r"(v[27]), "r"(v[28]), "r"(v[29]), "r"(v[30]), "r"(v[31])
+      : "memory");
+}
+__device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory"); }
+__device__ __forceinline__ void tmem_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory"); }
+
+// shared-memory matrix descriptor, 128-byte swizzle (layout type 2), sm100 version 1
+__device__ __forceinline__ uint64_t smem_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+  uint64_t d = static_cast<uint64_t>((saddr >> 4) & 0x3FFF);
+  d |= static_cast<uint64_t>((lbo >> 4) & 0x3FFF) << 16;
+  d |= static_cast<uint64_t>((sbo >> 4) & 0x3FFF) << 32;
+  d |= 1ull << 46;
+  d |= 2ull << 61;
+  return d;
+}
+// instruction descriptor of kind::f16: fp32 accumulate, 16-bit A/B of
+// format fmt (0 = f16, 1 = bf16), K-major A, B major b_mn, shape M x N
+__host__ __device__ constexpr uint32_t instr_desc(uint32_t fmt, uint32_t b_mn, uint32_t m, uint32_t n) {
+  return (1u << 4) | (fmt << 7) | (fmt << 10) | (b_mn << 16) | ((n >> 3) << 17) | ((m >> 4) << 24);
+}
+
+struct PrefillParams {
+  int hq, hkv, group, qt;  // qt = query positions per item
+  int log2ps, box_rows;     // keys per TMA box = min(page_size, 128)
+  int64_t bt_stride;
+  const int32_t* bt;
+  int32_t oob_row;          // a row coordinate past the cache: zero-filled box
+  float qscale;             // scale * log2(e)
+  int causal;
+  void* out;
+  int out_dtype;
+  const int32_t* items;
+};
+
+template <typename T>
+struct Fmt;
+template <>
+struct Fmt<__nv_bfloat16> {
+  static constexpr uint32_t kFmt = 1;
+};
+template <>
+struct Fmt<__half> {
+  static constexpr uint32_t kFmt = 0;
+};
+
+template <typename T, int D>
+__global__ void __launch_bounds__(kThreads, 1)
+    prefill_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
+                      const __grid_constant__ CUtensorMap tm_v, const __grid_constant__ PrefillParams p) {
+  constexpr int NCH = D / 64;                 // 64-column chunks of the head dim
+  constexpr int kQBytes = NCH * kChunkB;      // Q tile
+  constexpr int kKVBytes = NCH * kChunkB;     // one K (or V) tile of 128 keys
+  constexpr int kPBytes = (kN / 64) * kChunkB;
+  constexpr uint32_t kIdescQK = instr_desc(Fmt<T>::kFmt, 0, kM, kN);
+  constexpr uint32_t kIdescPV = instr_desc(Fmt<T>::kFmt, 1, kM, D);
+  constexpr uint32_t kTmemCols = 512;
+  constexpr uint32_t kColO = 2 * kN;
+
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  const uint32_t sQ = smem_addr(smem);
+  const uint32_t sK = sQ + kQBytes;                 // 2 stages
+  const uint32_t sV = sK + 2 * kKVBytes;            // 2 stages
+  const uint32_t sP = sV + 2 * kKVBytes;
+  uint8_t* sPp = smem + (sP - sQ);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + (sP - sQ) + kPBytes);
+  // barrier slots
+  enum { B_Q = 0, B_KF = 1, B_VF = 3, B_KE = 5, B_VE = 7, B_SF = 9, B_SE = 11, B_PF = 13, B_PE = 14, B_N = 15 };
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + B_N);
+  auto bar = [&](int i) { return smem_addr(bars + i); };
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const int32_t* it = p.items + static_cast<int64_t>(blockIdx.x) * kItemInts;
+  const int q_row0 = it[0], q_count = it[1], qpos0 = it[2], kv_len = it[3];
+  const int mrow = it[4], kvh = it[5], n_tiles = it[6];
+
+  if (threadIdx.x == 0) {
+    mbar_init(bar(B_Q), 1);
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(bar(B_KF + s), 1);
+      mbar_init(bar(B_VF + s), 1);
+      mbar_init(bar(B_KE + s), 1);
+      mbar_init(bar(B_VE + s), 1);
+      mbar_init(bar(B_SF + s), 1);
+      mbar_init(bar(B_SE + s), 128);
+    }
+    mbar_init(bar(B_PF), 128);
+    mbar_init(bar(B_PE), 1);
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  if (warp == 2) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(
+                     smem_addr(tmem_slot)),
+                 "r"(kTmemCols)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n" ::: "memory");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      // ---------------- TMA producer ----------------
+      asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<uint64_t>(&tm_k)) : "memory");
+      asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<uint64_t>(&tm_v)) : "memory");
+      mbar_expect_tx(bar(B_Q), kQBytes);
+      for (int c = 0; c < NCH; ++c) tma_load_3d(sQ + c * kChunkB, &tm_q, bar(B_Q), c * 64, kvh * p.group, q_row0);
+      const int ps = 1 << p.log2ps;
+      const int n_pages = (kv_len + ps - 1) >> p.log2ps;
+      const int boxes = kN / p.box_rows;
+      const int32_t* tbl = p.bt ? p.bt + static_cast<int64_t>(mrow) * p.bt_stride : nullptr;
+      for (int j = 0; j < n_tiles; ++j) {
+        const int st = j & 1;
+        // rows of this tile's boxes (block-table walk, OOB row past the table)
+        int rows[16];
+        for (int b = 0; b < boxes; ++b) {
+          const int key0 = j * kN + b * p.box_rows;
+          if (p.bt) {
+            const int pg = key0 >> p.log2ps;
+            rows[b] = pg < n_pages ? tbl[pg] * ps + (key0 & (ps - 1)) : p.oob_row;
+          } else {
+            rows[b] = mrow + key0;  // gathered: contiguous rows (past the end: zero fill)
+          }
+        }
+        if (j >= 2) mbar_wait(bar(B_KE + st), ((j >> 1) - 1) & 1);
+        mbar_expect_tx(bar(B_KF + st), kKVBytes);
+        for (int b = 0; b < boxes; ++b)
+          for (int c = 0; c < NCH; ++c)
+            tma_load_3d(sK + st * kKVBytes + c * kChunkB + b * p.box_rows * kRowB, &tm_k, bar(B_KF + st),
+                        c * 64, kvh, rows[b]);
+        if (j >= 2) mbar_wait(bar(B_VE + st), ((j >> 1) - 1) & 1);
+        mbar_expect_tx(bar(B_VF + st), kKVBytes);
+        for (int b = 0; b < boxes; ++b)
+          for (int c = 0; c < NCH; ++c)
+            tma_load_3d(sV + st * kKVBytes + c * kChunkB + b * p.box_rows * kRowB, &tm_v, bar(B_VF + st),
+                        c * 64, kvh, rows[b]);
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      // ---------------- MMA issuer ----------------
+      mbar_wait(bar(B_Q), 0);
+      tc_fence_after();
+      auto issue_pv = [&](int i) {
+        const int st = i & 1;
+        mbar_wait(bar(B_PF), i & 1);
+        mbar_wait(bar(B_VF + st), (i >> 1) & 1);
+        tc_fence_after();
+#pragma unroll
+        for (int k = 0; k < kN / 16; ++k) {
+          // A = P (K-major, 64-key chunks), B = V (MN-major: LBO = chunk stride, SBO = 8 keys)
+          const uint64_t ad = smem_desc(sP + (k >> 2) * kChunkB + (k & 3) * 32, 16, 1024);
+          const uint64_t bd = smem_desc(sV + st * kKVBytes + k * 16 * kRowB, kChunkB, 1024);
+          tc_mma(tmem + kColO, ad, bd, kIdescPV, (i > 0 || k > 0) ? 1u : 0u);
+        }
+        tc_commit(bar(B_VE + st));
+        tc_commit(bar(B_PE));
+      };
+      for (int j = 0; j < n_tiles; ++j) {
+        const int st = j & 1;
+        if (j >= 2) mbar_wait(bar(B_SE + st), ((j >> 1) - 1) & 1);
+        mbar_wait(bar(B_KF + st), (j >> 1) & 1);
+        tc_fence_after();
+#pragma unroll
+        for (int k = 0; k < D / 16; ++k) {
+          const uint64_t ad = smem_desc(sQ + (k >> 2) * kChunkB + (k & 3) * 32, 16, 1024);
+          const uint64_t bd = smem_desc(sK + st * kKVBytes + (k >> 2) * kChunkB + (k & 3) * 32, 16, 1024);
+          tc_mma(tmem + st * kN, ad, bd, kIdescQK, k > 0 ? 1u : 0u);
+        }
+        tc_commit(bar(B_KE + st));
+        tc_commit(bar(B_SF + st));
+        if (j >= 1) issue_pv(j - 1);
+      }
+      if (n_tiles > 0) issue_pv(n_tiles - 1);
+    }
+  } else if (warp >= 4) {
+    // ---------------- softmax + epilogue (thread = query row) ----------------
+    const int r = threadIdx.x - 128;
+    const uint32_t lane_base = static_cast<uint32_t>((warp & 3) * 32) << 16;
+    const int qi = r / p.group;
+    const int qpos = qpos0 + qi;
+    const int nk = p.causal ? min(qpos + 1, kv_len) : kv_len;  // allowed key prefix of this row
+    float m_used = -INFINITY, l = 0.f;
+    for (int j = 0; j < n_tiles; ++j) {
+      const int st = j & 1;
+      mbar_wait(bar(B_SF + st), (j >> 1) & 1);
+      tc_fence_after();
+      float s[kN];
+#pragma unroll
+      for (int c = 0; c < kN / 32; ++c) tmem_ld32(tmem + lane_base + st * kN + c * 32, reinterpret_cast<uint32_t*>(s + c * 32));
+      tmem_wait_ld();
+      tc_fence_before();
+      mbar_arrive(bar(B_SE + st));
+      const int kbase = j * kN;
+      if (kbase + kN > nk) {
+#pragma unroll
+        for (int c = 0; c < kN; ++c)
+          if (kbase + c >= nk) s[c] = -INFINITY;
+      }
+      float mx = s[0];
+#pragma unroll
+      for (int c = 1; c < kN; ++c) mx = fmaxf(mx, s[c]);
+      mx *= p.qscale;
+      float factor = 1.f;
+      const bool need = mx > m_used + kRescaleThreshold;
+      if (need) {
+        factor = exp2f(m_used - mx);  // 0 on the first tile (m_used = -inf)
+        m_used = mx;
+      }
+      l *= factor;
+      const float negm = -m_used;
+      uint32_t pk[kN / 2];
+#pragma unroll
+      for (int c = 0; c < kN; c += 2) {
+        const float p0 = exp2f(fmaf(s[c], p.qscale, negm));
+        const float p1 = exp2f(fmaf(s[c + 1], p.qscale, negm));
+        l += p0 + p1;
+        pk[c >> 1] = pack2<T>(p0, p1);
+      }
+      // O and the P buffer are free once PV_{j-1} completed
+      if (j > 0) {
+        mbar_wait(bar(B_PE), (j - 1) & 1);
+        tc_fence_after();
+        if (__any_sync(0xffffffffu, need)) {
+#pragma unroll 1
+          for (int c = 0; c < D / 32; ++c) {
+            uint32_t o[32];
+            tmem_ld32(tmem + lane_base + kColO + c * 32, o);
+            tmem_wait_ld();
+#pragma unroll
+            for (int e = 0; e < 32; ++e) o[e] = __float_as_uint(__uint_as_float(o[e]) * factor);
+            tmem_st32(tmem + lane_base + kColO + c * 32, o);
+          }
+          tmem_wait_st();
+        }
+      }
+      // P row -> swizzled K-major smem (16-byte chunk q of 64-key chunk kc)
+#pragma unroll
+      for (int q = 0; q < kN / 8; ++q) {
+        const int kc = q >> 3, inner = q & 7;
+        uint8_t* dst = sPp + kc * kChunkB + r * kRowB + ((inner ^ (r & 7)) << 4);
+        *reinterpret_cast<uint4*>(dst) = make_uint4(pk[4 * q], pk[4 * q + 1], pk[4 * q + 2], pk[4 * q + 3]);
+      }
+      asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+      tc_fence_before();
+      mbar_arrive(bar(B_PF));
+    }
+    // epilogue: O / l for the valid rows
+    if (n_tiles > 0) {
+      mbar_wait(bar(B_PE), (n_tiles - 1) & 1);
+      tc_fence_after();
+    }
+    const bool valid = qi < q_count;
+    const float inv = l > 0.f ? 1.f / l : 0.f;
+    const int64_t orow = (static_cast<int64_t>(q_row0) + qi) * p.hq + kvh * p.group + (r - qi * p.group);
+#pragma unroll 1
+    for (int c = 0; c < D / 32; ++c) {
+      uint32_t o[32];
+      tmem_ld32(tmem + lane_base + kColO + c * 32, o);
+      tmem_wait_ld();
+      if (valid) {
+        if (p.out_dtype == PKV_F32) {
+          float4* dst = reinterpret_cast<float4*>(static_cast<float*>(p.out) + orow * D + c * 32);
+#pragma unroll
+          for (int e = 0; e < 8; ++e)
+            dst[e] = make_float4(__uint_as_float(o[4 * e]) * inv, __uint_as_float(o[4 * e + 1]) * inv,
+                                 __uint_as_float(o[4 * e + 2]) * inv, __uint_as_float(o[4 * e + 3]) * inv);
+        } else {
+          uint4* dst = reinterpret_cast<uint4*>(static_cast<uint16_t*>(p.out) + orow * D + c * 32);
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            uint32_t w[4];
+#pragma unroll
+            for (int h = 0; h < 4; ++h) {
+              const float a = __uint_as_float(o[8 * e + 2 * h]) * inv;
+              const float b = __uint_as_float(o[8 * e + 2 * h + 1]) * inv;
+              w[h] = p.out_dtype == PKV_BF16 ? pack2<__nv_bfloat16>(a, b) : pack2<__half>(a, b);
+            }
+            dst[e] = make_uint4(w[0], w[1], w[2], w[3]);
+          }
+        }
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 2) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "r"(kTmemCols)
+                 : "memory");
+  }
+}
+
+// ---- host side --------------------------------------------------------------
+using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                   const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                   CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeTiledFn encode_fn() {
+  static EncodeTiledFn fn = nullptr;
+  if (!fn) {
+    void* ptr = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &ptr, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeTiledFn>(ptr);
+  }
+  return fn;
+}
+
+// 3-D map over [dim2][dim1][dim0] 16-bit elements, box (64, box1, box2), 128-B swizzle
+int make_map(CUtensorMap* map, const void* base, int dtype, uint64_t dim0, uint64_t dim1, uint64_t dim2,
+             uint32_t box1, uint32_t box2) {
+  EncodeTiledFn fn = encode_fn();
+  if (!fn) return fail(PKV_CUDA_ERROR, "cuTensorMapEncodeTiled unavailable");
+  const cuuint64_t dims[3] = {dim0, dim1, dim2};
+  const cuuint64_t strides[2] = {dim0 * 2, dim0 * dim1 * 2};
+  const cuuint32_t box[3] = {64, box1, box2};
+  const cuuint32_t estr[3] = {1, 1, 1};
+  const CUresult r = fn(map, dtype == PKV_BF16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT16,
+                        3, const_cast<void*>(base), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                        CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                        CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(PKV_CUDA_ERROR, "cuTensorMapEncodeTiled failed (%d)", static_cast<int>(r));
+  return PKV_OK;
+}
+
+template <typename T, int D>
+size_t smem_bytes() {
+  constexpr int NCH = D / 64;
+  // at least 116 KB: one CTA per SM, so the 512-column TMEM allocation never waits
+  return std::max<size_t>(1024 + NCH * kChunkB * 5 + (kN / 64) * kChunkB + 16 * 8 + 16, 116 * 1024);
+}
+
+template <typename T, int D>
+int launch(const pkv_prefill_args* a, const PrefillParams& pp, cudaStream_t stream) {
+  CUtensorMap mq, mk, mv;
+  const int G = a->hq / a->hkv;
+  int st = make_map(&mq, a->q, a->kv_dtype, D, a->hq, a->total_q, G, kM / G);
+  if (st) return st;
+  const uint32_t box_rows = static_cast<uint32_t>(pp.box_rows);
+  st = make_map(&mk, a->k_cache, a->kv_dtype, D, a->hkv, a->cache_rows, 1, box_rows);
+  if (st) return st;
+  st = make_map(&mv, a->v_cache, a->kv_dtype, D, a->hkv, a->cache_rows, 1, box_rows);
+  if (st) return st;
+  const size_t smem = smem_bytes<T, D>();
+  auto kern = prefill_tc_kernel<T, D>;
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    attr_set = true;
+  }
+  kern<<<static_cast<unsigned>(a->n_items), kThreads, smem, stream>>>(mq, mk, mv, pp);
+  PKV_CHECK_LAUNCH();
+  return PKV_OK;
+}
+
+int query_tile(int hq, int hkv) { return kM / (hq / hkv); }
+
+}  // namespace
+}  // namespace pkv
+
+using namespace pkv;
+
+extern "C" int pkv_prefill_supported(int32_t hq, int32_t hkv, int32_t head_dim, int32_t page_size,
+                                     int32_t kv_dtype) {
+  if (hq <= 0 || hkv <= 0 || hq % hkv) return 0;
+  const int G = hq / hkv;
+  if (G > kM || kM % G) return 0;
+  if (head_dim != 64 && head_dim != 128) return 0;
+  if (page_size < 8 || (page_size & (page_size - 1))) return 0;
+  if (kv_dtype != PKV_BF16 && kv_dtype != PKV_F16) return 0;
+  return 1;
+}
+
+extern "C" int64_t pkv_prefill_plan_ints(const int32_t* q_len, int64_t n_seqs, int32_t hq, int32_t hkv) {
+  if (hq <= 0 || hkv <= 0 || hq % hkv || n_seqs < 0) return 0;
+  const int qt = query_tile(hq, hkv);
+  int64_t tiles = 0;
+  for (int64_t s = 0; s < n_seqs; ++s) tiles += (std::max(q_len[s], 0) + qt - 1) / qt;
+  return tiles * hkv * kItemInts;
+}
+
+extern "C" int pkv_prefill_plan(const int64_t* q_start, const int32_t* q_len, const int32_t* seq_len,
+                                const int32_t* seq_row, int64_t n_seqs, int32_t hq, int32_t hkv,
+                                int32_t causal, int32_t* plan_out, int64_t cap, int64_t* n_items_out) {
+  if (hq <= 0 || hkv <= 0 || hq % hkv) return fail(PKV_SHAPE_MISMATCH, "hq must be a multiple of hkv");
+  const int G = hq / hkv;
+  if (G > kM || kM % G) return fail(PKV_CONFIG_ERROR, "group size %d does not divide %d", G, kM);
+  const int qt = query_tile(hq, hkv);
+  struct Rec {
+    int32_t v[kItemInts];
+  };
+  std::vector<Rec> items;
+  for (int64_t s = 0; s < n_seqs; ++s) {
+    const int32_t ql = q_len[s], kl = seq_len[s];
+    if (ql < 0 || ql > kl) return fail(PKV_OUT_OF_RANGE, "sequence %lld: %d queries over %d keys",
+                                       static_cast<long long>(s), ql, kl);
+    if (q_start[s] + ql > (int64_t(1) << 31)) return fail(PKV_OUT_OF_RANGE, "query rows beyond 2^31");
+    for (int t = 0; t * qt < ql; ++t) {
+      const int cnt = std::min(qt, ql - t * qt);
+      const int pos0 = kl - ql + t * qt;
+      const int nk = causal ? std::min(pos0 + cnt, kl) : kl;  // keys of the last valid row
+      const int tiles = (nk + kN - 1) / kN;
+      for (int h = 0; h < hkv; ++h) {
+        Rec r;
+        r.v[0] = static_cast<int32_t>(q_start[s] + int64_t(t) * qt);
+        r.v[1] = cnt;
+        r.v[2] = pos0;
+        r.v[3] = kl;
+        r.v[4] = seq_row[s];
+        r.v[5] = h;
+        r.v[6] = tiles;
+        r.v[7] = 0;
+        items.push_back(r);
+      }
+    }
+  }
+  // longest items first: the hardware block scheduler then approximates LPT
+  std::stable_sort(items.begin(), items.end(), [](const Rec& x, const Rec& y) { return x.v[6] > y.v[6]; });
+  const int64_t need = static_cast<int64_t>(items.size()) * kItemInts;
+  if (need > cap) return fail(PKV_VALUE_ERROR, "plan buffer too small (%lld < %lld)", static_cast<long long>(cap),
+                              static_cast<long long>(need));
+  if (!items.empty()) std::memcpy(plan_out, items.data(), need * sizeof(int32_t));
+  *n_items_out = static_cast<int64_t>(items.size());
+  return PKV_OK;
+}
+
+extern "C" int pkv_paged_prefill(const pkv_prefill_args* a, void* stream_) {
+  if (!a) return fail(PKV_VALUE_ERROR, "null args");
+  if (a->n_items <= 0) return PKV_OK;
+  if (!pkv_prefill_supported(a->hq, a->hkv, a->head_dim, a->page_size, a->kv_dtype))
+    return fail(PKV_CONFIG_ERROR, "tcgen05 prefill does not support hq=%d hkv=%d head_dim=%d page_size=%d dtype=%d",
+                a->hq, a->hkv, a->head_dim, a->page_size, a->kv_dtype);
+  if (!a->plan) return fail(PKV_VALUE_ERROR, "prefill needs the pkv_prefill_plan() items");
+  if (a->cache_rows <= 0 || a->cache_rows >= (int64_t(1) << 31) - 256)
+    return fail(PKV_OUT_OF_RANGE, "cache rows must be in (0, 2^31 - 256)");
+  if (a->out_dtype != PKV_F32 && a->out_dtype != a->kv_dtype)
+    return fail(PKV_CONFIG_ERROR, "prefill output must be fp32 or the cache dtype");
+  if (a->n_items > 0x7fffffff) return fail(PKV_CONFIG_ERROR, "too many prefill items");
+  PrefillParams pp;
+  pp.hq = a->hq;
+  pp.hkv = a->hkv;
+  pp.group = a->hq / a->hkv;
+  pp.qt = kM / pp.group;
+  pp.log2ps = __builtin_ctz(a->page_size);
+  // paged: one box per page (or per 128-key slice of a larger page);
+  // gathered (block_table == NULL): one 128-row box per tile
+  pp.box_rows = a->block_table ? std::min(a->page_size, kN) : kN;
+  pp.bt_stride = a->bt_stride;
+  pp.bt = a->block_table;
+  pp.oob_row = static_cast<int32_t>(a->cache_rows);
+  pp.qscale = a->scale * kLog2eP;
+  pp.causal = a->causal;
+  pp.out = a->out;
+  pp.out_dtype = a->out_dtype;
+  pp.items = a->plan;
+  cudaStream_t stream = static_cast<cudaStream_t>(stream_);
+  if (a->prof_start) cudaEventRecord(static_cast<cudaEvent_t>(a->prof_start), stream);
+  int st;
+  if (a->kv_dtype == PKV_BF16)
+    st = a->head_dim == 128 ? launch<__nv_bfloat16, 128>(a, pp, stream) : launch<__nv_bfloat16, 64>(a, pp, stream);
+  else
+    st = a->head_dim == 128 ? launch<__half, 128>(a, pp, stream) : launch<__half, 64>(a, pp, stream);
+  if (st) return st;
+  if (a->prof_stop) cudaEventRecord(static_cast<cudaEvent_t>(a->prof_stop), stream);
+  return PKV_OK;
 }

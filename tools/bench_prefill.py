@@ -1,0 +1,92 @@
+"""C4 prefill timing: K1 append of N prompt tokens + K3 tcgen05 prefill over
+the paged cache (Llama-3-8B GQA 32q/8kv x128, bf16, page 16).  Prints one
+JSON line per N with device times (CUDA events) and TFLOP/s under the
+reference's FLOP convention 4*Hq*D*sum n(n+1)/2 (attention.py:224-226)."""
+
+import argparse
+import ctypes as C
+import json
+import os
+import sys
+
+import numpy as np
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+
+from paper_2506_07311_b200 import AttentionConfig, KvStore, MaskMeta, PagePool, _lib  # noqa: E402
+from paper_2506_07311_b200.attention import suffix_runs  # noqa: E402
+from paper_2506_07311_b200.store import _stream  # noqa: E402
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--n", default="2048,4096,8192")
+    ap.add_argument("--iters", type=int, default=10)
+    ap.add_argument("--hq", type=int, default=32)
+    ap.add_argument("--hkv", type=int, default=8)
+    ap.add_argument("--d", type=int, default=128)
+    ap.add_argument("--batch", type=int, default=1)
+    args = ap.parse_args()
+    dev = torch.device("cuda:0")
+    hq, hkv, d, ps = args.hq, args.hkv, args.d, 16
+    peaks = json.load(open(os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))),
+                                        "MEASURED_PEAKS.json")))
+    for n in [int(x) for x in args.n.split(",")]:
+        B = args.batch
+        pool = PagePool(B * (n // ps + 2) + 16, page_size=ps)
+        store = KvStore(pool, hkv, d, dtype=torch.bfloat16, device=dev)
+        for b in range(B):
+            pool.reserve(b, n)
+        cfg = AttentionConfig(head_count=hq, head_dim=d, page_size=ps, kv_head_count=hkv)
+        k = torch.randn((B * n, hkv, d), device=dev).bfloat16()
+        v = torch.randn((B * n, hkv, d), device=dev).bfloat16()
+        for b in range(B):
+            store.assign(b, np.arange(n), k[b * n:(b + 1) * n], v[b * n:(b + 1) * n])
+        meta = MaskMeta.self_attention(store.batch_view(list(range(B))))
+        q = torch.randn((B * n, hq, d), device=dev).bfloat16()
+        out = torch.empty((B * n, hq, d), device=dev, dtype=torch.float32)
+        runs = suffix_runs(meta)
+        rows = np.asarray([pool.table(b).mirror_row for b in range(B)], dtype=np.int32)
+        plan = _lib.prefill_plan(runs[0], runs[1], meta.view.lengths, rows, hq, hkv, True)
+        dplan = torch.from_numpy(plan).to(dev)
+        mirror = pool.device_table(dev)
+        lib = _lib.load()
+        a = _lib.PrefillArgs(q=q.data_ptr(), total_q=B * n, k_cache=store.keys.data_ptr(),
+                             v_cache=store.values.data_ptr(), kv_dtype=_lib.PKV_BF16,
+                             cache_rows=store.keys.shape[0], block_table=mirror.data_ptr(),
+                             bt_stride=mirror.shape[1], page_size=ps, hq=hq, hkv=hkv, head_dim=d,
+                             scale=cfg.scale, causal=1, out=out.data_ptr(), out_dtype=_lib.PKV_F32,
+                             plan=dplan.data_ptr(), n_items=plan.shape[0])
+        sp = _stream(dev)
+        for _ in range(3):
+            _lib.check(lib.pkv_paged_prefill(C.byref(a), sp))
+        torch.cuda.synchronize()
+        ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.iters)]
+        for s, e in ev:
+            s.record()
+            lib.pkv_paged_prefill(C.byref(a), sp)
+            e.record()
+        torch.cuda.synchronize()
+        ms = sorted(s.elapsed_time(e) for s, e in ev)
+        med = ms[len(ms) // 2]
+        # append timing (K1 over the whole prompt)
+        pos = np.arange(n)
+        ta = []
+        for _ in range(5):
+            s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            s.record()
+            store.assign(0, pos, k[:n], v[:n])
+            e.record()
+            torch.cuda.synchronize()
+            ta.append(s.elapsed_time(e))
+        flops = 4 * hq * d * B * n * (n + 1) // 2
+        tf = flops / (med * 1e-3) / 1e12
+        print(json.dumps({"n": n, "batch": B, "items": int(plan.shape[0]), "prefill_ms": med,
+                          "tflops": round(tf, 1), "frac_of_sustained": round(tf / peaks["bf16_tflops_sustained"], 3),
+                          "append_ms": min(ta), "append_gbs": round(4 * n * hkv * d * 2 / (min(ta) * 1e-3) / 1e9, 1)}))
+        sys.stdout.flush()
+
+
+if __name__ == "__main__":
+    main()
