@@ -66,7 +66,8 @@ def parse():
 # ---------------------------------------------------------------------------
 
 def workload(args, rank: int, world: int):
-    from oracle.workloads import CONFIG_SHAPES, config_lengths, lpt_partition
+    from paper_2506_07311_b200.sharding import lpt_partition
+    from paper_2506_07311_b200.workloads import CONFIG_SHAPES, config_lengths
 
     if args.config == "c3":
         lengths = config_lengths("c3", batch=args.batch, context=args.context)

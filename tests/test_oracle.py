@@ -172,3 +172,17 @@ def test_oracle_allocator_vs_live_reference_script(live_reference):
                 outs.append(("err", type(exc).__name__))
         assert outs[0] == outs[1], op
         assert a.dump() == b.dump(), op
+
+
+def test_product_workloads_and_sharder_match_oracle():
+    """The product-side generator / LPT sharder agree with the oracle's copies."""
+    from oracle.workloads import config_lengths as o_lengths, lpt_partition as o_lpt
+    from paper_2506_07311_b200.sharding import lpt_partition, shard_balance
+    from paper_2506_07311_b200.workloads import config_lengths as p_lengths
+
+    for name in ("c1", "c2", "c5"):
+        assert p_lengths(name) == o_lengths(name)
+    c5 = p_lengths("c5")
+    for n in (1, 2, 4, 8):
+        assert lpt_partition(c5, n) == o_lpt(c5, n)
+        assert shard_balance(c5, lpt_partition(c5, n)) < 1.001
