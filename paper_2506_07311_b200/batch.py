@@ -58,24 +58,42 @@ class DecodeBatch:
             dev = torch.empty(width, dtype=torch.int32, device=self.device)
             self._ring.append((host, dev, torch.cuda.Event()))
         self._slot = 0
+        self._ring_np = [h.numpy() for h, _, _ in self._ring]
         self.last_launches = 0
+        i64p, i32p, u32p = C.POINTER(C.c_int64), C.POINTER(C.c_int32), C.POINTER(C.c_uint32)
+        self._handles_p = self.handles.ctypes.data_as(i64p)
+        self._pos_p = self._pos.ctypes.data_as(i32p)
+        self._rows_p = self._rows.ctypes.data_as(i32p)
+        self._pages_p = self._pages.ctypes.data_as(u32p)
+        self._copies_p = self._copies.ctypes.data_as(i64p)
+        self._n_pages = C.c_int64()
+        self._plan_n = C.c_int64()
+        self._lib = _lib.load()
+        ws_bytes = self._lib.pkv_attention_workspace_bytes(self.n, config.head_count, config.head_dim)
+        self._ws = _Workspace.get(self.device, ws_bytes)
+        self._qcodes = {torch.float32: _lib.PKV_F32, torch.float16: _lib.PKV_F16,
+                        torch.bfloat16: _lib.PKV_BF16}
+        # one persistent argument block; step() updates the per-call fields
+        self._args = _lib.AttentionArgs(
+            n_queries=self.n, seq_start=None, hq=config.head_count, hkv=config.kv_head_count,
+            head_dim=config.head_dim, scale=float(config.scale), num_sms=0, target_waves=0,
+            prof_start=None, prof_stop=None)
+        self._args_p = C.byref(self._args)
 
     def prepare(self) -> int:
         """Allocator work of one token step (host, one native call); returns
         the number of page clear/copy launches it caused."""
-        n_pages = C.c_int64()
-        i64p, i32p, u32p = C.POINTER(C.c_int64), C.POINTER(C.c_int32), C.POINTER(C.c_uint32)
-        _lib.call("pkv_pool_prepare_append", self.pool._h, self.handles.ctypes.data_as(i64p), self.n,
-                  self._pos.ctypes.data_as(i32p), self._rows.ctypes.data_as(i32p),
-                  self._pages.ctypes.data_as(u32p), self._pages.size, C.byref(n_pages),
-                  self._copies.ctypes.data_as(i64p))
+        n_pages = self._n_pages
+        _lib.call("pkv_pool_prepare_append", self.pool._h, self._handles_p, self.n, self._pos_p,
+                  self._rows_p, self._pages_p, self._pages.size, C.byref(n_pages), self._copies_p)
         launches = 0
         if n_pages.value:
             self.pool._clear_pages(self._pages[: n_pages.value].tolist())
             launches += len(self.pool._stores)
-        for old, new in self._copies.reshape(-1, 2):
-            if new >= 0:
-                self.pool._copy_rows(int(old), int(new), self.pool.page_size)
+        dst = self._copies[1::2]
+        if (dst >= 0).any():
+            for j in np.nonzero(dst >= 0)[0].tolist():
+                self.pool._copy_rows(int(self._copies[2 * j]), int(dst[j]), self.pool.page_size)
                 launches += len(self.pool._stores)
         return launches
 
@@ -92,41 +110,51 @@ class DecodeBatch:
         cfg = self.config
         n = self.n
         host, dev, done = self._ring[self._slot]
+        mh = self._ring_np[self._slot]
         self._slot = (self._slot + 1) % len(self._ring)
         done.synchronize()  # the previous upload from this buffer has landed
-        mh = host.numpy()
-        nkeys = self._pos + 1  # keys attended: the whole context
-        mh[n:2 * n] = nkeys
+        np.add(self._pos, 1, out=mh[n:2 * n])  # keys attended: the whole context
         mh[2 * n:3 * n] = self._rows
-        plan = _lib.attention_plan(nkeys, self._rows, store.page_size, cfg.head_count, cfg.kv_head_count)
-        used = 3 * n + plan.size
-        mh[3 * n:used] = plan
+        # host work plan written straight into the pinned staging buffer
+        got = self._plan_n
+        _lib.check(self._lib.pkv_attention_plan(mh[n:].ctypes.data, mh[2 * n:].ctypes.data, n,
+                                                store.page_size, cfg.head_count, cfg.kv_head_count, 0, 0,
+                                                host.data_ptr() + 12 * n, self._plan_len, C.byref(got)),
+                   "pkv_attention_plan")
+        used = 3 * n + got.value
         dev[:used].copy_(host[:used], non_blocking=True)
         done.record()
-        mirror = self.pool.device_table(self.device)
+        mirror = self.pool.device_table(self.device)  # applies any pending table edits
         k = k_new if isinstance(k_new, torch.Tensor) else torch.from_numpy(np.ascontiguousarray(k_new))
         v = v_new if isinstance(v_new, torch.Tensor) else torch.from_numpy(np.ascontiguousarray(v_new))
-        k = k.to(device=self.device, dtype=store.torch_dtype, non_blocking=True).contiguous()
-        v = v.to(device=self.device, dtype=store.torch_dtype, non_blocking=True).contiguous()
-        md = dev.data_ptr()
-        q, qcode = _q_tensor(queries, self.device)
+        if k.device != self.device or k.dtype != store.torch_dtype or not k.is_contiguous():
+            k = k.to(device=self.device, dtype=store.torch_dtype, non_blocking=True).contiguous()
+        if v.device != self.device or v.dtype != store.torch_dtype or not v.is_contiguous():
+            v = v.to(device=self.device, dtype=store.torch_dtype, non_blocking=True).contiguous()
+        if isinstance(queries, torch.Tensor) and queries.device == self.device and queries.is_contiguous() \
+                and queries.dtype in self._qcodes:
+            q, qcode = queries, self._qcodes[queries.dtype]
+        else:
+            q, qcode = _q_tensor(queries, self.device)
         out_t, out_code = torch_dtype(out_dtype or torch.float32)
         out = torch.empty((n, cfg.head_count, cfg.head_dim), dtype=out_t, device=self.device)
-        ws_bytes = _lib.load().pkv_attention_workspace_bytes(n, cfg.head_count, cfg.head_dim)
-        ws = _Workspace.get(self.device, ws_bytes)
-        args = _lib.AttentionArgs(
-            q=q.data_ptr(), q_dtype=qcode, n_queries=n, q_seq=md, q_nkeys=md + 4 * n,
-            k_cache=store.keys.data_ptr(), v_cache=store.values.data_ptr(), kv_dtype=store.dtype_code,
-            block_table=mirror.data_ptr(), bt_stride=mirror.shape[1], seq_row=md + 8 * n,
-            seq_start=None, page_size=store.page_size, hq=cfg.head_count, hkv=cfg.kv_head_count,
-            head_dim=cfg.head_dim, scale=float(cfg.scale), out=out.data_ptr(), out_dtype=out_code,
-            workspace=ws.data_ptr(), workspace_bytes=ws.numel(), num_sms=0, target_waves=0,
-            mode=PRECISION_MODES[precision], k_new=k.data_ptr(), v_new=v.data_ptr(),
-            plan=md + 12 * n, plan_host=host.data_ptr() + 12 * n)
+        md = dev.data_ptr()
+        a = self._args
+        a.q, a.q_dtype = q.data_ptr(), qcode
+        a.q_seq, a.q_nkeys, a.seq_row = md, md + 4 * n, md + 8 * n
+        a.k_cache, a.v_cache, a.kv_dtype = store.keys.data_ptr(), store.values.data_ptr(), store.dtype_code
+        a.block_table, a.bt_stride = mirror.data_ptr(), mirror.shape[1]
+        a.page_size = store.page_size
+        a.out, a.out_dtype = out.data_ptr(), out_code
+        a.workspace, a.workspace_bytes = self._ws.data_ptr(), self._ws.numel()
+        a.mode = PRECISION_MODES[precision]
+        a.k_new, a.v_new = k.data_ptr(), v.data_ptr()
+        a.plan, a.plan_host = md + 12 * n, host.data_ptr() + 12 * n
         # K1 append is fused into the decode launch (the last split of every
         # sequence reads the new token from k/v and writes it into its page)
-        _lib.check(_lib.load().pkv_paged_attention(C.byref(args), _stream(self.device)),
-                   "pkv_paged_attention")
+        st = self._lib.pkv_paged_attention(self._args_p, _stream(self.device))
+        if st:
+            _lib.check(st, "pkv_paged_attention")
         tensor = (store.dtype_code == _lib.PKV_BF16 and precision != "exact") or precision == "tensor"
         split = int(mh[3 * n + 6]) > 0  # plan header: queries with > 1 split
         self.last_launches = launches + ((1 + split) if tensor else 4)

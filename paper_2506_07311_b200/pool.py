@@ -154,6 +154,7 @@ class PagePool:
         self._handles = itertools.count(1)
         self._stores: list = []
         self._mirror = None  # torch int32 [rows, cols] on the stores' device
+        self._mq_pending, self._mq_full = C.c_int64(), C.c_int32()
 
     def __del__(self):
         h = getattr(self, "_h", None)
@@ -356,11 +357,13 @@ class PagePool:
         import torch
 
         lib = _lib.load()
-        pending, full = C.c_int64(), C.c_int32()
+        pending, full = self._mq_pending, self._mq_full
         _lib.check(lib.pkv_pool_mirror_pending(self._h, C.byref(pending), C.byref(full)))
+        m = self._mirror
+        if not pending.value and not full.value and m is not None and m.device == device:
+            return m  # fast path: nothing changed since the last call
         rows, cols = C.c_int64(), C.c_int64()
         _lib.check(lib.pkv_pool_mirror_shape(self._h, C.byref(rows), C.byref(cols)))
-        m = self._mirror
         if full.value or m is None or tuple(m.shape) != (rows.value, cols.value) or m.device != device:
             host = np.empty((rows.value, cols.value), dtype=np.int32)
             _lib.check(lib.pkv_pool_mirror_export(
@@ -373,7 +376,8 @@ class PagePool:
             _lib.check(lib.pkv_pool_mirror_drain(
                 self._h, pairs.ctypes.data_as(C.POINTER(C.c_int32)), pending.value, C.byref(n),
                 C.byref(full)))
-            dev_pairs = torch.from_numpy(pairs[:n.value]).to(device, non_blocking=False)
+            # pageable source: the copy is staged before returning, no stream sync
+            dev_pairs = torch.from_numpy(pairs[:n.value]).to(device, non_blocking=True)
             stream = torch.cuda.current_stream(device).cuda_stream
             _lib.check(lib.pkv_mirror_apply(C.c_void_p(m.data_ptr()), C.c_void_p(dev_pairs.data_ptr()),
                                             n.value, C.c_void_p(stream)), "pkv_mirror_apply")

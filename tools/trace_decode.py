@@ -17,7 +17,7 @@ B = int(sys.argv[1]) if len(sys.argv) > 1 else 1
 ctx = int(sys.argv[2]) if len(sys.argv) > 2 else 8192
 dev = torch.device('cuda', 0)
 if B == 0:
-    from oracle.workloads import config_lengths
+    from paper_2506_07311_b200.workloads import config_lengths
     lens = config_lengths("c2")
     B = len(lens)
     pool, store, cfg = bench.build_cache(lens, 32, 32, 128, 16, 4, dev)
