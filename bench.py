@@ -316,8 +316,8 @@ def run_ours(args, rank, world, device):
         "tokens_all": tokens_all, "kv_all": kv_all, "alg_all": alg_all,
         "k2_ms_mean": sum(k2_ms) / K, "k2_alg_bytes_mean": alg_bytes / K,
         "clocks": clocks.summary(), "lengths": lengths, "shape": (hq, hkv, d, ps),
-        # decode launch + split combine (plan header word 6: split queries)
-        "launches": sum(1 + int(plans[W + i][6] > 0) for i in range(K)),
+        # one decode launch per step (K1 append fused, split merge in-kernel)
+        "launches": K,
     }
     if not args.no_e2e:
         result["e2e"] = run_e2e(args, pool, store, cfg, lengths, device, flush, world)
@@ -524,7 +524,7 @@ def main():
                        "parallelism": f"request-sharded x{world}", "l2": "flushed between steps (read of 2x L2 of unrelated data)"},
             "pct_of_8TBs": round(100 * value / world / NOMINAL_HBM_GBS, 2),
             "tokens_per_s": r["tokens_all"] / (r["total_ms_max"] / 1e3),
-            "roofline": {"bound": "hbm", "kernel": "decode_kernel (K2)", "achieved": round(k2_achieved, 1),
+            "roofline": {"bound": "hbm", "kernel": "decode_tc_kernel (K2-TC, K1 fused)", "achieved": round(k2_achieved, 1),
                          "peak": peak, "unit": "GB/s", "frac": round(k2_achieved / peak, 4),
                          "traffic": traffic, "peak_source": peak_src,
                          "k2_ms_mean": r["k2_ms_mean"],

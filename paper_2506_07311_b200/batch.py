@@ -156,6 +156,6 @@ class DecodeBatch:
         if st:
             _lib.check(st, "pkv_paged_attention")
         tensor = (store.dtype_code == _lib.PKV_BF16 and precision != "exact") or precision == "tensor"
-        split = int(mh[3 * n + 6]) > 0  # plan header: queries with > 1 split
-        self.last_launches = launches + ((1 + split) if tensor else 4)
+        # tensor-core path: one launch (append fused, split merge in-kernel)
+        self.last_launches = launches + (1 if tensor else 4)
         return out

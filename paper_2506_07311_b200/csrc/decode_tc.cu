@@ -61,9 +61,6 @@ constexpr int kThreadsTc = kWarpsTc * 32;
 constexpr int kStagesTc = 3;
 constexpr int kCh = 16;        // keys per chunk
 constexpr int kMergeRows = 4;  // rows per warp slot of the intra-CTA merge
-// planner cost of an item: head-pages streamed + a fixed per-item overhead
-// (pipeline refill, query load, merge), in head-page units (~2 us)
-constexpr int64_t kItemOverhead = 12;
 constexpr int kTraceSlots = 64;
 
 __device__ __forceinline__ unsigned long long gtimer() {
@@ -73,91 +70,189 @@ __device__ __forceinline__ unsigned long long gtimer() {
 }
 // per warp: 32 slots [start, plan, (item start, first data, chunks done,
 // stored) x 7, end]; lane 0 of every warp of CTAs < 256 records
-__device__ __forceinline__ void trace(int slot) {
-  if (g_trace_on && (threadIdx.x & 31) == 0 && slot < 32 && blockIdx.x < 256)
+// The switch is read once per kernel (a volatile load per stamp would add a
+// global round trip to every item of production runs).
+__device__ __forceinline__ void trace_at(bool on, int slot) {
+  if (on && (threadIdx.x & 31) == 0 && slot < 32 && blockIdx.x < 256)
     g_trace[(blockIdx.x * 8 + (threadIdx.x >> 5)) * 32 + slot] = gtimer();
 }
+#define trace(slot) trace_at(trace_on, (slot))
 
-// plan layout (int32), see plan_decode()
+// plan layout (int32), see plan_decode():
+//   header[kHdr] | nk[nq] | row[nq] | cta_off[grid+1] | items[total][6]
+//   | comb[n_comb][4] | counters[n_comb][kWarpsTc] (zeros)
+// item  = {query, head item (head block x query group), first page, end page,
+//          partial slot or -1 when the item covers its whole (query, head
+//          item), comb record or -1}
+// comb  = {query, head item, first slot, pieces}: a (query, head item) whose
+//          pages were cut across CTAs; its pieces own consecutive slots.  The
+//          last piece to finish (per head warp, counted in `counters`, which
+//          the host uploads as zeros and the merging warp resets) merges all
+//          pieces in page order — deterministic, and no combine launch.
 enum {
-  H_HB = 0, H_WPH, H_QGS, H_QGROUPS, H_HEAD_ITEMS, H_TOTAL_ITEMS, H_NSPLIT_Q, H_NQ,
-  H_GRID, H_CTA_OFF, H_CTA_ITEMS, kHdr = 12
+  H_HB = 0, H_WPH, H_QGS, H_QGROUPS, H_HEAD_ITEMS, H_TOTAL_ITEMS, H_NCOMB, H_NQ,
+  H_GRID, H_CTA_OFF, H_ITEMS, H_COMB, H_CTR, kHdr = 13
 };
-constexpr int kCtaItemsSmem = 64;  // per-CTA item list staged in shared memory
-__host__ __device__ constexpr int64_t o_order(int64_t) { return kHdr; }
-__host__ __device__ constexpr int64_t o_ioff(int64_t nq) { return kHdr + nq; }
-__host__ __device__ constexpr int64_t o_nsplit(int64_t nq) { return kHdr + 2 * nq + 1; }
-__host__ __device__ constexpr int64_t o_soff(int64_t nq) { return kHdr + 3 * nq + 1; }
-__host__ __device__ constexpr int64_t o_nk(int64_t nq) { return kHdr + 4 * nq + 2; }
-__host__ __device__ constexpr int64_t o_row(int64_t nq) { return kHdr + 5 * nq + 2; }
-__host__ __device__ constexpr int64_t o_cq(int64_t nq) { return kHdr + 6 * nq + 2; }
+constexpr int kItemInts = 6;
+constexpr int kCombInts = 4;
+constexpr int kCtaItemsSmem = 64;  // per-CTA item records staged in shared memory
+__host__ __device__ constexpr int64_t o_nk(int64_t) { return kHdr; }
+__host__ __device__ constexpr int64_t o_row(int64_t nq) { return kHdr + nq; }
+__host__ __device__ constexpr int64_t o_cta(int64_t nq) { return kHdr + 2 * nq; }
 
 struct PlanView {
-  const int32_t *order, *ioff, *nsplit, *soff, *nk, *row;
-  int hb, wph, qgs, qgroups, head_items, total_items, nq;
+  const int32_t *nk, *row;
+  const int32_t* items;  // this CTA's first record (shared or global memory)
+  int count;             // items of this CTA
+  int hb, wph, qgs, qgroups, nq, ps;
 };
 
 // one warp's view of a work item
 struct Item {
-  int qi, kvh, sub, qh0, rows, split, nsplit, kb, ke, nchunks, nk, row, slot;
-  bool valid;
+  int qi, kvh, sub, qh0, rows, kb, ke, nchunks, nk, row, slot, comb;
+  bool valid, last;  // last: the item holds the query's final page (fused append)
 };
 
-__device__ __forceinline__ Item make_item(int64_t gidx, const PlanView& pv, const TcParams& p, int warp) {
+__device__ __forceinline__ Item make_item(int k, const PlanView& pv, const TcParams& p, int warp) {
   Item it;
-  it.valid = gidx < pv.total_items;
+  it.valid = k < pv.count;
   if (!it.valid) return it;
-  const int gi = static_cast<int>(gidx);
-  int lo = 0, hi = pv.nq;  // sorted position j with ioff[j] <= gi < ioff[j+1]
-  while (hi - lo > 1) {
-    const int mid = (lo + hi) >> 1;
-    if (pv.ioff[mid] <= gi) lo = mid; else hi = mid;
-  }
-  const int q = pv.order[lo];
-  const int rem = gi - pv.ioff[lo];
+  const int32_t* r = pv.items + k * kItemInts;
+  const int q = r[0], hix = r[1], pb = r[2], pe = r[3];
+  it.slot = r[4];
+  it.comb = r[5];
   it.qi = q;
-  it.split = rem / pv.head_items;
-  const int hix = rem - it.split * pv.head_items;
   const int hb = hix / pv.qgroups;
   const int qg = hix - hb * pv.qgroups;
   it.kvh = hb * pv.hb + warp / pv.wph;
   it.sub = warp % pv.wph;
   it.qh0 = it.kvh * p.group + qg * pv.qgs;
   it.rows = min(pv.qgs, p.group - qg * pv.qgs);
-  it.nsplit = pv.nsplit[q];
   it.nk = pv.nk[q];
   it.row = pv.row[q];
-  it.slot = pv.soff[q] + it.split;
-  const int ps = 1 << p.log2ps;
-  const int pages = (it.nk + ps - 1) >> p.log2ps;
-  int p0, p1;
-  if (it.nsplit == 1) {
-    p0 = 0;
-    p1 = pages;
-  } else if (pages < 65536) {  // 32-bit division (64-bit is emulated)
-    p0 = static_cast<int>((static_cast<unsigned>(it.split) * pages) / static_cast<unsigned>(it.nsplit));
-    p1 = static_cast<int>((static_cast<unsigned>(it.split + 1) * pages) / static_cast<unsigned>(it.nsplit));
-  } else {
-    p0 = static_cast<int>((int64_t(it.split) * pages) / it.nsplit);
-    p1 = static_cast<int>((int64_t(it.split + 1) * pages) / it.nsplit);
-  }
-  it.kb = p0 * ps;
-  it.ke = min(it.nk, p1 * ps);
+  it.kb = pb << p.log2ps;
+  it.ke = min(it.nk, pe << p.log2ps);
+  it.last = it.ke == it.nk;
   it.nchunks = (it.ke - it.kb + kCh - 1) / kCh;
   return it;
 }
 
-// k-th item of this CTA (host LPT assignment; staged list, global beyond it)
-struct CtaItems {
-  const int32_t* smem_list;
-  const int32_t* global_list;
-  int count;
-  int total;
-  __device__ __forceinline__ int64_t operator()(int64_t k) const {
-    if (k >= count) return total;  // invalid item: end of this CTA's work
-    return k < kCtaItemsSmem ? smem_list[k] : global_list[k];
+// Split finish: called by a whole warp after it stored the partial (m, l, O)
+// rows [qh0, qh0 + rows) of its piece.  The last piece of the unit to arrive
+// (per head warp slot) merges every piece in page order and writes the output.
+template <int D>
+__device__ __forceinline__ void finish_split(const TcParams& p, const int32_t* plan, int comb, int hslot,
+                                             int qi, int qh0, int rows, int lane) {
+  __threadfence();
+  __syncwarp();
+  int* ctr = const_cast<int32_t*>(plan) + plan[H_CTR] + comb * kWarpsTc + hslot;
+  const int32_t* c = plan + plan[H_COMB] + comb * kCombInts;
+  const int s0 = __ldg(c + 2), ns = __ldg(c + 3);
+  int last = 0;
+  if (lane == 0) last = atomicAdd(ctr, 1) == ns - 1;
+  if (!__shfl_sync(0xffffffffu, last, 0)) return;
+  __threadfence();
+  const float2* ml = reinterpret_cast<const float2*>(p.ws_ml);
+  constexpr int E = D / 32;
+  for (int r = 0; r < rows; ++r) {
+    const int qh = qh0 + r;
+    // lanes over pieces for the row max and denominator
+    float mx = -INFINITY;
+    for (int s = lane; s < ns; s += 32) mx = fmaxf(mx, __ldcg(ml + int64_t(s0 + s) * p.hq + qh).x);
+#pragma unroll
+    for (int o = 16; o; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    float den = 0.f;
+    for (int s = lane; s < ns; s += 32) {
+      const float2 v = __ldcg(ml + int64_t(s0 + s) * p.hq + qh);
+      den += (v.x == -INFINITY ? 0.f : exp2f(v.x - mx)) * v.y;
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) den += __shfl_xor_sync(0xffffffffu, den, o);
+    // O: 8 pieces in flight per step, summed in page order
+    float acc[E];
+#pragma unroll
+    for (int e = 0; e < E; ++e) acc[e] = 0.f;
+    for (int sb = 0; sb < ns; sb += 8) {
+      float wv[8], ov[8][E];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const bool in = sb + u < ns;
+        const int64_t slot = int64_t(s0 + sb + (in ? u : 0)) * p.hq + qh;
+        wv[u] = in ? __ldcg(ml + slot).x : -INFINITY;
+#pragma unroll
+        for (int e = 0; e < E; ++e) ov[u][e] = in ? __ldcg(p.ws_o + slot * D + lane + 32 * e) : 0.f;
+      }
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const float w = wv[u] == -INFINITY ? 0.f : exp2f(wv[u] - mx);
+#pragma unroll
+        for (int e = 0; e < E; ++e) acc[e] += w * ov[u][e];
+      }
+    }
+    const float inv = 1.f / den;
+#pragma unroll
+    for (int e = 0; e < E; ++e)
+      store_from_float(p.out, (int64_t(qi) * p.hq + qh) * D + lane + 32 * e, p.out_dtype, acc[e] * inv);
   }
-};
+  if (lane == 0) *ctr = 0;  // self-cleaning: the plan buffer can be replayed
+}
+
+__device__ __forceinline__ void named_bar(int id, int threads) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(threads) : "memory");
+}
+
+// Split finish for a head group of `grp` threads (wph warps) that stored its
+// piece's partial rows: one thread counts the arrival; if this piece is the
+// unit's last, the whole group merges all pieces in page order in parallel.
+template <int D>
+__device__ __forceinline__ void finish_split_group(const TcParams& p, const int32_t* plan, int comb, int hslot,
+                                                   int qi, int qh0, int rows, int tt, int grp, int bar_id,
+                                                   int* flag) {
+  __threadfence();
+  named_bar(bar_id, grp);
+  int* ctr = const_cast<int32_t*>(plan) + plan[H_CTR] + comb * kWarpsTc + hslot;
+  const int32_t* c = plan + plan[H_COMB] + comb * kCombInts;
+  const int s0 = __ldg(c + 2), ns = __ldg(c + 3);
+  if (tt == 0) *flag = atomicAdd(ctr, 1) == ns - 1;
+  named_bar(bar_id, grp);
+  if (!*flag) return;
+  __threadfence();
+  const float2* ml = reinterpret_cast<const float2*>(p.ws_ml);
+  // one pass over the pieces with an online rescale; 16 pieces' (m, l) and
+  // O loads are issued together so the merge costs ~one L2 round trip
+#pragma unroll 1
+  for (int e = tt; e < rows * D; e += grp) {
+    const int r = e / D, d = e - r * D;
+    const int qh = qh0 + r;
+    float mx = -INFINITY, den = 0.f, acc = 0.f;
+    for (int sb = 0; sb < ns; sb += 16) {
+      float2 mv[16];
+      float ov[16];
+#pragma unroll
+      for (int u = 0; u < 16; ++u) {
+        const bool in = sb + u < ns;
+        const int64_t slot = int64_t(s0 + sb + (in ? u : 0)) * p.hq + qh;
+        mv[u] = in ? __ldcg(ml + slot) : make_float2(-INFINITY, 0.f);
+        ov[u] = in ? __ldcg(p.ws_o + slot * D + d) : 0.f;
+      }
+      float bm = mx;
+#pragma unroll
+      for (int u = 0; u < 16; ++u) bm = fmaxf(bm, mv[u].x);
+      const float cr = mx == -INFINITY ? 0.f : exp2f(mx - bm);
+      den *= cr;
+      acc *= cr;
+#pragma unroll
+      for (int u = 0; u < 16; ++u) {
+        const float w = mv[u].x == -INFINITY ? 0.f : exp2f(mv[u].x - bm);
+        den += w * mv[u].y;
+        acc += w * ov[u];
+      }
+      mx = bm;
+    }
+    store_from_float(p.out, (int64_t(qi) * p.hq + qh) * D + d, p.out_dtype, acc / den);
+  }
+  if (tt == 0) *ctr = 0;  // self-cleaning: the plan buffer can be replayed
+}
 
 template <typename T, int D, bool SPLITQ, bool ROWS16>
 __global__ void __launch_bounds__(kThreadsTc, 1) decode_tc_kernel(const __grid_constant__ TcParams p) {
@@ -174,54 +269,38 @@ __global__ void __launch_bounds__(kThreadsTc, 1) decode_tc_kernel(const __grid_c
   asm volatile("griddepcontrol.launch_dependents;");
 
   extern __shared__ __align__(1024) unsigned char smem[];
-  __shared__ int s_arr[kWarpsTc];   // per head: arrivals at the current item
-  __shared__ int s_done[kWarpsTc];  // per head: items merged
-  __shared__ int32_t s_cta_items[kCtaItemsSmem];
+  __shared__ int s_flag[kWarpsTc];  // per head: this CTA's piece merges the split
+  __shared__ int32_t s_cta_items[kCtaItemsSmem * kItemInts];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const bool trace_on = g_trace_on != 0;
   trace(0);
-  if (threadIdx.x < kWarpsTc) {
-    s_arr[threadIdx.x] = 0;
-    s_done[threadIdx.x] = 0;
-  }
-  CtaItems items;
-  {
-    const int32_t* off = p.plan + p.plan[H_CTA_OFF];
-    const int32_t* list = p.plan + p.plan[H_CTA_ITEMS];
-    const int first = __ldg(off + blockIdx.x);
-    items.count = __ldg(off + blockIdx.x + 1) - first;
-    items.global_list = list + first;
-    items.smem_list = s_cta_items;
-    items.total = __ldg(p.plan + H_TOTAL_ITEMS);
-    if (threadIdx.x < kCtaItemsSmem && threadIdx.x < items.count) s_cta_items[threadIdx.x] = __ldg(list + first + threadIdx.x);
-  }
-
   // ---------------- plan (host-computed; staged into shared memory) ---------
   PlanView pv;
   {
     const int32_t* g = p.plan;
     const int nq = p.nq;
+    const int32_t* off = g + o_cta(nq);
+    const int first = __ldg(off + blockIdx.x);
+    pv.count = __ldg(off + blockIdx.x + 1) - first;
+    const int32_t* gitems = g + __ldg(g + H_ITEMS) + int64_t(first) * kItemInts;
+    const bool items_smem = pv.count <= kCtaItemsSmem;
+    for (int i = threadIdx.x; i < (items_smem ? pv.count * kItemInts : 0); i += kThreadsTc)
+      s_cta_items[i] = __ldg(gitems + i);
     const int32_t* src = g;
     if (p.plan_in_smem) {
       int32_t* s = reinterpret_cast<int32_t*>(smem);
-      const int n = static_cast<int>(o_cq(nq));
+      const int n = static_cast<int>(o_cta(nq));
       for (int i = threadIdx.x; i < n; i += kThreadsTc) s[i] = __ldg(g + i);
-      __syncthreads();
       src = s;
-    } else {
-      __syncthreads();
     }
-    pv.order = src + o_order(nq);
-    pv.ioff = src + o_ioff(nq);
-    pv.nsplit = src + o_nsplit(nq);
-    pv.soff = src + o_soff(nq);
+    __syncthreads();
+    pv.items = items_smem ? s_cta_items : gitems;
     pv.nk = src + o_nk(nq);
     pv.row = src + o_row(nq);
     pv.hb = src[H_HB];
     pv.wph = src[H_WPH];
     pv.qgs = src[H_QGS];
     pv.qgroups = src[H_QGROUPS];
-    pv.head_items = src[H_HEAD_ITEMS];
-    pv.total_items = src[H_TOTAL_ITEMS];
     pv.nq = nq;
   }
   trace(1);
@@ -240,7 +319,7 @@ __global__ void __launch_bounds__(kThreadsTc, 1) decode_tc_kernel(const __grid_c
   int win = -1, win_val = 0;
   auto start_item = [&]() {
     for (;;) {
-      P = make_item(items(pk), pv, p, warp);
+      P = make_item(static_cast<int>(pk), pv, p, warp);
       pc = P.sub;
       win = -1;
       if (!P.valid) return;
@@ -249,7 +328,7 @@ __global__ void __launch_bounds__(kThreadsTc, 1) decode_tc_kernel(const __grid_c
         const int qe = p.q_dtype == PKV_F32 ? 4 : 2;
         const char* qrow = static_cast<const char*>(p.q) + (int64_t(P.qi) * p.hq + P.qh0) * D * qe;
         if (lane * 128 < P.rows * D * qe) asm volatile("prefetch.global.L2 [%0];" ::"l"(qrow + lane * 128));
-        if (p.k_new != nullptr && P.split == P.nsplit - 1) {
+        if (p.k_new != nullptr && P.last) {
           // fused append: write the new token's head slice into its page
           const int pos = P.nk - 1;
           const int64_t page = p.bt[int64_t(P.row) * p.bt_stride + (pos >> p.log2ps)];
@@ -289,7 +368,7 @@ __global__ void __launch_bounds__(kThreadsTc, 1) decode_tc_kernel(const __grid_c
       } else {
         rowidx = P.row + k0 + lane;
       }
-      const bool fuse = p.k_new != nullptr && P.split == P.nsplit - 1;
+      const bool fuse = p.k_new != nullptr && P.last;
       const int64_t head_off = int64_t(P.kvh) * ROWB;
       const int64_t new_off = (int64_t(P.qi) * p.hkv + P.kvh) * ROWB + cc * 16;
       const uint32_t kdst = ring_addr + stage * STAGE;
@@ -328,7 +407,7 @@ __global__ void __launch_bounds__(kThreadsTc, 1) decode_tc_kernel(const __grid_c
   const float qscale = p.qscale;
   const int head_local = warp / pv.wph;
   for (int64_t k = 0;; ++k) {
-    const Item C = make_item(items(k), pv, p, warp);
+    const Item C = make_item(static_cast<int>(k), pv, p, warp);
     if (!C.valid) break;
     trace(2 + 4 * int(k));
 
@@ -487,7 +566,7 @@ __global__ void __launch_bounds__(kThreadsTc, 1) decode_tc_kernel(const __grid_c
 #pragma unroll
       for (int n = 0; n < NT; ++n) {
         const int d = n * 8 + 2 * t4;
-        if (C.nsplit == 1) {
+        if (C.slot < 0) {
           if (g < C.rows) {
             store_from_float(p.out, out_base + int64_t(g) * D + d, p.out_dtype, o[n][0] / l0);
             store_from_float(p.out, out_base + int64_t(g) * D + d + 1, p.out_dtype, o[n][1] / l0);
@@ -502,22 +581,21 @@ __global__ void __launch_bounds__(kThreadsTc, 1) decode_tc_kernel(const __grid_c
             __stcg(reinterpret_cast<float2*>(p.ws_o + (pslot + g + 8) * D + d), make_float2(o[n][2], o[n][3]));
         }
       }
-      if (C.nsplit > 1 && t4 == 0) {
+      if (C.slot >= 0 && t4 == 0) {
         if (g < C.rows) __stcg(reinterpret_cast<float2*>(p.ws_ml) + pslot + g, make_float2(m0, l0));
         if (ROWS16 && g + 8 < C.rows) __stcg(reinterpret_cast<float2*>(p.ws_ml) + pslot + g + 8, make_float2(m1, l1));
       }
+      if (C.slot >= 0) finish_split<D>(p, p.plan, C.comb, warp, C.qi, C.qh0, C.rows, lane);
       trace(5 + 4 * int(k));
       continue;
     }
 
-    // ---- WPH warps share this head: asynchronous shared-memory merge.  A
-    // warp overwrites its slot only after the head's previous item merged;
-    // the last of the head's warps to arrive merges in warp order.
-    if (k > 0) {
-      if (lane == 0)
-        while (*reinterpret_cast<volatile int*>(&s_done[head_local]) < static_cast<int>(k)) __nanosleep(32);
-      __syncwarp();
-    }
+    // ---- WPH warps share this head: the head's warps meet at a named
+    // barrier and merge their partials in parallel (thread tt of the group
+    // owns elements tt, tt + 32*wph, ... of the rows x D block).
+    const int grp = pv.wph * 32;
+    const int bar_id = 1 + head_local;
+    const int tt = (warp - head_local * pv.wph) * 32 + lane;
     if (g < C.rows) {  // rows <= kMergeRows when wph > 1 (planner)
       float* dst = s_mo + (warp * kMergeRows + g) * D;
 #pragma unroll
@@ -527,104 +605,36 @@ __global__ void __launch_bounds__(kThreadsTc, 1) decode_tc_kernel(const __grid_c
         s_ml[(warp * kMergeRows + g) * 2 + 1] = l0;
       }
     }
-    __syncwarp();
-    int last = 0;
-    if (lane == 0) last = atomicAdd(&s_arr[head_local], 1) == pv.wph - 1;
-    last = __shfl_sync(0xffffffffu, last, 0);
+    named_bar(bar_id, grp);
     trace(5 + 4 * int(k));
-    if (!last) continue;
-    constexpr int E = D / 32;
-    float acc[kMergeRows][E], rmx[kMergeRows], rden[kMergeRows];
     const int w0 = head_local * pv.wph;
-#pragma unroll
-    for (int r = 0; r < kMergeRows; ++r) {
-      if (r >= C.rows) break;
+#pragma unroll 1
+    for (int e = tt; e < C.rows * D; e += grp) {
+      const int r = e / D, d = e - r * D;
       float mx = -INFINITY;
       for (int w = w0; w < w0 + pv.wph; ++w) mx = fmaxf(mx, s_ml[(w * kMergeRows + r) * 2]);
-      float den = 0.f;
-#pragma unroll
-      for (int e = 0; e < E; ++e) acc[r][e] = 0.f;
+      float den = 0.f, acc = 0.f;
       for (int w = w0; w < w0 + pv.wph; ++w) {
         const float mw = s_ml[(w * kMergeRows + r) * 2];
         const float wgt = mw == -INFINITY ? 0.f : exp2f(mw - mx);
         den += wgt * s_ml[(w * kMergeRows + r) * 2 + 1];
-#pragma unroll
-        for (int e = 0; e < E; ++e) acc[r][e] += wgt * s_mo[(w * kMergeRows + r) * D + lane + 32 * e];
+        acc += wgt * s_mo[(w * kMergeRows + r) * D + d];
       }
-      rmx[r] = mx;
-      rden[r] = den;
-    }
-    __syncwarp();
-    if (lane == 0) {  // release the head's slots before touching global memory
-      s_arr[head_local] = 0;
-      *reinterpret_cast<volatile int*>(&s_done[head_local]) = static_cast<int>(k) + 1;
-    }
-#pragma unroll
-    for (int r = 0; r < kMergeRows; ++r) {
-      if (r >= C.rows) break;
-#pragma unroll
-      for (int e = 0; e < E; ++e) {
-        const int d = lane + 32 * e;
-        if (C.nsplit == 1)
-          store_from_float(p.out, out_base + int64_t(r) * D + d, p.out_dtype, acc[r][e] / rden[r]);
-        else
-          __stcg(p.ws_o + (pslot + r) * D + d, acc[r][e]);
+      if (C.slot < 0) {
+        store_from_float(p.out, out_base + int64_t(r) * D + d, p.out_dtype, acc / den);
+      } else {
+        __stcg(p.ws_o + (pslot + r) * D + d, acc);
+        if (d == 0) __stcg(reinterpret_cast<float2*>(p.ws_ml) + pslot + r, make_float2(mx, den));
       }
-      if (C.nsplit > 1 && lane == 0) __stcg(reinterpret_cast<float2*>(p.ws_ml) + pslot + r, make_float2(rmx[r], rden[r]));
     }
+    trace(28);
+    if (C.slot >= 0) finish_split_group<D>(p, p.plan, C.comb, head_local, C.qi, C.qh0, C.rows, tt, grp, bar_id,
+                                           &s_flag[head_local]);
+    named_bar(bar_id, grp);  // the head's merge slots are free for its next item
+    trace(30);
   }
   cp_async_wait<0>();
   trace(31);
-}
-
-// K2c: merge the split partials of every (query with > 1 split, query head).
-// One warp per (query, head, 32-wide slice of D); ascending split order.
-template <int D>
-__global__ void __launch_bounds__(256) combine_tc_kernel(const __grid_constant__ TcParams p) {
-  asm volatile("griddepcontrol.wait;" ::: "memory");  // decode grid done + flushed
-  const int nq = p.nq;
-  const int32_t* plan = p.plan;
-  const int nsq = plan[H_NSPLIT_Q];
-  const int32_t* cq = plan + o_cq(nq);
-  const int32_t* nsplit = plan + o_nsplit(nq);
-  const int32_t* soff = plan + o_soff(nq);
-  const int lane = threadIdx.x & 31;
-  constexpr int SL = D / 32;
-  const int64_t tasks = int64_t(nsq) * p.hq * SL;
-  const float2* ml = reinterpret_cast<const float2*>(p.ws_ml);
-  for (int64_t t = int64_t(blockIdx.x) * 8 + (threadIdx.x >> 5); t < tasks; t += int64_t(gridDim.x) * 8) {
-    const int sl = static_cast<int>(t % SL);
-    const int64_t r = t / SL;
-    const int qh = static_cast<int>(r % p.hq);
-    const int q = cq[r / p.hq];
-    const int ns = nsplit[q], s0 = soff[q];
-    float mx = -INFINITY;
-    for (int s = lane; s < ns; s += 32) mx = fmaxf(mx, __ldcg(ml + (int64_t(s0 + s) * p.hq + qh)).x);
-#pragma unroll
-    for (int o = 16; o; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-    float den = 0.f;
-    for (int s = lane; s < ns; s += 32) {
-      const float2 v = __ldcg(ml + (int64_t(s0 + s) * p.hq + qh));
-      den += exp2f(v.x - mx) * v.y;
-    }
-#pragma unroll
-    for (int o = 16; o; o >>= 1) den += __shfl_xor_sync(0xffffffffu, den, o);
-    const int d = sl * 32 + lane;
-    float acc = 0.f;
-    for (int sb = 0; sb < ns; sb += 8) {
-      float wv[8], ov[8];
-#pragma unroll
-      for (int u = 0; u < 8; ++u) {
-        const int64_t slot = int64_t(s0 + sb + u) * p.hq + qh;
-        const bool in = sb + u < ns;
-        wv[u] = in ? __ldcg(ml + slot).x : -INFINITY;
-        ov[u] = in ? __ldcg(p.ws_o + slot * D + d) : 0.f;
-      }
-#pragma unroll
-      for (int u = 0; u < 8; ++u) acc += (wv[u] == -INFINITY ? 0.f : exp2f(wv[u] - mx)) * ov[u];
-    }
-    store_from_float(p.out, (int64_t(q) * p.hq + qh) * D + d, p.out_dtype, acc / den);
-  }
 }
 
 template <typename T, int D>
@@ -640,27 +650,29 @@ bool decode_tc_supported(int kv_dtype, int head_dim) {
 }
 
 constexpr int kMaxGrid = 1024;
-constexpr int kMaxWaves = 8;
 int64_t decode_plan_ints(int64_t nq, int hq) {
-  // cq[nq] + cta_off[grid+1] + cta_items[<= waves*grid + nq*hq]
-  return o_cq(nq) + nq + (kMaxGrid + 1) + (int64_t(kMaxWaves) * kMaxGrid + nq * hq);
+  // header + nk/row + cta offsets + items (units + 2 cuts per CTA) + comb
+  const int64_t units = nq * hq;  // head items per query <= hq
+  return o_cta(nq) + (kMaxGrid + 1) + (units + 2 * kMaxGrid) * kItemInts +
+         (kMaxGrid + 1) * (kCombInts + kWarpsTc);
 }
 
-// Host planner: head blocking, even page splits, size-sorted item order.
+// Host planner ("stream-K" for paged decode).  The work of every (query,
+// head item) — a head block of hb kv heads x one group of query rows — is laid
+// out on one line in query order, each unit charged its pages plus a fixed
+// per-item overhead; the line is cut into `grid` equal segments, one per CTA,
+// so every CTA streams the same number of bytes and runs only ~units/grid + 1
+// items.  A cut inside a unit splits its pages between neighbouring CTAs (the
+// pieces get partial slots and a combine record); cuts that would leave a
+// piece shorter than the per-item overhead snap to the unit boundary.
 int plan_decode(const int32_t* nk, const int32_t* row, int64_t nq, int page_size, int hq, int hkv,
                 int num_sms, int waves, int32_t* out, int64_t cap, int64_t* n_out) {
   if (cap < decode_plan_ints(nq, hq)) return fail(PKV_VALUE_ERROR, "plan buffer too small");
-  num_sms = std::min(num_sms, kMaxGrid);
-  waves = std::min(waves, kMaxWaves);  // <= 0: search
+  num_sms = std::max(1, std::min(num_sms, kMaxGrid));
   const int G = hq / hkv;
   const int ps = page_size;
-  std::vector<int64_t> pages(nq);
-  int64_t total_pages = 0, max_pages = 0;
-  for (int64_t i = 0; i < nq; ++i) {
-    pages[i] = (int64_t(nk[i]) + ps - 1) / ps;
-    total_pages += pages[i];
-    max_pages = std::max(max_pages, pages[i]);
-  }
+  int64_t total_pages = 0;
+  for (int64_t i = 0; i < nq; ++i) total_pages += (int64_t(nk[i]) + ps - 1) / ps;
   // head block: one warp per kv head when there are enough (query, head
   // block) units to fill the GPU, otherwise several warps per head
   int hb = 1;
@@ -676,83 +688,16 @@ int plan_decode(const int32_t* nk, const int32_t* row, int64_t nq, int page_size
   const int qgs = wph == 1 ? 16 : kMergeRows;
   const int qgroups = (G + qgs - 1) / qgs;
   const int head_items = (hkv / hb) * qgroups;
-  const int64_t min_sp = (int64_t(2) * kCh * wph + ps - 1) / ps;  // >= 2 chunks per warp
-  std::vector<int32_t> ns(nq), order(nq);
-  std::vector<int64_t> size(nq);
-  // split size for `w` waves; the item cost model (head-pages plus a fixed
-  // per-item overhead) drives both the choice and the LPT assignment
-  auto split_for = [&](int w) {
-    const int64_t target = int64_t(num_sms) * w;
-    const int64_t sp = (total_pages * head_items + target - 1) / target;
-    return std::max<int64_t>({sp, min_sp, (max_pages + 255) / 256, 1});
-  };
-  auto build = [&](int64_t sp) {
-    for (int64_t i = 0; i < nq; ++i) {
-      ns[i] = static_cast<int32_t>(std::max<int64_t>(1, (pages[i] + sp - 1) / sp));
-      size[i] = (pages[i] + ns[i] - 1) / ns[i];
-    }
-    std::iota(order.begin(), order.end(), 0);
-    std::stable_sort(order.begin(), order.end(), [&](int32_t a, int32_t b) { return size[a] > size[b]; });
-  };
-  auto makespan = [&](int grid) {
-    std::vector<int64_t> load(grid, 0);
-    std::priority_queue<std::pair<int64_t, int>, std::vector<std::pair<int64_t, int>>, std::greater<>> heap;
-    for (int c = 0; c < grid; ++c) heap.emplace(0, c);
-    int64_t worst = 0;
-    for (int64_t j = 0; j < nq; ++j) {
-      const int32_t q = order[j];
-      const int64_t cost = size[q] * hb + kItemOverhead;
-      for (int64_t t = 0; t < int64_t(ns[q]) * head_items; ++t) {
-        auto top = heap.top();
-        heap.pop();
-        top.first += cost;
-        worst = std::max(worst, top.first);
-        heap.push(top);
-      }
-    }
-    return worst;
-  };
-  int64_t best_sp = split_for(std::max(1, waves));
-  // The wave search simulates the LPT schedule for 7 wave counts (~0.3 ms
-  // for a few thousand items); a serving loop calls the planner every token
-  // with nearly the same lengths, so the chosen split is memoised per shape
-  // bucket (total and longest context in 32-page buckets).
-  struct Memo {
-    int64_t key[7];
-    int64_t sp;
-  };
-  static thread_local Memo memo[16];
-  static thread_local int memo_next = 0;
-  const int64_t mkey[7] = {nq, hq, hkv, ps, num_sms, total_pages >> 5, max_pages >> 5};
-  bool memo_hit = false;
-  if (waves <= 0) {
-    for (const Memo& m : memo)
-      if (std::equal(mkey, mkey + 7, m.key) && m.sp > 0) {
-        best_sp = m.sp;
-        memo_hit = true;
-        break;
-      }
-  }
-  if (waves <= 0 && !memo_hit) {  // search the wave count with the smallest predicted makespan
-    int64_t best = -1;
-    for (int w : {1, 2, 3, 4, 5, 6, 8}) {
-      const int64_t sp = split_for(w);
-      build(sp);
-      int64_t items = 0;
-      for (int64_t i = 0; i < nq; ++i) items += int64_t(ns[i]) * head_items;
-      const int grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(num_sms, items)));
-      const int64_t m = makespan(grid);
-      if (best < 0 || m < best) {
-        best = m;
-        best_sp = sp;
-      }
-    }
-    Memo& slot = memo[memo_next];
-    memo_next = (memo_next + 1) % 16;
-    std::copy(mkey, mkey + 7, slot.key);
-    slot.sp = best_sp;
-  }
-  build(best_sp);
+  // costs in pages of one unit; the per-item overhead (pipeline refill,
+  // query load, partial store) is ~4 us ~ `ovh` pages of a CTA's stream
+  const int64_t page_bytes = int64_t(hb) * ps * 128 * 2 * 2;  // K+V of the block (D ~ 128)
+  const int64_t ovh = std::max<int64_t>(1, (int64_t(200) << 10) / page_bytes) * (waves > 0 ? waves : 1);
+  const int64_t min_piece = std::max<int64_t>(ovh / 2, (2 * kCh * wph + ps - 1) / ps);
+  const int64_t units = nq * head_items;
+  const int64_t line = total_pages * head_items + ovh * units;
+  int grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(num_sms, total_pages * head_items / min_piece)));
+  const double seg = double(line) / grid;
+
   int32_t* o = out;
   o[H_HB] = hb;
   o[H_WPH] = wph;
@@ -760,68 +705,89 @@ int plan_decode(const int32_t* nk, const int32_t* row, int64_t nq, int page_size
   o[H_QGROUPS] = qgroups;
   o[H_HEAD_ITEMS] = head_items;
   o[H_NQ] = static_cast<int32_t>(nq);
-  for (int h = H_GRID; h < kHdr; ++h) o[h] = 0;
-  int64_t acc = 0;
-  for (int64_t j = 0; j < nq; ++j) {
-    o[o_order(nq) + j] = order[j];
-    o[o_ioff(nq) + j] = static_cast<int32_t>(acc);
-    acc += int64_t(ns[order[j]]) * head_items;
-  }
-  if (acc > (int64_t(1) << 31) - 1) return fail(PKV_CONFIG_ERROR, "too many work items");
-  o[o_ioff(nq) + nq] = static_cast<int32_t>(acc);
-  o[H_TOTAL_ITEMS] = static_cast<int32_t>(acc);
-  int64_t s = 0, nsq = 0;
   for (int64_t i = 0; i < nq; ++i) {
-    o[o_nsplit(nq) + i] = ns[i];
-    o[o_soff(nq) + i] = static_cast<int32_t>(s);
-    s += ns[i];
     o[o_nk(nq) + i] = nk[i];
     o[o_row(nq) + i] = row[i];
-    if (ns[i] > 1) o[o_cq(nq) + nsq++] = static_cast<int32_t>(i);
   }
-  o[o_soff(nq) + nq] = static_cast<int32_t>(s);
-  o[H_NSPLIT_Q] = static_cast<int32_t>(nsq);
-
-  // greedy LPT: items in size order (largest first) to the least-loaded CTA;
-  // cost = pages of the split plus a fixed per-item overhead
-  const int64_t total_items = acc;
-  const int grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(num_sms, total_items)));
-  // (load, cta) packed into one int64 (grid <= kMaxGrid < 2^11) for a flat
-  // min-heap; items are dealt in index order, so every CTA's list ascends
-  std::vector<int32_t> cta_of(static_cast<size_t>(total_items));
-  std::vector<int32_t> count(grid + 1, 0);
-  {
-    std::vector<int64_t> heap(grid);
-    for (int c = 0; c < grid; ++c) heap[c] = c;  // load 0, already a heap
-    auto cmp = [](int64_t a, int64_t b) { return a > b; };
-    int64_t gi = 0;
-    for (int64_t j = 0; j < nq; ++j) {
-      const int32_t q = order[j];
-      const int64_t cost = (size[q] * hb + kItemOverhead) << 11;
-      const int64_t n_items = int64_t(ns[q]) * head_items;
-      for (int64_t t = 0; t < n_items; ++t, ++gi) {
-        std::pop_heap(heap.begin(), heap.end(), cmp);
-        const int32_t c = static_cast<int32_t>(heap.back() & 2047);
-        cta_of[gi] = c;
-        ++count[c + 1];
-        heap.back() += cost;
-        std::push_heap(heap.begin(), heap.end(), cmp);
+  int32_t* cta = o + o_cta(nq);
+  const int64_t items_pos = o_cta(nq) + grid + 1;
+  int32_t* items = o + items_pos;
+  // items are appended in line order; the comb list is built after them
+  int64_t n_items = 0, n_slots = 0;
+  std::vector<int32_t> comb;
+  const int64_t item_cap = (cap - items_pos) / kItemInts;
+  // remaining work on the line (pages + one overhead per unit or piece);
+  // each CTA's budget is the remaining work over the remaining CTAs, so
+  // rounding and snapped cuts never pile up on the last CTA
+  double remaining = double(line + ovh * (grid - 1));  // ~one cut per CTA boundary
+  int c = 0;           // current CTA
+  double budget = remaining / grid, used = 0.0;
+  cta[0] = 0;
+  auto next_cta = [&]() {
+    ++c;
+    cta[c] = static_cast<int32_t>(n_items);
+    budget = remaining / std::max(1, grid - c);
+    used = 0.0;
+  };
+  for (int64_t q = 0; q < nq; ++q) {
+    const int64_t pages = (int64_t(nk[q]) + ps - 1) / ps;
+    for (int h = 0; h < head_items; ++h) {
+      int64_t p0 = 0;
+      const int64_t first_item = n_items;
+      int npieces = 0;
+      while (p0 < pages) {
+        int64_t take = pages - p0;
+        const double room = budget - used - double(ovh);  // pages that still fit here
+        if (c < grid - 1 && room < double(take)) {
+          int64_t fit = static_cast<int64_t>(room + 0.5);
+          if (fit < min_piece) fit = 0;               // too small: start in the next CTA
+          if (take - fit < min_piece) fit = take;     // remainder too small: keep it here
+          take = fit;
+        }
+        if (take > 0) {
+          if (n_items >= item_cap) return fail(PKV_VALUE_ERROR, "plan buffer too small for items");
+          int32_t* r = items + n_items * kItemInts;
+          r[0] = static_cast<int32_t>(q);
+          r[1] = h;
+          r[2] = static_cast<int32_t>(p0);
+          r[3] = static_cast<int32_t>(p0 + take);
+          r[4] = -1;
+          r[5] = -1;
+          ++n_items;
+          ++npieces;
+          p0 += take;
+          used += double(take + ovh);
+          remaining -= double(take + ovh);
+        }
+        if (p0 < pages) next_cta();
       }
+      if (npieces > 1) {
+        const int32_t comb_idx = static_cast<int32_t>(comb.size() / kCombInts);
+        for (int k = 0; k < npieces; ++k) {
+          items[(first_item + k) * kItemInts + 4] = static_cast<int32_t>(n_slots++);
+          items[(first_item + k) * kItemInts + 5] = comb_idx;
+        }
+        comb.insert(comb.end(), {static_cast<int32_t>(q), h, static_cast<int32_t>(n_slots - npieces), npieces});
+      }
+      if (c < grid - 1 && used >= budget - 0.5) next_cta();  // segment filled exactly
     }
   }
-  const int64_t off_pos = o_cq(nq) + nq;
-  const int64_t items_pos = off_pos + grid + 1;
-  if (items_pos + total_items > cap) return fail(PKV_VALUE_ERROR, "plan buffer too small for %lld items",
-                                                  static_cast<long long>(total_items));
-  for (int c = 0; c < grid; ++c) count[c + 1] += count[c];
-  for (int c = 0; c <= grid; ++c) o[off_pos + c] = count[c];
-  for (int64_t gi = 0; gi < total_items; ++gi) o[items_pos + count[cta_of[gi]]++] = static_cast<int32_t>(gi);
-  const int64_t cur = total_items;
-  o[off_pos + grid] = static_cast<int32_t>(cur);
+  while (c < grid) cta[++c] = static_cast<int32_t>(n_items);
+  if (n_slots > 2 * int64_t(kMaxGrid)) return fail(PKV_CONFIG_ERROR, "too many partial slots");
+  const int64_t comb_pos = items_pos + n_items * kItemInts;
+  const int64_t ncomb = static_cast<int64_t>(comb.size() / kCombInts);
+  const int64_t ctr_pos = comb_pos + int64_t(comb.size());
+  if (ctr_pos + ncomb * kWarpsTc > cap) return fail(PKV_VALUE_ERROR, "plan buffer too small for comb");
+  std::copy(comb.begin(), comb.end(), o + comb_pos);
+  std::fill(o + ctr_pos, o + ctr_pos + ncomb * kWarpsTc, 0);
+  o[H_TOTAL_ITEMS] = static_cast<int32_t>(n_items);
+  o[H_NCOMB] = static_cast<int32_t>(comb.size() / kCombInts);
   o[H_GRID] = grid;
-  o[H_CTA_OFF] = static_cast<int32_t>(off_pos);
-  o[H_CTA_ITEMS] = static_cast<int32_t>(items_pos);
-  if (n_out) *n_out = items_pos + total_items;
+  o[H_CTA_OFF] = static_cast<int32_t>(o_cta(nq));
+  o[H_ITEMS] = static_cast<int32_t>(items_pos);
+  o[H_COMB] = static_cast<int32_t>(comb_pos);
+  o[H_CTR] = static_cast<int32_t>(ctr_pos);
+  if (n_out) *n_out = ctr_pos + ncomb * kWarpsTc;
   return PKV_OK;
 }
 
@@ -838,7 +804,7 @@ int launch_decode_tc(TcParams p, const int32_t* plan_host, int kv_dtype, int hea
   else
     fn = head_dim == 64 ? pick_rows<__half, 64>(splitq, rows16) : pick_rows<__half, 128>(splitq, rows16);
   const int merge_bytes = kWarpsTc * kMergeRows * head_dim * 4 + kWarpsTc * kMergeRows * 2 * 4;
-  const int64_t plan_bytes = o_cq(p.nq) * 4;
+  const int64_t plan_bytes = o_cta(p.nq) * 4;
   p.plan_in_smem = p.nq <= kSmemPlanMax;
   p.merge_offset = p.plan_in_smem ? static_cast<int>((plan_bytes + 127) / 128 * 128) : 0;
   p.ring_offset = (p.merge_offset + merge_bytes + 1023) / 1024 * 1024;
@@ -856,23 +822,6 @@ int launch_decode_tc(TcParams p, const int32_t* plan_host, int kv_dtype, int hea
   fn<<<grid, kThreadsTc, smem, stream>>>(p);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return fail(PKV_CUDA_ERROR, "decode_tc launch: %s", cudaGetErrorString(e));
-  const int nsq = plan_host[H_NSPLIT_Q];
-  if (nsq > 0) {
-    const int64_t tasks = int64_t(nsq) * p.hq * (head_dim / 32);
-    cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(static_cast<unsigned>(std::min<int64_t>((tasks + 7) / 8, int64_t(num_sms) * 8)));
-    cfg.blockDim = dim3(256);
-    cfg.dynamicSmemBytes = 0;
-    cfg.stream = stream;
-    cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    attr[0].val.programmaticStreamSerializationAllowed = 1;
-    cfg.attrs = attr;
-    cfg.numAttrs = 1;
-    e = head_dim == 64 ? cudaLaunchKernelEx(&cfg, combine_tc_kernel<64>, p)
-                       : cudaLaunchKernelEx(&cfg, combine_tc_kernel<128>, p);
-    if (e != cudaSuccess) return fail(PKV_CUDA_ERROR, "combine launch: %s", cudaGetErrorString(e));
-  }
   return PKV_OK;
 }
 

@@ -1,0 +1,72 @@
+"""Host planner of the tensor-core decode (no GPU): the stream-K style
+segment partition covers every (query, head item) page exactly once, pieces
+of a cut unit get consecutive partial slots and one combine record, and CTA
+loads are balanced."""
+
+import numpy as np
+import pytest
+
+from paper_2506_07311_b200 import _lib
+from paper_2506_07311_b200.workloads import config_lengths
+
+HDR = 13
+
+
+def parse(plan):
+    hb, wph, qgs, qgroups, head_items, total, ncomb, nq, grid, cta_off, items_off, comb_off, ctr_off = plan[:HDR]
+    nk = plan[HDR:HDR + nq]
+    cta = plan[cta_off:cta_off + grid + 1]
+    items = plan[items_off:items_off + 6 * total].reshape(-1, 6)
+    assert (plan[ctr_off:ctr_off + 8 * ncomb] == 0).all() and ctr_off + 8 * ncomb == plan.size
+    comb = plan[comb_off:comb_off + 4 * ncomb].reshape(-1, 4)
+    return dict(hb=hb, wph=wph, head_items=head_items, nq=nq, grid=grid, nk=nk, cta=cta, items=items, comb=comb)
+
+
+CASES = [
+    ("c2", config_lengths("c2"), 32, 32),
+    ("c3-b64", [8192] * 64, 32, 8),
+    ("c3-b1-32k", [32768], 32, 8),
+    ("c5", config_lengths("c5"), 32, 8),
+    ("tiny", [1, 2, 17], 8, 2),
+    ("many", list(np.random.default_rng(3).integers(1, 40, 2500)), 4, 2),
+]
+
+
+@pytest.mark.parametrize("name,lengths,hq,hkv", CASES, ids=[c[0] for c in CASES])
+def test_segment_plan_covers_every_page_once(name, lengths, hq, hkv):
+    ps = 16
+    nk = np.asarray(lengths, dtype=np.int32)
+    plan = _lib.attention_plan(nk, np.arange(nk.size, dtype=np.int32), ps, hq, hkv)
+    P = parse(plan)
+    assert P["nq"] == nk.size and np.array_equal(P["nk"], nk)
+    items, comb = P["items"], P["comb"]
+    cta = P["cta"]
+    assert cta[0] == 0 and cta[-1] == len(items) and (np.diff(cta) >= 0).all()
+    pages = -(-nk.astype(np.int64) // ps)
+    covered = {}
+    for q, h, p0, p1, slot, ci in items:
+        assert 0 <= p0 < p1 <= pages[q]
+        covered.setdefault((q, h), []).append((p0, p1, slot))
+        assert (slot < 0) == (ci < 0) and (ci < 0 or tuple(comb[ci][:2]) == (q, h))
+    assert len(covered) == nk.size * P["head_items"]
+    comb_map = {(q, h): (s0, n) for q, h, s0, n in comb}
+    slots = []
+    for (q, h), pieces in covered.items():
+        assert pieces[0][0] == 0 and pieces[-1][1] == pages[q]
+        assert all(a[1] == b[0] for a, b in zip(pieces, pieces[1:]))  # contiguous, in order
+        if len(pieces) == 1:
+            assert pieces[0][2] == -1 and (q, h) not in comb_map
+        else:
+            s0, n = comb_map[(q, h)]
+            assert n == len(pieces) and [p[2] for p in pieces] == list(range(s0, s0 + n))
+            slots += list(range(s0, s0 + n))
+    assert sorted(slots) == list(range(len(slots)))
+    # balance: bytes per CTA within one max piece of the mean
+    load = np.zeros(P["grid"])
+    for c in range(P["grid"]):
+        for q, h, p0, p1, _, _ in items[cta[c]:cta[c + 1]]:
+            load[c] += p1 - p0
+    if P["grid"] > 1:
+        assert load.max() <= load.mean() * 1.15 + 64, (load.max(), load.mean())
+    # few items per CTA
+    assert len(items) <= nk.size * P["head_items"] + 2 * P["grid"]

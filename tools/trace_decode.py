@@ -28,8 +28,10 @@ q = torch.randn((B, cfg.head_count, 128), device=dev).bfloat16()
 lib = _lib.load()
 for _ in range(3):
     paged_attention(q, store, meta, cfg)
+import os
 flush = torch.ones(64 << 20, device=dev)
-flush.sum()
+if not os.environ.get("WARM"):
+    flush.sum()
 torch.cuda.synchronize()
 lib.pkv_debug_trace(1, None, 0)
 paged_attention(q, store, meta, cfg)
@@ -59,11 +61,17 @@ for c in range(148):
                 gaps["stored->next start"].append(nxt - st)
 for k_, v in gaps.items():
     v = np.array(v)
+    if v.size == 0:
+        continue
     print("%-26s n=%5d mean %6.2f  p50 %6.2f  p90 %6.2f  max %6.2f  sum/warp %6.2f" % (
         k_, v.size, v.mean(), np.median(v), np.percentile(v, 90), v.max(), v.sum() / (148 * 8)))
 ends = np.nanmax(rel[:, :, 31], axis=1)
+starts = np.nanmin(rel[:, :, 0], axis=1)
+print("CTA start deciles:", np.round(np.sort(starts)[::15], 1))
+first = np.nanmin(rel[:, :, 2], axis=1)
+print("CTA first-item deciles:", np.round(np.sort(first)[::15], 1))
 print("CTA end deciles:", np.round(np.sort(ends)[::15], 1))
-for c in [0, int(np.nanargmax(ends))]:
+for c in [0, int(np.argsort(ends)[len(ends) // 2]), int(np.nanargmax(ends))]:
     print("cta", c)
     for w in range(8):
         items = []
@@ -72,4 +80,5 @@ for c in [0, int(np.nanargmax(ends))]:
             if np.isnan(s):
                 break
             items.append("[%.1f f%.1f d%.1f s%.1f]" % (s, f, d, st))
-        print("  w%d" % w, " ".join(items), "end %.1f" % rel[c, w, 31])
+        print("  w%d" % w, " ".join(items), "merged %.1f stored %.1f finished %.1f end %.1f" % (
+            rel[c, w, 28], rel[c, w, 29], rel[c, w, 30], rel[c, w, 31]))
