@@ -497,12 +497,12 @@ __global__ void __launch_bounds__(kThreadsTc, 1) decode_tc_kernel(const __grid_c
         mx0 = fmaxf(mx0, __shfl_xor_sync(0xffffffffu, mx0, 1));
         mx0 = fmaxf(mx0, __shfl_xor_sync(0xffffffffu, mx0, 2));
         const float mn0 = fmaxf(m0, mx0 * qscale);
-        const float c0 = exp2f(m0 - mn0);
+        const float c0 = ex2_ftz(m0 - mn0);
         m0 = mn0;
         uint32_t pa[4];
         {
-          const float p00 = exp2f(fmaf(s0[0], qscale, -mn0)), p01 = exp2f(fmaf(s0[1], qscale, -mn0));
-          const float p10 = exp2f(fmaf(s1[0], qscale, -mn0)), p11 = exp2f(fmaf(s1[1], qscale, -mn0));
+          const float p00 = ex2_ftz(fmaf(s0[0], qscale, -mn0)), p01 = ex2_ftz(fmaf(s0[1], qscale, -mn0));
+          const float p10 = ex2_ftz(fmaf(s1[0], qscale, -mn0)), p11 = ex2_ftz(fmaf(s1[1], qscale, -mn0));
           pa[0] = pack2<T>(p00, p01);
           pa[2] = pack2<T>(p10, p11);
           l0 = l0 * c0 + (unpack_sum<T>(pa[0]) + unpack_sum<T>(pa[2]));
@@ -513,10 +513,10 @@ __global__ void __launch_bounds__(kThreadsTc, 1) decode_tc_kernel(const __grid_c
           mx1 = fmaxf(mx1, __shfl_xor_sync(0xffffffffu, mx1, 1));
           mx1 = fmaxf(mx1, __shfl_xor_sync(0xffffffffu, mx1, 2));
           const float mn1 = fmaxf(m1, mx1 * qscale);
-          c1 = exp2f(m1 - mn1);
+          c1 = ex2_ftz(m1 - mn1);
           m1 = mn1;
-          const float p02 = exp2f(fmaf(s0[2], qscale, -mn1)), p03 = exp2f(fmaf(s0[3], qscale, -mn1));
-          const float p12 = exp2f(fmaf(s1[2], qscale, -mn1)), p13 = exp2f(fmaf(s1[3], qscale, -mn1));
+          const float p02 = ex2_ftz(fmaf(s0[2], qscale, -mn1)), p03 = ex2_ftz(fmaf(s0[3], qscale, -mn1));
+          const float p12 = ex2_ftz(fmaf(s1[2], qscale, -mn1)), p13 = ex2_ftz(fmaf(s1[3], qscale, -mn1));
           pa[1] = pack2<T>(p02, p03);
           pa[3] = pack2<T>(p12, p13);
           l1 = l1 * c1 + (unpack_sum<T>(pa[1]) + unpack_sum<T>(pa[3]));

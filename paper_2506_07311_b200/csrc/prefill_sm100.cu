@@ -334,19 +334,22 @@ __global__ void __launch_bounds__(kThreads, 1)
       float factor = 1.f;
       const bool need = mx > m_used + kRescaleThreshold;
       if (need) {
-        factor = exp2f(m_used - mx);  // 0 on the first tile (m_used = -inf)
+        factor = ex2_ftz(m_used - mx);  // 0 on the first tile (m_used = -inf)
         m_used = mx;
       }
       l *= factor;
-      const float negm = -m_used;
+      const float2 negm2 = make_float2(-m_used, -m_used);
+      const float2 qs2 = make_float2(p.qscale, p.qscale);
       uint32_t pk[kN / 2];
+      float2 l2 = make_float2(0.f, 0.f);
 #pragma unroll
       for (int c = 0; c < kN; c += 2) {
-        const float p0 = exp2f(fmaf(s[c], p.qscale, negm));
-        const float p1 = exp2f(fmaf(s[c + 1], p.qscale, negm));
-        l += p0 + p1;
-        pk[c >> 1] = pack2<T>(p0, p1);
+        const float2 t = ffma2(make_float2(s[c], s[c + 1]), qs2, negm2);
+        const float2 pp = make_float2(ex2_ftz(t.x), ex2_ftz(t.y));
+        l2 = fadd2(l2, pp);
+        pk[c >> 1] = pack2<T>(pp.x, pp.y);
       }
+      l += l2.x + l2.y;
       // O and the P buffer are free once PV_{j-1} completed
       if (j > 0) {
         mbar_wait(bar(B_PE), (j - 1) & 1);
