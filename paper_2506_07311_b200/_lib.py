@@ -17,6 +17,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libpkv200.so")
 
 PKV_F32, PKV_F16, PKV_BF16 = 0, 1, 2
+PREFILL_ITEM_INTS = 10  # {q_row0, cnt_a, cnt_b, qpos0, kv_len, row, kv_head, tiles_a, tiles_b, 0}
 
 _STATUS = {
     1: errors.CapacityExhausted,
@@ -159,7 +160,7 @@ def attention_plan(q_nkeys, q_row, page_size: int, hq: int, hkv: int, target_wav
 
 def prefill_plan(q_start, q_len, seq_len, seq_row, hq: int, hkv: int, causal: bool):
     """Host work plan of the tcgen05 prefill (pkv_prefill_plan) as int32 numpy
-    [n_items, 8]."""
+    [n_items, PREFILL_ITEM_INTS]."""
     import numpy as np
 
     qs = np.ascontiguousarray(q_start, dtype=np.int64)
@@ -168,9 +169,9 @@ def prefill_plan(q_start, q_len, seq_len, seq_row, hq: int, hkv: int, causal: bo
     sr = np.ascontiguousarray(seq_row, dtype=np.int32)
     lib = load()
     cap = int(lib.pkv_prefill_plan_ints(ql.ctypes.data, ql.size, hq, hkv))
-    out = np.empty(max(cap, 8), dtype=np.int32)
+    out = np.empty(max(cap, PREFILL_ITEM_INTS), dtype=np.int32)
     got = C.c_int64()
     check(lib.pkv_prefill_plan(qs.ctypes.data, ql.ctypes.data, sl.ctypes.data, sr.ctypes.data, ql.size,
                                hq, hkv, int(bool(causal)), out.ctypes.data, out.size, C.byref(got)),
           "pkv_prefill_plan")
-    return out[: 8 * got.value].reshape(-1, 8).copy()
+    return out[: PREFILL_ITEM_INTS * got.value].reshape(-1, PREFILL_ITEM_INTS).copy()

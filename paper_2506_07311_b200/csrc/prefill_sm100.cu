@@ -47,12 +47,12 @@
 namespace pkv {
 namespace {
 
-constexpr int kThreads = 256;
+constexpr int kThreads = 384;  // 4 control warps + 2 softmax warpgroups
 constexpr int kM = 128;          // query rows per item (MMA M)
 constexpr int kN = 128;          // keys per tile (MMA N of QK^T, K of PV)
 constexpr int kRowB = 128;       // bytes per swizzled row (64 x 16-bit)
 constexpr int kChunkB = kM * kRowB;  // one 64-column chunk of a 128-row tile: 16 KB
-constexpr int kItemInts = 8;
+constexpr int kItemInts = 10;
 constexpr float kLog2eP = 1.4426950408889634f;
 constexpr float kRescaleThreshold = 8.0f;  // log2 units
 
@@ -170,37 +170,61 @@ struct Fmt<__half> {
   static constexpr uint32_t kFmt = 0;
 };
 
+// tcgen05.mma with the A operand (P) read from tensor memory
+__device__ __forceinline__ void tc_mma_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_t b_desc, uint32_t idesc,
+                                          uint32_t accumulate) {
+  asm volatile(
+      "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
+      " tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n}\n" ::"r"(d_tmem),
+      "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+// 16 consecutive 32-bit TMEM columns of this thread's lane
+__device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t* v) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, "
+      "%13, %14, %15, %16};\n" ::"r"(taddr),
+      "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]), "r"(v[8]),
+      "r"(v[9]), "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]), "r"(v[15])
+      : "memory");
+}
+
+// Two query tiles (A: item rows 0-127, B: rows 128-255) share every K/V
+// tile.  TMEM: S_A | S_B | O_A | O_B; P_t (16-bit) overwrites the first 64
+// columns of S_t and is the A operand of O_t += P_t V.  Per tile the chain
+// QK_t(j) -> softmax_t(j) -> PV_t(j) -> QK_t(j+1) is serial (P aliases S, and
+// the MMAs of one issuing thread execute in order), so the two tiles
+// ping-pong: while one softmax warpgroup works, the tensor core runs the
+// other tile's PV and next QK.
 template <typename T, int D>
 __global__ void __launch_bounds__(kThreads, 1)
     prefill_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
                       const __grid_constant__ CUtensorMap tm_v, const __grid_constant__ PrefillParams p) {
   constexpr int NCH = D / 64;                 // 64-column chunks of the head dim
-  constexpr int kQBytes = NCH * kChunkB;      // Q tile
+  constexpr int kQBytes = NCH * kChunkB;      // one Q tile
   constexpr int kKVBytes = NCH * kChunkB;     // one K (or V) tile of 128 keys
-  constexpr int kPBytes = (kN / 64) * kChunkB;
   constexpr uint32_t kIdescQK = instr_desc(Fmt<T>::kFmt, 0, kM, kN);
   constexpr uint32_t kIdescPV = instr_desc(Fmt<T>::kFmt, 1, kM, D);
   constexpr uint32_t kTmemCols = 512;
-  constexpr uint32_t kColO = 2 * kN;
 
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  const uint32_t sQ = smem_addr(smem);
-  const uint32_t sK = sQ + kQBytes;                 // 2 stages
-  const uint32_t sV = sK + 2 * kKVBytes;            // 2 stages
-  const uint32_t sP = sV + 2 * kKVBytes;
-  uint8_t* sPp = smem + (sP - sQ);
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + (sP - sQ) + kPBytes);
-  // barrier slots
-  enum { B_Q = 0, B_KF = 1, B_VF = 3, B_KE = 5, B_VE = 7, B_SF = 9, B_SE = 11, B_PF = 13, B_PE = 14, B_N = 15 };
+  const uint32_t sQ = smem_addr(smem);                // 2 tiles
+  const uint32_t sK = sQ + 2 * kQBytes;               // 2 stages
+  const uint32_t sV = sK + 2 * kKVBytes;              // 2 stages
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + 2 * kQBytes + 4 * kKVBytes);
+  enum { B_Q = 0, B_KF = 1, B_VF = 3, B_KE = 5, B_VE = 7, B_SF = 9, B_PF = 11, B_OD = 13, B_N = 15 };
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + B_N);
   auto bar = [&](int i) { return smem_addr(bars + i); };
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
   const int32_t* it = p.items + static_cast<int64_t>(blockIdx.x) * kItemInts;
-  const int q_row0 = it[0], q_count = it[1], qpos0 = it[2], kv_len = it[3];
-  const int mrow = it[4], kvh = it[5], n_tiles = it[6];
+  const int q_row0 = it[0], qpos0 = it[3], kv_len = it[4];
+  const int mrow = it[5], kvh = it[6];
+  const int cnt[2] = {it[1], it[2]};
+  const int nt[2] = {it[7], it[8]};
+  const int n_tiles = max(nt[0], nt[1]);
 
   if (threadIdx.x == 0) {
     mbar_init(bar(B_Q), 1);
@@ -210,10 +234,9 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(bar(B_KE + s), 1);
       mbar_init(bar(B_VE + s), 1);
       mbar_init(bar(B_SF + s), 1);
-      mbar_init(bar(B_SE + s), 128);
+      mbar_init(bar(B_PF + s), 128);
+      mbar_init(bar(B_OD + s), 1);
     }
-    mbar_init(bar(B_PF), 128);
-    mbar_init(bar(B_PE), 1);
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
   if (warp == 2) {
@@ -233,15 +256,17 @@ __global__ void __launch_bounds__(kThreads, 1)
       // ---------------- TMA producer ----------------
       asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<uint64_t>(&tm_k)) : "memory");
       asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<uint64_t>(&tm_v)) : "memory");
-      mbar_expect_tx(bar(B_Q), kQBytes);
-      for (int c = 0; c < NCH; ++c) tma_load_3d(sQ + c * kChunkB, &tm_q, bar(B_Q), c * 64, kvh * p.group, q_row0);
+      const int ntiles_q = cnt[1] > 0 ? 2 : 1;
+      mbar_expect_tx(bar(B_Q), kQBytes * ntiles_q);
+      for (int t = 0; t < ntiles_q; ++t)
+        for (int c = 0; c < NCH; ++c)
+          tma_load_3d(sQ + t * kQBytes + c * kChunkB, &tm_q, bar(B_Q), c * 64, kvh * p.group, q_row0 + t * p.qt);
       const int ps = 1 << p.log2ps;
       const int n_pages = (kv_len + ps - 1) >> p.log2ps;
       const int boxes = kN / p.box_rows;
       const int32_t* tbl = p.bt ? p.bt + static_cast<int64_t>(mrow) * p.bt_stride : nullptr;
       for (int j = 0; j < n_tiles; ++j) {
         const int st = j & 1;
-        // rows of this tile's boxes (block-table walk, OOB row past the table)
         int rows[16];
         for (int b = 0; b < boxes; ++b) {
           const int key0 = j * kN + b * p.box_rows;
@@ -271,65 +296,75 @@ __global__ void __launch_bounds__(kThreads, 1)
       // ---------------- MMA issuer ----------------
       mbar_wait(bar(B_Q), 0);
       tc_fence_after();
-      auto issue_pv = [&](int i) {
-        const int st = i & 1;
-        mbar_wait(bar(B_PF), i & 1);
-        mbar_wait(bar(B_VF + st), (i >> 1) & 1);
+      auto issue_qk = [&](int t, int j) {
+        const int st = j & 1;
+#pragma unroll
+        for (int k = 0; k < D / 16; ++k) {
+          const uint64_t ad = smem_desc(sQ + t * kQBytes + (k >> 2) * kChunkB + (k & 3) * 32, 16, 1024);
+          const uint64_t bd = smem_desc(sK + st * kKVBytes + (k >> 2) * kChunkB + (k & 3) * 32, 16, 1024);
+          tc_mma(tmem + t * kN, ad, bd, kIdescQK, k > 0 ? 1u : 0u);
+        }
+        tc_commit(bar(B_SF + t));
+      };
+      auto issue_pv = [&](int t, int j) {
+        const int st = j & 1;
+        mbar_wait(bar(B_VF + st), (j >> 1) & 1);
+        mbar_wait(bar(B_PF + t), j & 1);
         tc_fence_after();
 #pragma unroll
         for (int k = 0; k < kN / 16; ++k) {
-          // A = P (K-major, 64-key chunks), B = V (MN-major: LBO = chunk stride, SBO = 8 keys)
-          const uint64_t ad = smem_desc(sP + (k >> 2) * kChunkB + (k & 3) * 32, 16, 1024);
+          // A = P_t in TMEM (16 keys = 8 packed columns per step), B = V (MN-major)
           const uint64_t bd = smem_desc(sV + st * kKVBytes + k * 16 * kRowB, kChunkB, 1024);
-          tc_mma(tmem + kColO, ad, bd, kIdescPV, (i > 0 || k > 0) ? 1u : 0u);
+          tc_mma_ts(tmem + 2 * kN + t * D, tmem + t * kN + k * 8, bd, kIdescPV, (j > 0 || k > 0) ? 1u : 0u);
         }
-        tc_commit(bar(B_VE + st));
-        tc_commit(bar(B_PE));
       };
-      for (int j = 0; j < n_tiles; ++j) {
+      // iteration j issues, per tile t: PV_t(j-1) (P_t(j-1) must be consumed
+      // before QK_t(j) overwrites it) then QK_t(j); j == n_tiles drains
+      for (int j = 0; j <= n_tiles; ++j) {
         const int st = j & 1;
-        if (j >= 2) mbar_wait(bar(B_SE + st), ((j >> 1) - 1) & 1);
-        mbar_wait(bar(B_KF + st), (j >> 1) & 1);
-        tc_fence_after();
-#pragma unroll
-        for (int k = 0; k < D / 16; ++k) {
-          const uint64_t ad = smem_desc(sQ + (k >> 2) * kChunkB + (k & 3) * 32, 16, 1024);
-          const uint64_t bd = smem_desc(sK + st * kKVBytes + (k >> 2) * kChunkB + (k & 3) * 32, 16, 1024);
-          tc_mma(tmem + st * kN, ad, bd, kIdescQK, k > 0 ? 1u : 0u);
+        if (j < n_tiles) {
+          mbar_wait(bar(B_KF + st), (j >> 1) & 1);
+          tc_fence_after();
         }
-        tc_commit(bar(B_KE + st));
-        tc_commit(bar(B_SF + st));
-        if (j >= 1) issue_pv(j - 1);
+        for (int t = 0; t < 2; ++t) {
+          if (j > 0 && j - 1 < nt[t]) issue_pv(t, j - 1);
+          if (j < nt[t]) issue_qk(t, j);
+          if (j == nt[t] && nt[t] > 0) tc_commit(bar(B_OD + t));  // after its final PV
+        }
+        if (j < n_tiles) tc_commit(bar(B_KE + st));
+        if (j > 0) tc_commit(bar(B_VE + ((j - 1) & 1)));  // every PV of V tile j-1 is issued
       }
-      if (n_tiles > 0) issue_pv(n_tiles - 1);
     }
   } else if (warp >= 4) {
-    // ---------------- softmax + epilogue (thread = query row) ----------------
-    const int r = threadIdx.x - 128;
+    // ---------------- softmax + epilogue: warpgroup t, thread = query row ----------------
+    const int t = (warp - 4) >> 2;
+    const int r = threadIdx.x - 128 - 128 * t;
     const uint32_t lane_base = static_cast<uint32_t>((warp & 3) * 32) << 16;
+    const uint32_t tS = tmem + lane_base + t * kN;
+    const uint32_t tO = tmem + lane_base + 2 * kN + t * D;
     const int qi = r / p.group;
-    const int qpos = qpos0 + qi;
+    const int qpos = qpos0 + t * p.qt + qi;
     const int nk = p.causal ? min(qpos + 1, kv_len) : kv_len;  // allowed key prefix of this row
     float m_used = -INFINITY, l = 0.f;
-    for (int j = 0; j < n_tiles; ++j) {
-      const int st = j & 1;
-      mbar_wait(bar(B_SF + st), (j >> 1) & 1);
+    const float2 qs2 = make_float2(p.qscale, p.qscale);
+    for (int j = 0; j < nt[t]; ++j) {
+      mbar_wait(bar(B_SF + t), j & 1);
       tc_fence_after();
-      float s[kN];
-#pragma unroll
-      for (int c = 0; c < kN / 32; ++c) tmem_ld32(tmem + lane_base + st * kN + c * 32, reinterpret_cast<uint32_t*>(s + c * 32));
-      tmem_wait_ld();
-      tc_fence_before();
-      mbar_arrive(bar(B_SE + st));
       const int kbase = j * kN;
-      if (kbase + kN > nk) {
+      const bool masked = kbase + kN > nk;
+      // pass 1: row max (S read from TMEM in 32-column chunks)
+      float mx = -INFINITY;
+#pragma unroll 1
+      for (int c = 0; c < kN / 32; ++c) {
+        uint32_t v[32];
+        tmem_ld32(tS + c * 32, v);
+        tmem_wait_ld();
 #pragma unroll
-        for (int c = 0; c < kN; ++c)
-          if (kbase + c >= nk) s[c] = -INFINITY;
+        for (int e = 0; e < 32; ++e) {
+          const float x = (masked && kbase + c * 32 + e >= nk) ? -INFINITY : __uint_as_float(v[e]);
+          mx = fmaxf(mx, x);
+        }
       }
-      float mx = s[0];
-#pragma unroll
-      for (int c = 1; c < kN; ++c) mx = fmaxf(mx, s[c]);
       mx *= p.qscale;
       float factor = 1.f;
       const bool need = mx > m_used + kRescaleThreshold;
@@ -338,78 +373,78 @@ __global__ void __launch_bounds__(kThreads, 1)
         m_used = mx;
       }
       l *= factor;
-      const float2 negm2 = make_float2(-m_used, -m_used);
-      const float2 qs2 = make_float2(p.qscale, p.qscale);
-      uint32_t pk[kN / 2];
-      float2 l2 = make_float2(0.f, 0.f);
-#pragma unroll
-      for (int c = 0; c < kN; c += 2) {
-        const float2 t = ffma2(make_float2(s[c], s[c + 1]), qs2, negm2);
-        const float2 pp = make_float2(ex2_ftz(t.x), ex2_ftz(t.y));
-        l2 = fadd2(l2, pp);
-        pk[c >> 1] = pack2<T>(pp.x, pp.y);
-      }
-      l += l2.x + l2.y;
-      // O and the P buffer are free once PV_{j-1} completed
-      if (j > 0) {
-        mbar_wait(bar(B_PE), (j - 1) & 1);
-        tc_fence_after();
-        if (__any_sync(0xffffffffu, need)) {
+      // O_t is stable here: PV_t(j-1) completed before S_t(j) was committed
+      if (j > 0 && __any_sync(0xffffffffu, need)) {
 #pragma unroll 1
-          for (int c = 0; c < D / 32; ++c) {
-            uint32_t o[32];
-            tmem_ld32(tmem + lane_base + kColO + c * 32, o);
-            tmem_wait_ld();
+        for (int c = 0; c < D / 32; ++c) {
+          uint32_t o[32];
+          tmem_ld32(tO + c * 32, o);
+          tmem_wait_ld();
 #pragma unroll
-            for (int e = 0; e < 32; ++e) o[e] = __float_as_uint(__uint_as_float(o[e]) * factor);
-            tmem_st32(tmem + lane_base + kColO + c * 32, o);
-          }
-          tmem_wait_st();
+          for (int e = 0; e < 32; ++e) o[e] = __float_as_uint(__uint_as_float(o[e]) * factor);
+          tmem_st32(tO + c * 32, o);
         }
       }
-      // P row -> swizzled K-major smem (16-byte chunk q of 64-key chunk kc)
+      // pass 2: P = 2^(s*qscale - m) rounded to 16 bits, written over S
+      const float2 negm2 = make_float2(-m_used, -m_used);
+      float2 l2 = make_float2(0.f, 0.f);
+#pragma unroll 1
+      for (int c = 0; c < kN / 32; ++c) {
+        uint32_t v[32], pk[16];
+        tmem_ld32(tS + c * 32, v);
+        tmem_wait_ld();
 #pragma unroll
-      for (int q = 0; q < kN / 8; ++q) {
-        const int kc = q >> 3, inner = q & 7;
-        uint8_t* dst = sPp + kc * kChunkB + r * kRowB + ((inner ^ (r & 7)) << 4);
-        *reinterpret_cast<uint4*>(dst) = make_uint4(pk[4 * q], pk[4 * q + 1], pk[4 * q + 2], pk[4 * q + 3]);
+        for (int e = 0; e < 32; e += 2) {
+          float2 x = make_float2(__uint_as_float(v[e]), __uint_as_float(v[e + 1]));
+          if (masked) {
+            if (kbase + c * 32 + e >= nk) x.x = -INFINITY;
+            if (kbase + c * 32 + e + 1 >= nk) x.y = -INFINITY;
+          }
+          const float2 tt = ffma2(x, qs2, negm2);
+          const float2 pp = make_float2(ex2_ftz(tt.x), ex2_ftz(tt.y));
+          l2 = fadd2(l2, pp);
+          pk[e >> 1] = pack2<T>(pp.x, pp.y);
+        }
+        tmem_st16(tS + c * 16, pk);
       }
-      asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+      l += l2.x + l2.y;
+      tmem_wait_st();
       tc_fence_before();
-      mbar_arrive(bar(B_PF));
+      mbar_arrive(bar(B_PF + t));
     }
     // epilogue: O / l for the valid rows
-    if (n_tiles > 0) {
-      mbar_wait(bar(B_PE), (n_tiles - 1) & 1);
+    if (nt[t] > 0) {
+      mbar_wait(bar(B_OD + t), 0);
       tc_fence_after();
-    }
-    const bool valid = qi < q_count;
-    const float inv = l > 0.f ? 1.f / l : 0.f;
-    const int64_t orow = (static_cast<int64_t>(q_row0) + qi) * p.hq + kvh * p.group + (r - qi * p.group);
+      const bool valid = qi < cnt[t];
+      const float inv = l > 0.f ? 1.f / l : 0.f;
+      const int64_t orow =
+          (static_cast<int64_t>(q_row0) + t * p.qt + qi) * p.hq + kvh * p.group + (r - qi * p.group);
 #pragma unroll 1
-    for (int c = 0; c < D / 32; ++c) {
-      uint32_t o[32];
-      tmem_ld32(tmem + lane_base + kColO + c * 32, o);
-      tmem_wait_ld();
-      if (valid) {
-        if (p.out_dtype == PKV_F32) {
-          float4* dst = reinterpret_cast<float4*>(static_cast<float*>(p.out) + orow * D + c * 32);
+      for (int c = 0; c < D / 32; ++c) {
+        uint32_t o[32];
+        tmem_ld32(tO + c * 32, o);
+        tmem_wait_ld();
+        if (valid) {
+          if (p.out_dtype == PKV_F32) {
+            float4* dst = reinterpret_cast<float4*>(static_cast<float*>(p.out) + orow * D + c * 32);
 #pragma unroll
-          for (int e = 0; e < 8; ++e)
-            dst[e] = make_float4(__uint_as_float(o[4 * e]) * inv, __uint_as_float(o[4 * e + 1]) * inv,
-                                 __uint_as_float(o[4 * e + 2]) * inv, __uint_as_float(o[4 * e + 3]) * inv);
-        } else {
-          uint4* dst = reinterpret_cast<uint4*>(static_cast<uint16_t*>(p.out) + orow * D + c * 32);
+            for (int e = 0; e < 8; ++e)
+              dst[e] = make_float4(__uint_as_float(o[4 * e]) * inv, __uint_as_float(o[4 * e + 1]) * inv,
+                                   __uint_as_float(o[4 * e + 2]) * inv, __uint_as_float(o[4 * e + 3]) * inv);
+          } else {
+            uint4* dst = reinterpret_cast<uint4*>(static_cast<uint16_t*>(p.out) + orow * D + c * 32);
 #pragma unroll
-          for (int e = 0; e < 4; ++e) {
-            uint32_t w[4];
+            for (int e = 0; e < 4; ++e) {
+              uint32_t w[4];
 #pragma unroll
-            for (int h = 0; h < 4; ++h) {
-              const float a = __uint_as_float(o[8 * e + 2 * h]) * inv;
-              const float b = __uint_as_float(o[8 * e + 2 * h + 1]) * inv;
-              w[h] = p.out_dtype == PKV_BF16 ? pack2<__nv_bfloat16>(a, b) : pack2<__half>(a, b);
+              for (int h = 0; h < 4; ++h) {
+                const float a = __uint_as_float(o[8 * e + 2 * h]) * inv;
+                const float b = __uint_as_float(o[8 * e + 2 * h + 1]) * inv;
+                w[h] = p.out_dtype == PKV_BF16 ? pack2<__nv_bfloat16>(a, b) : pack2<__half>(a, b);
+              }
+              dst[e] = make_uint4(w[0], w[1], w[2], w[3]);
             }
-            dst[e] = make_uint4(w[0], w[1], w[2], w[3]);
           }
         }
       }
@@ -462,7 +497,7 @@ template <typename T, int D>
 size_t smem_bytes() {
   constexpr int NCH = D / 64;
   // at least 116 KB: one CTA per SM, so the 512-column TMEM allocation never waits
-  return std::max<size_t>(1024 + NCH * kChunkB * 5 + (kN / 64) * kChunkB + 16 * 8 + 16, 116 * 1024);
+  return std::max<size_t>(1024 + NCH * kChunkB * 6 + 16 * 8 + 16, 116 * 1024);
 }
 
 template <typename T, int D>
@@ -509,11 +544,14 @@ extern "C" int pkv_prefill_supported(int32_t hq, int32_t hkv, int32_t head_dim, 
 extern "C" int64_t pkv_prefill_plan_ints(const int32_t* q_len, int64_t n_seqs, int32_t hq, int32_t hkv) {
   if (hq <= 0 || hkv <= 0 || hq % hkv || n_seqs < 0) return 0;
   const int qt = query_tile(hq, hkv);
-  int64_t tiles = 0;
-  for (int64_t s = 0; s < n_seqs; ++s) tiles += (std::max(q_len[s], 0) + qt - 1) / qt;
-  return tiles * hkv * kItemInts;
+  int64_t pairs = 0;
+  for (int64_t s = 0; s < n_seqs; ++s) pairs += (std::max(q_len[s], 0) + 2 * qt - 1) / (2 * qt);
+  return pairs * hkv * kItemInts;
 }
 
+// Work items: one kv head x two consecutive query tiles (A, B) of 128/G
+// positions each; per tile the key range is the causal prefix of its last
+// valid query (n_tiles of 128 keys).  Longest first.
 extern "C" int pkv_prefill_plan(const int64_t* q_start, const int32_t* q_len, const int32_t* seq_len,
                                 const int32_t* seq_row, int64_t n_seqs, int32_t hq, int32_t hkv,
                                 int32_t causal, int32_t* plan_out, int64_t cap, int64_t* n_items_out) {
@@ -530,27 +568,35 @@ extern "C" int pkv_prefill_plan(const int64_t* q_start, const int32_t* q_len, co
     if (ql < 0 || ql > kl) return fail(PKV_OUT_OF_RANGE, "sequence %lld: %d queries over %d keys",
                                        static_cast<long long>(s), ql, kl);
     if (q_start[s] + ql > (int64_t(1) << 31)) return fail(PKV_OUT_OF_RANGE, "query rows beyond 2^31");
-    for (int t = 0; t * qt < ql; ++t) {
-      const int cnt = std::min(qt, ql - t * qt);
-      const int pos0 = kl - ql + t * qt;
-      const int nk = causal ? std::min(pos0 + cnt, kl) : kl;  // keys of the last valid row
-      const int tiles = (nk + kN - 1) / kN;
+    for (int t0 = 0; t0 * qt < ql; t0 += 2) {
+      int cnt[2], tiles[2];
+      for (int u = 0; u < 2; ++u) {
+        const int first = (t0 + u) * qt;
+        cnt[u] = std::max(0, std::min(qt, ql - first));
+        const int pos0 = kl - ql + first;
+        const int nk = causal ? std::min(pos0 + cnt[u], kl) : kl;  // keys of the tile's last row
+        tiles[u] = cnt[u] > 0 ? (nk + kN - 1) / kN : 0;
+      }
       for (int h = 0; h < hkv; ++h) {
         Rec r;
-        r.v[0] = static_cast<int32_t>(q_start[s] + int64_t(t) * qt);
-        r.v[1] = cnt;
-        r.v[2] = pos0;
-        r.v[3] = kl;
-        r.v[4] = seq_row[s];
-        r.v[5] = h;
-        r.v[6] = tiles;
-        r.v[7] = 0;
+        r.v[0] = static_cast<int32_t>(q_start[s] + int64_t(t0) * qt);
+        r.v[1] = cnt[0];
+        r.v[2] = cnt[1];
+        r.v[3] = kl - ql + t0 * qt;
+        r.v[4] = kl;
+        r.v[5] = seq_row[s];
+        r.v[6] = h;
+        r.v[7] = tiles[0];
+        r.v[8] = tiles[1];
+        r.v[9] = 0;
         items.push_back(r);
       }
     }
   }
   // longest items first: the hardware block scheduler then approximates LPT
-  std::stable_sort(items.begin(), items.end(), [](const Rec& x, const Rec& y) { return x.v[6] > y.v[6]; });
+  std::stable_sort(items.begin(), items.end(), [](const Rec& x, const Rec& y) {
+    return std::max(x.v[7], x.v[8]) > std::max(y.v[7], y.v[8]);
+  });
   const int64_t need = static_cast<int64_t>(items.size()) * kItemInts;
   if (need > cap) return fail(PKV_VALUE_ERROR, "plan buffer too small (%lld < %lld)", static_cast<long long>(cap),
                               static_cast<long long>(need));

@@ -36,22 +36,27 @@ def test_plan_items_cover_every_query_once():
     rows = np.array([3, 0, 7, 1], dtype=np.int32)
     hq, hkv = 32, 8
     plan = _lib.prefill_plan(qs, ql, lens, rows, hq, hkv, causal=True)
+    assert plan.shape[1] == _lib.PREFILL_ITEM_INTS
     qt = 128 // (hq // hkv)
     cover = np.zeros((int(ql.sum()), hkv), dtype=np.int64)
-    for q_row0, cnt, pos0, kv_len, row, kvh, tiles, _ in plan:
-        assert 1 <= cnt <= qt
-        cover[q_row0:q_row0 + cnt, kvh] += 1
+    for q_row0, cnt_a, cnt_b, pos0, kv_len, row, kvh, tiles_a, tiles_b, _ in plan:
+        assert 1 <= cnt_a <= qt and 0 <= cnt_b <= qt and (cnt_b == 0 or cnt_a == qt)
         s = int(np.searchsorted(qs, q_row0, side="right") - 1)
         assert kv_len == lens[s] and row == rows[s]
         assert pos0 == lens[s] - ql[s] + (q_row0 - qs[s])
-        assert tiles == -(-min(pos0 + cnt, kv_len) // 128)
+        for t, (cnt, tiles) in enumerate(((cnt_a, tiles_a), (cnt_b, tiles_b))):
+            cover[q_row0 + t * qt:q_row0 + t * qt + cnt, kvh] += 1
+            want = -(-min(pos0 + t * qt + cnt, kv_len) // 128) if cnt else 0
+            assert tiles == want
     assert (cover == 1).all()
-    assert (np.diff(plan[:, 6]) <= 0).all()  # longest first
+    longest = np.maximum(plan[:, 7], plan[:, 8])
+    assert (np.diff(longest) <= 0).all()  # longest first
 
 
 def test_plan_non_causal_visits_all_keys_and_validates():
     plan = _lib.prefill_plan([0], [10], [1000], [0], 8, 8, causal=False)
-    assert plan.shape == (8, 8) and (plan[:, 6] == 8).all() and sorted(plan[:, 5]) == list(range(8))
+    assert plan.shape == (8, _lib.PREFILL_ITEM_INTS) and (plan[:, 7] == 8).all() and (plan[:, 8] == 0).all()
+    assert sorted(plan[:, 6]) == list(range(8))
     with pytest.raises(OutOfRange):
         _lib.prefill_plan([0], [20], [10], [0], 8, 8, causal=True)
 
