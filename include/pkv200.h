@@ -253,6 +253,7 @@ typedef struct pkv_prefill_args {
   int64_t n_items;
   void* prof_start;          /* optional cudaEvent_t pair around the launch */
   void* prof_stop;
+  void* debug;               /* optional device uint64[512]: timeline of CTA 0 (NULL = off) */
 } pkv_prefill_args;
 
 int pkv_prefill_supported(int32_t hq, int32_t hkv, int32_t head_dim, int32_t page_size,

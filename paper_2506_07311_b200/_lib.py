@@ -59,7 +59,7 @@ class PrefillArgs(C.Structure):
         ("cache_rows", _i64), ("block_table", _vp), ("bt_stride", _i64), ("page_size", _i32),
         ("hq", _i32), ("hkv", _i32), ("head_dim", _i32), ("scale", _f32), ("causal", _i32),
         ("out", _vp), ("out_dtype", _i32), ("plan", _vp), ("n_items", _i64),
-        ("prof_start", _vp), ("prof_stop", _vp),
+        ("prof_start", _vp), ("prof_stop", _vp), ("debug", _vp),
     ]
 
 

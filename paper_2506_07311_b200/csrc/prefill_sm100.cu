@@ -40,6 +40,7 @@
 #include <algorithm>
 #include <cstring>
 #include <numeric>
+#include <type_traits>
 #include <vector>
 
 #include "common.cuh"
@@ -157,7 +158,17 @@ struct PrefillParams {
   void* out;
   int out_dtype;
   const int32_t* items;
+  unsigned long long* dbg;  // debug timeline of CTA 0 (nullptr = off)
 };
+__device__ __forceinline__ unsigned long long gtime() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+#define PDBG(slot) \
+  do {             \
+    if (p.dbg && blockIdx.x == 0) p.dbg[slot] = gtime(); \
+  } while (0)
 
 template <typename T>
 struct Fmt;
@@ -311,6 +322,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         mbar_wait(bar(B_VF + st), (j >> 1) & 1);
         mbar_wait(bar(B_PF + t), j & 1);
         tc_fence_after();
+        if (j < 64) PDBG(256 + t * 64 + j);
 #pragma unroll
         for (int k = 0; k < kN / 16; ++k) {
           // A = P_t in TMEM (16 keys = 8 packed columns per step), B = V (MN-major)
@@ -325,6 +337,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (j < n_tiles) {
           mbar_wait(bar(B_KF + st), (j >> 1) & 1);
           tc_fence_after();
+          if (j < 64) PDBG(384 + j);
         }
         for (int t = 0; t < 2; ++t) {
           if (j > 0 && j - 1 < nt[t]) issue_pv(t, j - 1);
@@ -350,21 +363,31 @@ __global__ void __launch_bounds__(kThreads, 1)
     for (int j = 0; j < nt[t]; ++j) {
       mbar_wait(bar(B_SF + t), j & 1);
       tc_fence_after();
+      if (r == 0 && j < 64) PDBG(t * 64 + j);
       const int kbase = j * kN;
-      const bool masked = kbase + kN > nk;
-      // pass 1: row max (S read from TMEM in 32-column chunks)
-      float mx = -INFINITY;
+      // diagonal / tail tiles take the masked code path (warp-uniform branch)
+      const bool masked = __any_sync(0xffffffffu, kbase + kN > nk);
+      // pass 1: row max (S read from TMEM, two 32-column chunks in flight;
+      // four independent max chains)
+      float mx4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
+      auto pass1 = [&](auto mask_tag) {
+        constexpr bool kMask = decltype(mask_tag)::value;
 #pragma unroll 1
-      for (int c = 0; c < kN / 32; ++c) {
-        uint32_t v[32];
-        tmem_ld32(tS + c * 32, v);
-        tmem_wait_ld();
+        for (int c = 0; c < kN / 32; c += 2) {
+          uint32_t v[64];
+          tmem_ld32(tS + c * 32, v);
+          tmem_ld32(tS + c * 32 + 32, v + 32);
+          tmem_wait_ld();
+          const int lim = nk - (kbase + c * 32);  // element e is allowed iff e < lim
 #pragma unroll
-        for (int e = 0; e < 32; ++e) {
-          const float x = (masked && kbase + c * 32 + e >= nk) ? -INFINITY : __uint_as_float(v[e]);
-          mx = fmaxf(mx, x);
+          for (int e = 0; e < 64; ++e) {
+            const float x = (kMask && e >= lim) ? -INFINITY : __uint_as_float(v[e]);
+            mx4[e & 3] = fmaxf(mx4[e & 3], x);
+          }
         }
-      }
+      };
+      if (masked) pass1(std::true_type{}); else pass1(std::false_type{});
+      float mx = fmaxf(fmaxf(mx4[0], mx4[1]), fmaxf(mx4[2], mx4[3]));
       mx *= p.qscale;
       float factor = 1.f;
       const bool need = mx > m_used + kRescaleThreshold;
@@ -387,30 +410,39 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       // pass 2: P = 2^(s*qscale - m) rounded to 16 bits, written over S
       const float2 negm2 = make_float2(-m_used, -m_used);
-      float2 l2 = make_float2(0.f, 0.f);
+      float2 l2[4] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
+      auto pass2 = [&](auto mask_tag) {
+        constexpr bool kMask = decltype(mask_tag)::value;
 #pragma unroll 1
-      for (int c = 0; c < kN / 32; ++c) {
-        uint32_t v[32], pk[16];
-        tmem_ld32(tS + c * 32, v);
-        tmem_wait_ld();
+        for (int c = 0; c < kN / 32; ++c) {
+          uint32_t v[32], pk[16];
+          tmem_ld32(tS + c * 32, v);
+          tmem_wait_ld();
+          const int lim = nk - (kbase + c * 32);
 #pragma unroll
-        for (int e = 0; e < 32; e += 2) {
-          float2 x = make_float2(__uint_as_float(v[e]), __uint_as_float(v[e + 1]));
-          if (masked) {
-            if (kbase + c * 32 + e >= nk) x.x = -INFINITY;
-            if (kbase + c * 32 + e + 1 >= nk) x.y = -INFINITY;
+          for (int e = 0; e < 32; e += 2) {
+            float2 x = make_float2(__uint_as_float(v[e]), __uint_as_float(v[e + 1]));
+            if (kMask) {
+              if (e >= lim) x.x = -INFINITY;
+              if (e + 1 >= lim) x.y = -INFINITY;
+            }
+            const float2 tt = ffma2(x, qs2, negm2);
+            const float2 pp = make_float2(ex2_ftz(tt.x), ex2_ftz(tt.y));
+            l2[(e >> 1) & 3] = fadd2(l2[(e >> 1) & 3], pp);
+            pk[e >> 1] = pack2<T>(pp.x, pp.y);
           }
-          const float2 tt = ffma2(x, qs2, negm2);
-          const float2 pp = make_float2(ex2_ftz(tt.x), ex2_ftz(tt.y));
-          l2 = fadd2(l2, pp);
-          pk[e >> 1] = pack2<T>(pp.x, pp.y);
+          tmem_st16(tS + c * 16, pk);
         }
-        tmem_st16(tS + c * 16, pk);
+      };
+      if (masked) pass2(std::true_type{}); else pass2(std::false_type{});
+      {
+        const float2 a = fadd2(fadd2(l2[0], l2[1]), fadd2(l2[2], l2[3]));
+        l += a.x + a.y;
       }
-      l += l2.x + l2.y;
       tmem_wait_st();
       tc_fence_before();
       mbar_arrive(bar(B_PF + t));
+      if (r == 0 && j < 64) PDBG(128 + t * 64 + j);
     }
     // epilogue: O / l for the valid rows
     if (nt[t] > 0) {
@@ -634,6 +666,7 @@ extern "C" int pkv_paged_prefill(const pkv_prefill_args* a, void* stream_) {
   pp.out = a->out;
   pp.out_dtype = a->out_dtype;
   pp.items = a->plan;
+  pp.dbg = static_cast<unsigned long long*>(a->debug);
   cudaStream_t stream = static_cast<cudaStream_t>(stream_);
   if (a->prof_start) cudaEventRecord(static_cast<cudaEvent_t>(a->prof_start), stream);
   int st;

@@ -59,6 +59,19 @@ def main():
                              scale=cfg.scale, causal=1, out=out.data_ptr(), out_dtype=_lib.PKV_F32,
                              plan=dplan.data_ptr(), n_items=plan.shape[0])
         sp = _stream(dev)
+        if os.environ.get("PF_DEBUG"):
+            dbg = torch.zeros(512, dtype=torch.int64, device=dev)
+            a.debug = dbg.data_ptr()
+            _lib.check(lib.pkv_paged_prefill(C.byref(a), sp))
+            torch.cuda.synchronize()
+            t = dbg.cpu().numpy().astype(np.float64)
+            t0 = t[t > 0].min()
+            rel = np.where(t > 0, (t - t0) / 1e3, np.nan)
+            print("item 0:", plan[0].tolist())
+            for name, off in (("S_A ready", 0), ("S_B ready", 64), ("P_A done", 128), ("P_B done", 192),
+                              ("PV_A issue", 256), ("PV_B issue", 320), ("K ready", 384)):
+                print("%-10s" % name, " ".join("%6.2f" % x for x in rel[off:off + 24]))
+            a.debug = None
         for _ in range(3):
             _lib.check(lib.pkv_paged_prefill(C.byref(a), sp))
         torch.cuda.synchronize()
