@@ -14,7 +14,8 @@ import os
 from . import errors
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libpkv200.so")
+# PKV200_LIB overrides the library (kernel-variant experiments); default in-tree
+LIB_PATH = os.environ.get("PKV200_LIB") or os.path.join(_HERE, "libpkv200.so")
 
 PKV_F32, PKV_F16, PKV_BF16 = 0, 1, 2
 PREFILL_ITEM_INTS = 10  # {q_row0, cnt_a, cnt_b, qpos0, kv_len, row, kv_head, tiles_a, tiles_b, 0}

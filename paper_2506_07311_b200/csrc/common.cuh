@@ -219,31 +219,6 @@ __device__ __forceinline__ float2 fadd2(float2 a, float2 b) {
   return d;
 }
 
-// 2^x for two lanes on the FMA pipe (offloads the SFU in softmax): x is
-// clamped to >= -127, split as 2^floor(x) * 2^f with a degree-3 minimax
-// polynomial for 2^f on [0, 1) (max rel. error 8.6e-5, far below the 16-bit
-// rounding P goes through).  floor comes from a round-down add of 1.5*2^23,
-// whose low mantissa bits, shifted into the exponent field, are floor(x)
-// (the magic number's own bits vanish in the shift).
-__device__ __forceinline__ float2 exp2_poly2(float2 x) {
-  x.x = fmaxf(x.x, -127.f);
-  x.y = fmaxf(x.y, -127.f);
-  const float kMagic = 12582912.f;
-  float2 t;
-  asm("{\n .reg .b64 ra, rb, rd;\n mov.b64 ra, {%2, %3};\n mov.b64 rb, {%4, %4};\n"
-      " add.rm.f32x2 rd, ra, rb;\n mov.b64 {%0, %1}, rd;\n}\n"
-      : "=f"(t.x), "=f"(t.y)
-      : "f"(x.x), "f"(x.y), "f"(kMagic));
-  const float2 xi = fadd2(t, make_float2(-kMagic, -kMagic));      // floor(x), exact
-  const float2 f = ffma2(xi, make_float2(-1.f, -1.f), x);           // x - floor(x) in [0, 1)
-  float2 p = ffma2(f, make_float2(0.07705726579616763f, 0.07705726579616763f),
-                   make_float2(0.22765566734602127f, 0.22765566734602127f));
-  p = ffma2(f, p, make_float2(0.6951144126262895f, 0.6951144126262895f));
-  p = ffma2(f, p, make_float2(1.f, 1.f));
-  return make_float2(__uint_as_float(__float_as_uint(p.x) + (__float_as_uint(t.x) << 23)),
-                     __uint_as_float(__float_as_uint(p.y) + (__float_as_uint(t.y) << 23)));
-}
-
 // wrapping increment with acquire-release semantics at GPU scope
 __device__ __forceinline__ unsigned atom_inc_acq_rel(unsigned* addr, unsigned wrap) {
   unsigned old;
