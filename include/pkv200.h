@@ -206,6 +206,12 @@ typedef struct pkv_attention_args {
    * host copy (read by the launcher) and an identical device copy */
   const int32_t* plan;
   const int32_t* plan_host;
+  /* optional: copy meta_bytes from pinned meta_host to meta_dev on the stream
+   * before the launch (the packed [q_seq | nkeys | rows | plan] block the
+   * device pointers above point into) */
+  const void* meta_host;
+  void* meta_dev;
+  int64_t meta_bytes;
 } pkv_attention_args;
 
 /* Host planner of the tensor-core decode (a serving scheduler's job: the
@@ -219,6 +225,18 @@ int64_t pkv_attention_plan_ints(int64_t n_queries, int32_t hq);
 int pkv_attention_plan(const int32_t* q_nkeys, const int32_t* q_row, int64_t n_queries,
                        int32_t page_size, int32_t hq, int32_t hkv, int32_t num_sms,
                        int32_t target_waves, int32_t* plan_out, int64_t cap, int64_t* n_out);
+
+/* One decode step's host work for n sequences of a pool — the batched form of
+ * DecodeSession.step (decoder.py:263-284): pkv_pool_prepare_append (grow,
+ * copy-on-write, logical_len += 1), then the packed metadata
+ * [q_seq | nkeys | rows | plan] written into meta (pinned host memory,
+ * meta_cap int32; *meta_used receives the count).  The caller clears the
+ * granted pages / performs the reported copies in every store, uploads the
+ * metadata (or passes it as meta_host to pkv_paged_attention) and launches. */
+int pkv_decode_step_prepare(pkv_pool* pool, const int64_t* seqs, int64_t n, int32_t page_size,
+                            int32_t hq, int32_t hkv, int32_t* meta, int64_t meta_cap,
+                            int64_t* meta_used, uint32_t* pages_out, int64_t pages_cap,
+                            int64_t* n_pages_out, int64_t* copies_out);
 
 /* Workspace bound: the split planner never creates more than
  * n_queries + 8192 key splits, so the bound depends only on the query count. */

@@ -51,6 +51,7 @@ class AttentionArgs(C.Structure):
         ("prof_start", _vp), ("prof_stop", _vp),
         ("mode", _i32), ("k_new", _vp), ("v_new", _vp),
         ("plan", _vp), ("plan_host", _vp),
+        ("meta_host", _vp), ("meta_dev", _vp), ("meta_bytes", _i64),
     ]
 
 
@@ -99,6 +100,8 @@ SIGNATURES = {
     "pkv_page_copy": (C.c_int, [_vp, _vp, _vp, _i64, _i64, _i32, _vp]),
     "pkv_kv_append": (C.c_int, [_vp, _vp, _i64, _vp, _i32, _vp, _vp, _i64, _i32, _vp, _vp, _i64, _vp]),
     "pkv_attention_workspace_bytes": (_i64, [_i64, _i32, _i32]),
+    "pkv_decode_step_prepare": (C.c_int, [_vp, _vp, _i64, _i32, _i32, _i32, _vp, _i64, _P(_i64), _vp, _i64,
+                                          _P(_i64), _vp]),
     "pkv_attention_plan_ints": (_i64, [_i64, _i32]),
     "pkv_attention_plan": (C.c_int, [_vp, _vp, _i64, _i32, _i32, _i32, _i32, _i32, _vp, _i64, _P(_i64)]),
     "pkv_paged_attention": (C.c_int, [_P(AttentionArgs), _vp]),

@@ -43,8 +43,6 @@ class DecodeBatch:
         self.seq_ids = list(seq_ids)
         self.handles = np.asarray([self.pool.table(s)._handle for s in self.seq_ids], dtype=np.int64)
         self.n = len(self.seq_ids)
-        self._pos = np.empty(self.n, dtype=np.int32)
-        self._rows = np.empty(self.n, dtype=np.int32)
         self._copies = np.empty(2 * self.n, dtype=np.int64)
         self._pages = np.empty(2 * self.n + 1, dtype=np.uint32)
         self._plan_len = int(_lib.load().pkv_attention_plan_ints(self.n, config.head_count))
@@ -54,20 +52,20 @@ class DecodeBatch:
         self._ring = []
         for _ in range(4):
             host = torch.empty(width, dtype=torch.int32).pin_memory()
-            host[: self.n] = torch.arange(self.n, dtype=torch.int32)
             dev = torch.empty(width, dtype=torch.int32, device=self.device)
             self._ring.append((host, dev, torch.cuda.Event()))
         self._slot = 0
-        self._ring_np = [h.numpy() for h, _, _ in self._ring]
+        self._cur = None
+        self._uploaded = False
+        self._used = C.c_int64()
+        self._used_p = C.byref(self._used)
         self.last_launches = 0
-        i64p, i32p, u32p = C.POINTER(C.c_int64), C.POINTER(C.c_int32), C.POINTER(C.c_uint32)
+        i64p, u32p = C.POINTER(C.c_int64), C.POINTER(C.c_uint32)
         self._handles_p = self.handles.ctypes.data_as(i64p)
-        self._pos_p = self._pos.ctypes.data_as(i32p)
-        self._rows_p = self._rows.ctypes.data_as(i32p)
         self._pages_p = self._pages.ctypes.data_as(u32p)
         self._copies_p = self._copies.ctypes.data_as(i64p)
         self._n_pages = C.c_int64()
-        self._plan_n = C.c_int64()
+        self._n_pages_p = C.byref(self._n_pages)
         self._lib = _lib.load()
         ws_bytes = self._lib.pkv_attention_workspace_bytes(self.n, config.head_count, config.head_dim)
         self._ws = _Workspace.get(self.device, ws_bytes)
@@ -81,14 +79,27 @@ class DecodeBatch:
         self._args_p = C.byref(self._args)
 
     def prepare(self) -> int:
-        """Allocator work of one token step (host, one native call); returns
-        the number of page clear/copy launches it caused."""
-        n_pages = self._n_pages
-        _lib.call("pkv_pool_prepare_append", self.pool._h, self._handles_p, self.n, self._pos_p,
-                  self._rows_p, self._pages_p, self._pages.size, C.byref(n_pages), self._copies_p)
+        """Host work of one token step: one native call does the allocator
+        bookkeeping (grow, copy-on-write, logical_len) and writes the packed
+        metadata [q_seq | nkeys | rows | plan] into a pinned staging slot.
+        Returns the number of page clear/copy launches it caused."""
+        slot = self._slot
+        self._slot = (slot + 1) % len(self._ring)
+        host, dev, done = self._ring[slot]
+        done.synchronize()  # the previous upload from this slot has landed
+        cfg = self.config
+        st = self._lib.pkv_decode_step_prepare(
+            self.pool._h, self._handles_p, self.n, self.pool.page_size, cfg.head_count, cfg.kv_head_count,
+            host.data_ptr(), host.numel(), self._used_p, self._pages_p, self._pages.size, self._n_pages_p,
+            self._copies_p)
+        if st:
+            _lib.check(st, "pkv_decode_step_prepare")
+        self._cur = slot
+        self._uploaded = False
         launches = 0
-        if n_pages.value:
-            self.pool._clear_pages(self._pages[: n_pages.value].tolist())
+        n_pages = self._n_pages.value
+        if n_pages:
+            self.pool._clear_pages(self._pages[:n_pages].tolist())
             launches += len(self.pool._stores)
         dst = self._copies[1::2]
         if (dst >= 0).any():
@@ -106,24 +117,12 @@ class DecodeBatch:
         import torch
 
         launches = self.prepare() if advance else 0
+        if self._cur is None:
+            raise ValueError("call prepare() before step(advance=False)")
         store: KvStore = self.stores[layer]
         cfg = self.config
         n = self.n
-        host, dev, done = self._ring[self._slot]
-        mh = self._ring_np[self._slot]
-        self._slot = (self._slot + 1) % len(self._ring)
-        done.synchronize()  # the previous upload from this buffer has landed
-        np.add(self._pos, 1, out=mh[n:2 * n])  # keys attended: the whole context
-        mh[2 * n:3 * n] = self._rows
-        # host work plan written straight into the pinned staging buffer
-        got = self._plan_n
-        _lib.check(self._lib.pkv_attention_plan(mh[n:].ctypes.data, mh[2 * n:].ctypes.data, n,
-                                                store.page_size, cfg.head_count, cfg.kv_head_count, 0, 0,
-                                                host.data_ptr() + 12 * n, self._plan_len, C.byref(got)),
-                   "pkv_attention_plan")
-        used = 3 * n + got.value
-        dev[:used].copy_(host[:used], non_blocking=True)
-        done.record()
+        host, dev, done = self._ring[self._cur]
         mirror = self.pool.device_table(self.device)  # applies any pending table edits
         k = k_new if isinstance(k_new, torch.Tensor) else torch.from_numpy(np.ascontiguousarray(k_new))
         v = v_new if isinstance(v_new, torch.Tensor) else torch.from_numpy(np.ascontiguousarray(v_new))
@@ -139,6 +138,7 @@ class DecodeBatch:
         out_t, out_code = torch_dtype(out_dtype or torch.float32)
         out = torch.empty((n, cfg.head_count, cfg.head_dim), dtype=out_t, device=self.device)
         md = dev.data_ptr()
+        hp = host.data_ptr()
         a = self._args
         a.q, a.q_dtype = q.data_ptr(), qcode
         a.q_seq, a.q_nkeys, a.seq_row = md, md + 4 * n, md + 8 * n
@@ -149,12 +149,19 @@ class DecodeBatch:
         a.workspace, a.workspace_bytes = self._ws.data_ptr(), self._ws.numel()
         a.mode = PRECISION_MODES[precision]
         a.k_new, a.v_new = k.data_ptr(), v.data_ptr()
-        a.plan, a.plan_host = md + 12 * n, host.data_ptr() + 12 * n
+        a.plan, a.plan_host = md + 12 * n, hp + 12 * n
+        # the first layer of a token uploads the packed metadata on the stream
+        a.meta_host = None if self._uploaded else hp
+        a.meta_dev = md
+        a.meta_bytes = 4 * self._used.value
         # K1 append is fused into the decode launch (the last split of every
         # sequence reads the new token from k/v and writes it into its page)
         st = self._lib.pkv_paged_attention(self._args_p, _stream(self.device))
         if st:
             _lib.check(st, "pkv_paged_attention")
+        if not self._uploaded:
+            done.record()
+            self._uploaded = True
         tensor = (store.dtype_code == _lib.PKV_BF16 and precision != "exact") or precision == "tensor"
         # tensor-core path: one launch (append fused, split merge in-kernel)
         self.last_launches = launches + (1 if tensor else 4)

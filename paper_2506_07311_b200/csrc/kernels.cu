@@ -637,9 +637,41 @@ int64_t pkv_attention_workspace_bytes(int64_t n_queries, int32_t hq, int32_t hea
   return up(plan) + up(4 * splits * hq * 2) + up(4 * splits * hq * head_dim);
 }
 
+int pkv_decode_step_prepare(pkv_pool* pool, const int64_t* seqs, int64_t n, int32_t page_size,
+                            int32_t hq, int32_t hkv, int32_t* meta, int64_t meta_cap,
+                            int64_t* meta_used, uint32_t* pages_out, int64_t pages_cap,
+                            int64_t* n_pages_out, int64_t* copies_out) {
+  if (n <= 0) return pkv::fail(PKV_VALUE_ERROR, "no sequences");
+  if (meta_cap < 3 * n + pkv_attention_plan_ints(n, hq))
+    return pkv::fail(PKV_VALUE_ERROR, "metadata buffer too small");
+  int32_t* q_seq = meta;
+  int32_t* nkeys = meta + n;
+  int32_t* rows = meta + 2 * n;
+  // positions land in nkeys[] and become key counts (the appended token is attended)
+  int st = pkv_pool_prepare_append(pool, seqs, n, nkeys, rows, pages_out, pages_cap, n_pages_out,
+                                   copies_out);
+  if (st) return st;
+  for (int64_t i = 0; i < n; ++i) {
+    q_seq[i] = static_cast<int32_t>(i);
+    nkeys[i] += 1;
+  }
+  int64_t used = 0;
+  st = pkv_attention_plan(nkeys, rows, n, page_size, hq, hkv, 0, 0, meta + 3 * n,
+                          meta_cap - 3 * n, &used);
+  if (st) return st;
+  *meta_used = 3 * n + used;
+  return PKV_OK;
+}
+
 int pkv_paged_attention(const pkv_attention_args* a, void* stream_) {
   if (!a) return pkv::fail(PKV_VALUE_ERROR, "null args");
   cudaStream_t stream = static_cast<cudaStream_t>(stream_);
+  if (a->meta_host && a->meta_bytes > 0) {  // stage the packed metadata (pinned host -> device)
+    if (!a->meta_dev) return pkv::fail(PKV_VALUE_ERROR, "meta_host without meta_dev");
+    cudaError_t e = cudaMemcpyAsync(a->meta_dev, a->meta_host, static_cast<size_t>(a->meta_bytes),
+                                    cudaMemcpyHostToDevice, stream);
+    if (e != cudaSuccess) return pkv::fail(PKV_CUDA_ERROR, "metadata upload: %s", cudaGetErrorString(e));
+  }
   if (a->n_queries <= 0) return PKV_OK;
   if (a->hq <= 0 || a->hkv <= 0 || a->hq % a->hkv)
     return pkv::fail(PKV_SHAPE_MISMATCH, "query heads (%d) must be a multiple of kv heads (%d)",

@@ -366,10 +366,16 @@ int pkv_pool_prepare_append(pkv_pool* pool, const int64_t* seqs, int64_t n, int3
     Table* t = pool->find(seqs[i]);
     if (!t) return pkv::fail(PKV_UNKNOWN_SEQUENCE, "no block table for sequence %lld",
                              static_cast<long long>(seqs[i]));
-    for (int64_t j = 0; j < i; ++j)
-      if (tabs[j] == t) return pkv::fail(PKV_VALUE_ERROR, "sequence %lld listed twice",
-                                         static_cast<long long>(seqs[i]));
     tabs[i] = t;
+  }
+  {  // a sequence may appear once per step (O(n log n) check)
+    std::vector<Table*> sorted(tabs);
+    std::sort(sorted.begin(), sorted.end());
+    if (std::adjacent_find(sorted.begin(), sorted.end()) != sorted.end())
+      return pkv::fail(PKV_VALUE_ERROR, "a sequence is listed twice in one decode step");
+  }
+  for (int64_t i = 0; i < n; ++i) {
+    Table* t = tabs[i];
     const int64_t pos = t->logical_len;
     if (pos < 0 || pos >= (int64_t(1) << 31) - 1)
       return pkv::fail(PKV_OUT_OF_RANGE, "position %lld not addressable", static_cast<long long>(pos));
