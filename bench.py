@@ -56,6 +56,7 @@ def parse():
     ap.add_argument("--sweep", action="store_true", help="also print a C3 context sweep (stderr)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-prefill", action="store_true", help="skip the C4 prefill (K3) side measurement")
     ap.add_argument("--waves", type=int, default=0, help="split planner target waves (0 = default)")
     ap.add_argument("--heads", default="", help="experiment: override query:kv heads, e.g. 32:32")
     return ap.parse_args()
@@ -539,6 +540,8 @@ def main():
                            "h2d_bytes_per_step": e["h2d_bytes_per_step"],
                            "d2h_bytes_per_step": e["d2h_bytes_per_step"],
                            "ms_per_step": e["ms_per_step"], "tokens_per_s": e["tokens_per_s"]}
+        if world == 1 and not args.no_prefill:
+            line["prefill_c4"] = prefill_c4(device)
         if world == 1 and not args.no_cpu_baseline:
             name, lengths, hq, hkv, d, ps = workload(args, 0, 1)
             cb = cpu_sample(args, lengths, hq, hkv, d, ps)
@@ -550,6 +553,75 @@ def main():
     if world > 1:
         dist.barrier()
         dist.destroy_process_group()
+
+
+def prefill_c4(device, n=8192):
+    """Side measurement of BASELINE.json configs[3] (C4): one 8192-token
+    Llama-3-8B GQA prompt appended into the paged cache (K1) and attended
+    causally by the K3 tcgen05 prefill kernel.  TFLOP/s under the reference
+    FLOP convention 4*Hq*D*n(n+1)/2 (attention.py:224-226), CUDA events."""
+    import torch
+
+    from paper_2506_07311_b200 import AttentionConfig, KvStore, MaskMeta, PagePool, paged_attention
+
+    hq, hkv, d, ps = 32, 8, 128, 16
+    pool = PagePool(n // ps + 8, page_size=ps)
+    store = KvStore(pool, hkv, d, dtype=torch.bfloat16, device=device)
+    pool.reserve(0, n)
+    g = torch.Generator(device=device).manual_seed(4)
+    k = torch.randn((n, hkv, d), generator=g, device=device).bfloat16()
+    v = torch.randn((n, hkv, d), generator=g, device=device).bfloat16()
+    q = torch.randn((n, hq, d), generator=g, device=device).bfloat16()
+    cfg = AttentionConfig(head_count=hq, head_dim=d, page_size=ps, kv_head_count=hkv)
+    pos = np.arange(n)
+    store.assign(0, pos, k, v)
+    meta = MaskMeta.self_attention(store.batch_view([0]))
+    from paper_2506_07311_b200.attention import _launch_prefill, suffix_runs
+
+    runs = suffix_runs(meta)
+    rows = np.asarray([pool.table(0).mirror_row], dtype=np.int32)
+    mirror = pool.device_table(device)
+
+    def kernel_only(ev):
+        return _launch_prefill(q, meta, cfg, runs, k=store.keys, v=store.values, kv_code=store.dtype_code,
+                               bt=mirror, rows=rows, out_dtype=torch.float32, device=device,
+                               prof=(ev[0].cuda_event, ev[1].cuda_event) if ev else None)
+
+    for _ in range(3):
+        paged_attention(q, store, meta, cfg, precision="prefill")
+        kernel_only(None)
+    torch.cuda.synchronize(device)
+    times, app, kern = [], [], []
+    for _ in range(10):
+        e0, e1, e2 = (torch.cuda.Event(enable_timing=True) for _ in range(3))
+        e0.record()
+        store.assign(0, pos, k, v)  # K1 over the whole prompt (host validation included)
+        e1.record()
+        paged_attention(q, store, meta, cfg, precision="prefill")
+        e2.record()
+        ev = (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+        for x in ev:
+            x.record()  # materialise the cudaEvent_t handles
+        kernel_only(ev)
+        torch.cuda.synchronize(device)
+        app.append(e0.elapsed_time(e1))
+        times.append(e1.elapsed_time(e2))
+        kern.append(ev[0].elapsed_time(ev[1]))
+    ms = sorted(times)[len(times) // 2]
+    kms = sorted(kern)[len(kern) // 2]
+    flops = 4 * hq * d * n * (n + 1) // 2
+    tf = flops / (kms * 1e-3) / 1e12
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            sustained = float(json.load(f)["bf16_tflops_sustained"])
+    except Exception:
+        sustained = 1400.0
+    return {"workload": f"C4 causal prefill, 1 x {n} tokens, GQA 32q/8kv x128 bf16, page 16",
+            "kernel": "prefill_tc_kernel (K3, tcgen05/TMEM)", "kernel_ms": kms, "tflops": round(tf, 1),
+            "frac_of_sustained_bf16": round(tf / sustained, 3), "api_ms": ms,
+            "api_tflops": round(flops / (ms * 1e-3) / 1e12, 1), "append_ms": min(app),
+            "note": "kernel_ms: CUDA events around the K3 launch; api_ms: the whole paged_attention() call "
+                    "(host planning + metadata upload + launch); FLOPs per the reference convention"}
 
 
 def sweep(device):

@@ -83,6 +83,12 @@ int pkv_pool_fork(pkv_pool* pool, int64_t parent, int64_t child, int64_t prefix_
  * was already private; otherwise copy the full page old -> new */
 int pkv_pool_privatize(pkv_pool* pool, int64_t seq, int64_t block_idx, int64_t* old_page,
                        int64_t* new_page);
+/* KvStore.assign's copy-on-write loop (store.py:143-145): privatize the
+ * given blocks in order, stopping at the first failure (earlier blocks stay
+ * privatized, as with the reference's per-block loop); copies_out[2n]
+ * receives the (old, new) page pairs the caller must copy in every store */
+int pkv_pool_privatize_blocks(pkv_pool* pool, int64_t seq, const int64_t* blocks, int64_t n,
+                              int64_t* copies_out, int64_t* n_copies_out);
 /* PagePool.translate           pool.py:258-266 */
 int pkv_pool_translate(pkv_pool* pool, int64_t seq, int64_t position, uint32_t* page_out,
                        uint32_t* offset_out);

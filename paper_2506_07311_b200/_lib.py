@@ -76,6 +76,7 @@ SIGNATURES = {
     "pkv_pool_free": (C.c_int, [_vp, _i64, _P(_i64)]),
     "pkv_pool_fork": (C.c_int, [_vp, _i64, _i64, _i64, _P(_i64), _P(_i64), _P(_i64)]),
     "pkv_pool_privatize": (C.c_int, [_vp, _i64, _i64, _P(_i64), _P(_i64)]),
+    "pkv_pool_privatize_blocks": (C.c_int, [_vp, _i64, _vp, _i64, _vp, _P(_i64)]),
     "pkv_pool_prepare_append": (C.c_int, [_vp, _P(_i64), _i64, _P(_i32), _P(_i32), _P(_u32), _i64,
                                           _P(_i64), _P(_i64)]),
     "pkv_pool_translate": (C.c_int, [_vp, _i64, _i64, _P(_u32), _P(_u32)]),

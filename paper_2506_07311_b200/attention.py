@@ -29,7 +29,7 @@ import numpy as np
 
 from . import _lib
 from .errors import ConfigError, NoAllowedKeys, OutOfRange, ShapeMismatch
-from .store import BatchView, KvStore, _ptr, _stream, to_device, torch_dtype
+from .store import BatchView, KvStore, _ptr, _stream, stage_upload, to_device, torch_dtype
 
 
 class BlockKind(IntEnum):
@@ -264,7 +264,7 @@ def _launch_attention(q, qcode, meta, config, nkeys, *, k, v, kv_code, bt, bt_st
     nseq = seq_part.size
     # 2*nq int32 precede seq_part, so an int64 seq_start stays 8-byte aligned
     host = np.concatenate([q_seq, nkeys.astype(np.int32), seq_part, plan])
-    dev = torch.from_numpy(host).to(device)
+    dev = stage_upload(device, host)
     base = dev.data_ptr()
     seq_ptr = base + 4 * (2 * nq)
     plan_ptr = seq_ptr + 4 * nseq
@@ -348,7 +348,7 @@ def _launch_prefill(q, meta, config, runs, *, k, v, kv_code, bt, rows, out_dtype
         raise OutOfRange("K/V rows beyond 2^31 are not addressable")
     plan = _lib.prefill_plan(q_start, q_len, meta.view.lengths, rows, config.head_count,
                              config.kv_head_count, config.causal)
-    dev_plan = torch.from_numpy(plan).to(device)
+    dev_plan = stage_upload(device, plan.reshape(-1))
     args = _lib.PrefillArgs(
         q=q.data_ptr(), total_q=nq, k_cache=k.data_ptr(), v_cache=v.data_ptr(),
         kv_dtype=kv_code, cache_rows=k.shape[0], block_table=bt.data_ptr() if bt is not None else None,

@@ -353,6 +353,22 @@ int pkv_pool_privatize(pkv_pool* pool, int64_t seq, int64_t block_idx, int64_t* 
   return pool->release(std::vector<uint32_t>{old}, &dummy);
 }
 
+int pkv_pool_privatize_blocks(pkv_pool* pool, int64_t seq, const int64_t* blocks, int64_t n,
+                              int64_t* copies_out, int64_t* n_copies_out) {
+  *n_copies_out = 0;
+  for (int64_t i = 0; i < n; ++i) {
+    int64_t old = -1, fresh = -1;
+    const int st = pkv_pool_privatize(pool, seq, blocks[i], &old, &fresh);
+    if (st) return st;  // earlier blocks stay privatized, as with the reference's loop
+    if (fresh >= 0) {
+      copies_out[2 * *n_copies_out] = old;
+      copies_out[2 * *n_copies_out + 1] = fresh;
+      ++*n_copies_out;
+    }
+  }
+  return PKV_OK;
+}
+
 int pkv_pool_prepare_append(pkv_pool* pool, const int64_t* seqs, int64_t n, int32_t* positions_out,
                             int32_t* rows_out, uint32_t* pages_out, int64_t pages_cap,
                             int64_t* n_pages_out, int64_t* copies_out) {

@@ -264,6 +264,20 @@ class PagePool:
         self._copy_rows(old.value, new.value, self.page_size)
         return new.value
 
+    def privatize_blocks(self, seq_id, blocks: np.ndarray) -> int:
+        """store.py:143-145: privatize `blocks` (ascending) in one native call;
+        performs the page copies and returns how many there were."""
+        h = self._handle_or_ghost(seq_id)
+        blocks = np.ascontiguousarray(blocks, dtype=np.int64)
+        copies = np.empty(2 * max(blocks.size, 1), dtype=np.int64)
+        n = C.c_int64()
+        st = _lib.load().pkv_pool_privatize_blocks(self._h, h, blocks.ctypes.data, blocks.size,
+                                                     copies.ctypes.data, C.byref(n))
+        for i in range(n.value):  # copies of the blocks privatized before any failure
+            self._copy_rows(int(copies[2 * i]), int(copies[2 * i + 1]), self.page_size)
+        _lib.check(st, "pkv_pool_privatize_blocks")
+        return n.value
+
     # -- addressing --------------------------------------------------------------
     def translate(self, seq_id, position: int) -> PageAddress:
         h = self._handle_or_ghost(seq_id)
