@@ -1,6 +1,8 @@
 """Pin the CPU oracle (oracle/) to the real reference: golden vectors always,
 the live reference when it is mounted (build container only)."""
 
+import os
+
 import numpy as np
 import pytest
 
@@ -15,6 +17,8 @@ from oracle.attention import (
 from oracle.workloads import config_lengths, lpt_partition, scattered_instance
 
 from replay import replay_pool_script, replay_store_script
+
+GOLDEN_DIR = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
 
 
 def _oracle_pool(c, p):
@@ -186,3 +190,19 @@ def test_product_workloads_and_sharder_match_oracle():
     for n in (1, 2, 4, 8):
         assert lpt_partition(c5, n) == o_lpt(c5, n)
         assert shard_balance(c5, lpt_partition(c5, n)) < 1.001
+
+
+def test_toy_decoder_restatement_matches_reference_golden():
+    """The test-side toy model (tests/toy_decoder.py) reproduces the real
+    reference's no-cache logits, so it can drive DecodeSession on the GPU."""
+    from toy_decoder import ToyDecoder, load_cases
+
+    for case in load_cases(os.path.join(GOLDEN_DIR, "decoder_cases.npz")):
+        dec = ToyDecoder(case["config"])
+        toks = [int(t) for t in case["tokens"]]
+        for i, want in enumerate(case["nocache"]):
+            got = dec.forward_nocache(toks[: case["n_prompt"] + 10 * i])
+            assert relative_error(got, want) <= 1e-5, case["name"]
+        # greedy decode of the golden cached run is self-consistent
+        assert all(int(np.argmax(case["logits"][i])) == toks[case["n_prompt"] + i]
+                   for i in range(case["steps"]))
