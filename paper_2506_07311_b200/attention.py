@@ -442,3 +442,81 @@ def gathered_attention(queries, keys, values, meta: MaskMeta, config: AttentionC
                              bt_stride=0, seq_row=None, seq_start=seq_start,
                              out_dtype=out_dtype or torch.float32, device=device,
                              precision=precision)
+
+
+# ---------------------------------------------------------------------------
+# Dense float64 diagnostics (reference attention.py:389-474).  Not the hot
+# path: plain torch math on the device, for API parity with the reference's
+# oracle / instrumented mode.  GQA is accepted (kv head h // G), an extension.
+# ---------------------------------------------------------------------------
+
+def reference_attention(queries, keys, values, lengths, *, causal: bool = True, scale=None, q_lengths=None,
+                        device=None):
+    """attention.py:389-447: two-pass masked softmax in float64 over
+    contiguous per-sequence K/V; the trailing q_lengths[s] positions of each
+    sequence are the queries.  Returns float64 rows (device tensor)."""
+    import torch
+
+    from .store import _device
+
+    # a diagnostic, not the hot path: device="cpu" is allowed
+    dev = torch.device(device) if device is not None else (
+        queries.device if isinstance(queries, torch.Tensor) and queries.is_cuda else _device(None))
+    q = torch.as_tensor(np.asarray(queries) if not isinstance(queries, torch.Tensor) else queries).to(dev, torch.float64)
+    k = torch.as_tensor(np.asarray(keys) if not isinstance(keys, torch.Tensor) else keys).to(dev, torch.float64)
+    v = torch.as_tensor(np.asarray(values) if not isinstance(values, torch.Tensor) else values).to(dev, torch.float64)
+    if q.ndim != 3 or k.shape != v.shape or k.ndim != 3:
+        raise ShapeMismatch("queries/keys/values must be (rows, heads, head_dim)")
+    if k.shape[2] != q.shape[2] or q.shape[1] % k.shape[1]:
+        raise ShapeMismatch("queries and keys disagree on head layout")
+    lengths = np.asarray(lengths, dtype=np.int64)
+    if lengths.sum() != k.shape[0]:
+        raise ShapeMismatch("lengths do not add up to the KV row count")
+    q_lengths = lengths.copy() if q_lengths is None else np.asarray(q_lengths, dtype=np.int64)
+    if q_lengths.shape != lengths.shape or (q_lengths < 0).any() or (q_lengths > lengths).any():
+        raise ShapeMismatch("q_lengths must give 0 <= q_len <= len per sequence")
+    if q.shape[0] != q_lengths.sum():
+        raise ShapeMismatch("query rows do not match q_lengths")
+    g = q.shape[1] // k.shape[1]
+    scale = 1.0 / math.sqrt(q.shape[2]) if scale is None else float(scale)
+    out = torch.empty_like(q)
+    ko = qo = 0
+    for n, ql in zip(lengths.tolist(), q_lengths.tolist()):
+        if ql:
+            kk = k[ko:ko + n].repeat_interleave(g, dim=1)
+            vv = v[ko:ko + n].repeat_interleave(g, dim=1)
+            s = torch.einsum("qhd,khd->hqk", q[qo:qo + ql], kk) * scale
+            if causal:
+                pos = torch.arange(n - ql, n, device=dev)
+                s = s.masked_fill(torch.arange(n, device=dev)[None, :] > pos[:, None], float("-inf"))
+            p = torch.softmax(s, dim=-1)
+            out[qo:qo + ql] = torch.einsum("hqk,khd->qhd", p, vv)
+        ko += n
+        qo += ql
+    return out
+
+
+def attention_weights(queries, store: KvStore, meta: MaskMeta, config: AttentionConfig):
+    """attention.py:450-474: the (n_queries, heads, kv_slots) float64 softmax
+    weights over the paged content of the view, exactly zero on disallowed
+    keys; raises NoAllowedKeys for a query without allowed keys."""
+    import torch
+
+    _check_queries(queries, meta, config)
+    keys, _ = store.gather_view(meta.view)
+    dev = keys.device
+    q = torch.as_tensor(np.asarray(queries) if not isinstance(queries, torch.Tensor) else queries).to(dev, torch.float64)
+    g = config.head_count // config.kv_head_count
+    k = keys.to(torch.float64).repeat_interleave(g, dim=1)
+    s = torch.einsum("qhd,khd->qhk", q, k) * config.scale
+    nk = allowed_key_counts(meta, config.causal)
+    lo = meta.view.prefix_sums[meta.q_seq]
+    slots = torch.arange(meta.view.total_slots, device=dev)
+    lo_t = torch.as_tensor(lo, device=dev)[:, None]
+    hi_t = lo_t + torch.as_tensor(nk, device=dev)[:, None]
+    allow = (slots[None, :] >= lo_t) & (slots[None, :] < hi_t)
+    if meta.query_count and (~allow.any(dim=1)).any():
+        raise NoAllowedKeys("a query row has zero allowed keys")
+    s = s.masked_fill(~allow[:, None, :], float("-inf"))
+    p = torch.softmax(s, dim=-1)
+    return torch.where(allow[:, None, :], p, torch.zeros((), dtype=p.dtype, device=dev))

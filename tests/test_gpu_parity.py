@@ -402,3 +402,27 @@ def test_out_of_range_view_length_rejected():
     meta = MaskMeta(view=view, q_seq=np.array([0]), q_pos=np.array([0]))
     with pytest.raises(OutOfRange):
         paged_attention(np.ones((1, 1, 4), np.float32), store, meta, cfg)
+
+
+def test_attention_weights_diagnostic():
+    """attention_weights (reference attention.py:450-474): rows sum to one over
+    allowed keys, disallowed keys carry exactly zero, weights @ V == paged_attention."""
+    import torch
+
+    from paper_2506_07311_b200 import attention_weights
+
+    rng = np.random.default_rng(5)
+    lengths = [37, 5, 80]
+    inst = scattered_instance(rng, lengths, kv_heads=2, q_heads=4, head_dim=32, page_size=16,
+                              q_lengths=[4, 5, 1], make_pool=lambda c, p: PagePool(c, p),
+                              make_store=lambda pool, h, d: KvStore(pool, h, d))
+    cfg = AttentionConfig(head_count=4, head_dim=32, page_size=16, kv_head_count=2)
+    meta = MaskMeta.suffix(inst.store.batch_view(inst.seq_ids), [4, 5, 1])
+    w = attention_weights(inst.queries, inst.store, meta, cfg)
+    assert torch.allclose(w.sum(-1), torch.ones_like(w.sum(-1)), atol=1e-12)
+    _, vals = inst.store.gather_view(meta.view)
+    o = torch.einsum("qhk,khd->qhd", w, vals.double().repeat_interleave(2, dim=1))
+    out = paged_attention(inst.queries, inst.store, meta, cfg)
+    assert relative_error(out.cpu().numpy(), o.cpu().numpy()) <= 1e-5
+    # a future key of query 0 (sequence 0, position 33) has zero weight
+    assert float(w[0, :, 34:37].abs().max()) == 0.0

@@ -206,3 +206,16 @@ def test_toy_decoder_restatement_matches_reference_golden():
         # greedy decode of the golden cached run is self-consistent
         assert all(int(np.argmax(case["logits"][i])) == toks[case["n_prompt"] + i]
                    for i in range(case["steps"]))
+
+
+def test_package_reference_attention_matches_golden_float64(golden_attention):
+    """The package's dense float64 diagnostic (reference attention.py:389-447)
+    reproduces the real reference's reference_attention outputs."""
+    from paper_2506_07311_b200 import reference_attention
+
+    index, arrays = golden_attention
+    for case in index:
+        inst = build_oracle_case(case)
+        got = reference_attention(inst.queries, inst.keys, inst.values, inst.lengths, causal=case["causal"],
+                                  scale=case["scale"], q_lengths=inst.q_lengths, device="cpu")
+        assert relative_error(got.numpy(), arrays[case["name"] + "_ref64"]) <= 1e-12, case["name"]
