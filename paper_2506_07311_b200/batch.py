@@ -101,11 +101,12 @@ class DecodeBatch:
         if n_pages:
             self.pool._clear_pages(self._pages[:n_pages].tolist())
             launches += len(self.pool._stores)
-        dst = self._copies[1::2]
-        if (dst >= 0).any():
-            for j in np.nonzero(dst >= 0)[0].tolist():
-                self.pool._copy_rows(int(self._copies[2 * j]), int(dst[j]), self.pool.page_size)
-                launches += len(self.pool._stores)
+        pairs = self._copies.reshape(-1, 2)
+        cow = pairs[:, 1] >= 0
+        if cow.any():  # copy-on-write pages: one batched K0b launch per store
+            sel = pairs[cow]
+            self.pool._copy_pages(np.column_stack([sel, np.full(len(sel), self.pool.page_size)]))
+            launches += len(self.pool._stores)
         return launches
 
     def step(self, queries, k_new, v_new, *, out_dtype=None, layer: int = 0, advance: bool = True,

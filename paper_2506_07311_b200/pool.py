@@ -178,6 +178,11 @@ class PagePool:
         for s in self._stores:
             s.copy_rows(src, dst, rows)
 
+    def _copy_pages(self, triples) -> None:
+        """Batched page copies (one K0b launch per attached store)."""
+        for s in self._stores:
+            s.copy_pages(triples)
+
     # -- handle mapping -------------------------------------------------------
     def _handle_or_ghost(self, seq_id) -> int:
         h = self._ids.get(seq_id)
@@ -273,8 +278,9 @@ class PagePool:
         n = C.c_int64()
         st = _lib.load().pkv_pool_privatize_blocks(self._h, h, blocks.ctypes.data, blocks.size,
                                                      copies.ctypes.data, C.byref(n))
-        for i in range(n.value):  # copies of the blocks privatized before any failure
-            self._copy_rows(int(copies[2 * i]), int(copies[2 * i + 1]), self.page_size)
+        if n.value:  # copies of the blocks privatized before any failure, one launch per store
+            pairs = copies[: 2 * n.value].reshape(-1, 2)
+            self._copy_pages(np.column_stack([pairs, np.full(n.value, self.page_size)]))
         _lib.check(st, "pkv_pool_privatize_blocks")
         return n.value
 
