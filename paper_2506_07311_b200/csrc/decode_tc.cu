@@ -39,6 +39,7 @@
 // reads the new token from the input and writes it into its page
 // (reshape-and-cache folded into the decode launch).
 #include <algorithm>
+#include <cstdlib>
 #include <functional>
 #include <numeric>
 #include <queue>
@@ -691,7 +692,11 @@ int plan_decode(const int32_t* nk, const int32_t* row, int64_t nq, int page_size
   // costs in pages of one unit; the per-item overhead (pipeline refill,
   // query load, partial store) is ~4 us ~ `ovh` pages of a CTA's stream
   const int64_t page_bytes = int64_t(hb) * ps * 128 * 2 * 2;  // K+V of the block (D ~ 128)
-  const int64_t ovh = std::max<int64_t>(1, (int64_t(200) << 10) / page_bytes) * (waves > 0 ? waves : 1);
+  static const int64_t ovh_kb = [] {  // per-item overhead in KB of stream (tuning knob)
+    const char* e = std::getenv("PKV_DECODE_ITEM_KB");
+    return e ? std::max<int64_t>(1, std::atoll(e)) : int64_t(400);  // measured optimum (C2, C3, C5)
+  }();
+  const int64_t ovh = std::max<int64_t>(1, (ovh_kb << 10) / page_bytes) * (waves > 0 ? waves : 1);
   const int64_t min_piece = std::max<int64_t>(ovh / 2, (2 * kCh * wph + ps - 1) / ps);
   const int64_t units = nq * head_items;
   const int64_t line = total_pages * head_items + ovh * units;
