@@ -156,3 +156,55 @@ def head_shard_gather(out_local, group=None):
         buf = torch.stack(parts)
     # [n, B, h, D] -> [B, n*h, D]
     return buf.permute(1, 0, 2, 3).reshape(x.shape[0], world * x.shape[1], x.shape[2])
+
+
+class HeadShard:
+    """This rank's share of a head-sharded decode.
+
+    Rank r owns kv heads [klo, khi) and the query heads that read them
+    [qlo, qhi) of *every* sequence.  The allocator is replicated: every rank
+    runs the same reserve/grow/append stream on its own pool, so block tables
+    are identical everywhere and only the per-head K/V slices differ.  After
+    the local decode the [B, hq/n, D] output slices are all-gathered over the
+    process group (NCCL over NVLink on a B200 box)."""
+
+    def __init__(self, lengths, *, rank: int, world: int, hq: int, hkv: int, head_dim: int, page_size: int,
+                 dtype="bf16", device=None, headroom_tokens: int = 0):
+        from .attention import AttentionConfig
+        from .pool import PagePool
+        from .store import KvStore
+
+        self.rank, self.world = rank, world
+        self.qlo, self.qhi, self.klo, self.khi = head_shard_range(hq, hkv, rank, world)
+        self.lengths = [int(x) for x in lengths]
+        pages = sum(-(-(n + headroom_tokens) // page_size) for n in self.lengths)
+        self.pool = PagePool(max(pages, 1), page_size=page_size)
+        self.store = KvStore(self.pool, self.khi - self.klo, head_dim, dtype=dtype, device=device)
+        self.config = AttentionConfig(head_count=self.qhi - self.qlo, head_dim=head_dim, page_size=page_size,
+                                      kv_head_count=self.khi - self.klo)
+        for s, n in enumerate(self.lengths):
+            self.pool.reserve(s, n)
+        self._batch = None
+
+    def assign(self, seq, positions, k_full, v_full) -> None:
+        """Write this rank's head slice of full-width K/V rows [n, hkv, D]."""
+        self.store.assign(seq, positions, k_full[:, self.klo:self.khi], v_full[:, self.klo:self.khi])
+
+    def step_local(self, q_full, k_new_full, v_new_full, **kw):
+        """Decode step of every sequence on this rank's heads -> [B, hq/n, D]."""
+        from .batch import DecodeBatch
+
+        if self._batch is None:
+            self._batch = DecodeBatch(self.store, list(range(len(self.lengths))), self.config)
+        return self._batch.step(q_full[:, self.qlo:self.qhi].contiguous(),
+                                k_new_full[:, self.klo:self.khi].contiguous(),
+                                v_new_full[:, self.klo:self.khi].contiguous(), **kw)
+
+    def step(self, q_full, k_new_full, v_new_full, group=None, **kw):
+        """Local decode + all-gather of the head slices -> [B, hq, D]."""
+        import torch.distributed as dist
+
+        out = self.step_local(q_full, k_new_full, v_new_full, **kw)
+        if self.world > 1 and dist.is_available() and dist.is_initialized():
+            return head_shard_gather(out, group)
+        return out

@@ -47,3 +47,35 @@ def test_request_shards_decode_their_sequences():
         assert rep["tokens"] == sum(n + 1 for n in sh.lengths)
         assert rep["overhead"] < 0.5
     assert sorted(covered) == list(range(len(lengths)))
+
+
+def test_head_shards_reassemble_the_full_decode():
+    """Head-sharded mode (§8 e-2) simulated on one GPU: the two ranks' head
+    slices, concatenated in rank order (what head_shard_gather does over
+    NCCL), match a float64 reference of the full-width decode."""
+    from paper_2506_07311_b200.sharding import HeadShard
+
+    lengths = [300, 17, 1200]
+    world, hq, hkv, d, ps = 2, 32, 8, 128, 16
+    gen = torch.Generator(device="cuda").manual_seed(9)
+    ks = [torch.randn((n + 1, hkv, d), generator=gen, device="cuda").bfloat16() for n in lengths]
+    vs = [torch.randn((n + 1, hkv, d), generator=gen, device="cuda").bfloat16() for n in lengths]
+    q = torch.randn((len(lengths), hq, d), generator=gen, device="cuda").bfloat16()
+    kn = torch.stack([k[-1] for k in ks])
+    vn = torch.stack([v[-1] for v in vs])
+    outs, dumps = [], []
+    for rank in range(world):
+        sh = HeadShard(lengths, rank=rank, world=world, hq=hq, hkv=hkv, head_dim=d, page_size=ps,
+                       dtype=torch.bfloat16, device="cuda", headroom_tokens=4)
+        for s, n in enumerate(lengths):
+            sh.assign(s, np.arange(n), ks[s][:n], vs[s][:n])
+        outs.append(sh.step(q, kn, vn))  # no process group: the local slice
+        dumps.append(sh.pool.dump())
+    assert dumps[0] == dumps[1]  # replicated allocator: identical tables on every rank
+    full = torch.cat(outs, dim=1)
+    for b in range(len(lengths)):
+        k = ks[b].double().repeat_interleave(hq // hkv, 1)
+        v = vs[b].double().repeat_interleave(hq // hkv, 1)
+        p = torch.softmax(torch.einsum("hd,lhd->hl", q[b].double(), k) / np.sqrt(d), -1)
+        ref = torch.einsum("hl,lhd->hd", p, v)
+        assert relative_error(as_numpy(full[b]), ref.cpu().numpy()) <= 6e-3
