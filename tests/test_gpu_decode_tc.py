@@ -43,7 +43,7 @@ def dense_ref(q, keys, vals, lengths, nkeys, g, scale):
 
 
 def build(lengths, hkv, d, ps, dtype, seed=0, scatter=True):
-    pool = PagePool(sum(-(-n // ps) for n in lengths) * 2 + 8, page_size=ps)
+    pool = PagePool(sum(-(-n // ps) + 1 + i % 3 for i, n in enumerate(lengths)) + 8, page_size=ps)
     store = KvStore(pool, hkv, d, dtype=dtype)
     gen = torch.Generator(device="cuda").manual_seed(seed)
     ks, vs = [], []
@@ -185,3 +185,38 @@ def test_decode_batch_fused_append_matches_oracle(dtype, precision):
     torch.cuda.synchronize()
     assert np.array_equal(as_numpy(store.keys), ostore.keys)
     assert np.array_equal(as_numpy(store.values), ostore.values)
+
+
+@pytest.mark.parametrize("seed", range(8))
+def test_random_shapes_stress(seed):
+    """Random batch / context / head / page mixes (incl. thousands of short
+    sequences and single very long ones) against float64."""
+    rng = np.random.default_rng(100 + seed)
+    hkv = int(rng.choice([1, 2, 4, 8]))
+    g = int(rng.choice([1, 2, 4, 8]))
+    d = int(rng.choice([64, 128]))
+    ps = int(rng.choice([8, 16, 32, 64, 128]))
+    kind = seed % 4
+    if kind == 0:
+        lengths = [int(x) for x in rng.integers(1, 64, 1500)]
+    elif kind == 1:
+        lengths = [int(rng.integers(20000, 40000))]
+    elif kind == 2:
+        lengths = [int(x) for x in np.exp(rng.uniform(0, np.log(20000), 40)).astype(int) + 1]
+    else:
+        lengths = [int(x) for x in rng.integers(100, 3000, 96)]
+    dtype = torch.bfloat16 if seed % 2 == 0 else torch.float16
+    pool, store, keys, vals = build(lengths, hkv, d, ps, dtype, seed=seed, scatter=kind != 1)
+    cfg = AttentionConfig(head_count=hkv * g, head_dim=d, page_size=ps, kv_head_count=hkv)
+    meta = MaskMeta.decode(store.batch_view(list(range(len(lengths)))))
+    q = torch.randn((len(lengths), hkv * g, d), device="cuda").to(dtype)
+    out = paged_attention(q, store, meta, cfg, precision="tensor")
+    assert torch.isfinite(out).all()
+    idx = sorted(set(rng.integers(0, len(lengths), 24).tolist()))
+    offs = np.concatenate([[0], np.cumsum(lengths)])
+    for i in idx:
+        k = keys[offs[i]:offs[i + 1]].double().repeat_interleave(g, dim=1)
+        v = vals[offs[i]:offs[i + 1]].double().repeat_interleave(g, dim=1)
+        p = torch.softmax(torch.einsum("hd,lhd->hl", q[i].double(), k) * cfg.scale, -1)
+        ref = torch.einsum("hl,lhd->hd", p, v)
+        assert relative_error(as_numpy(out[i]), ref.cpu().numpy()) <= 6e-3, (seed, i)

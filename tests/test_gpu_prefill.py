@@ -34,7 +34,7 @@ BF16_TOL = 2e-2
 
 
 def build(lengths, hkv, d, ps, dtype, seed=0, scatter=True):
-    pool = PagePool(sum(-(-n // ps) for n in lengths) * 2 + 8, page_size=ps)
+    pool = PagePool(sum(-(-n // ps) + 1 + i % 3 for i, n in enumerate(lengths)) + 8, page_size=ps)
     store = KvStore(pool, hkv, d, dtype=dtype)
     gen = torch.Generator(device="cuda").manual_seed(seed)
     ks, vs = [], []
@@ -176,3 +176,26 @@ def test_forced_prefill_rejects_unsupported_shapes():
     # auto falls back to the decode kernels for the same call
     ref = dense_prefill_f64(q, ks, vs, [40], [40], 2, cfg.scale)
     assert relative_error(as_numpy(paged_attention(q, store, meta, cfg)), ref.cpu().numpy()) <= 6e-3
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_random_prefill_shapes_stress(seed):
+    """Random suffix metas over random batches (GQA group, head dim, page
+    size, dtype, causal) through K3 against float64 on sampled rows."""
+    rng = np.random.default_rng(200 + seed)
+    hkv = int(rng.choice([1, 2, 4, 8]))
+    g = int(rng.choice([1, 2, 4, 8, 16]))
+    d = int(rng.choice([64, 128]))
+    ps = int(rng.choice([8, 16, 64, 256]))
+    causal = bool(seed % 3)
+    dtype = torch.bfloat16 if seed % 2 == 0 else torch.float16
+    lengths = [int(x) for x in rng.integers(1, 1500, int(rng.integers(1, 7)))]
+    q_lens = [int(rng.integers(1, n + 1)) for n in lengths]
+    pool, store, ks, vs = build(lengths, hkv, d, ps, dtype, seed=seed)
+    cfg = AttentionConfig(head_count=hkv * g, head_dim=d, page_size=ps, kv_head_count=hkv, causal=causal)
+    meta = MaskMeta.suffix(store.batch_view(list(range(len(lengths)))), q_lens)
+    q = torch.randn((meta.query_count, hkv * g, d), device="cuda").to(dtype)
+    out = paged_attention(q, store, meta, cfg, precision="prefill")
+    assert torch.isfinite(out).all()
+    ref = dense_prefill_f64(q, ks, vs, lengths, q_lens, g, cfg.scale, causal=causal)
+    assert relative_error(as_numpy(out), ref.cpu().numpy()) <= 6e-3, seed
