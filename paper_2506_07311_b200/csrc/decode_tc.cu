@@ -39,6 +39,7 @@
 // reads the new token from the input and writes it into its page
 // (reshape-and-cache folded into the decode launch).
 #include <algorithm>
+#include <cstdio>
 #include <cstdlib>
 #include <functional>
 #include <numeric>
@@ -92,7 +93,7 @@ __device__ __forceinline__ void trace_at(bool on, int slot) {
 //          pieces in page order — deterministic, and no combine launch.
 enum {
   H_HB = 0, H_WPH, H_QGS, H_QGROUPS, H_HEAD_ITEMS, H_TOTAL_ITEMS, H_NCOMB, H_NQ,
-  H_GRID, H_CTA_OFF, H_ITEMS, H_COMB, H_CTR, kHdr = 13
+  H_GRID, H_CTA_OFF, H_ITEMS, H_COMB, H_CTR, H_CLUSTER, kHdr = 14
 };
 constexpr int kItemInts = 6;
 constexpr int kCombInts = 4;
@@ -105,7 +106,7 @@ struct PlanView {
   const int32_t *nk, *row;
   const int32_t* items;  // this CTA's first record (shared or global memory)
   int count;             // items of this CTA
-  int hb, wph, qgs, qgroups, nq, ps;
+  int hb, wph, qgs, qgroups, nq, ps, cluster;
 };
 
 // one warp's view of a work item
@@ -133,7 +134,7 @@ __device__ __forceinline__ Item make_item(int k, const PlanView& pv, const TcPar
   it.row = pv.row[q];
   it.kb = pb << p.log2ps;
   it.ke = min(it.nk, pe << p.log2ps);
-  it.last = it.ke == it.nk;
+  it.last = it.kb < it.nk && it.ke == it.nk;  // the piece holding the final token
   it.nchunks = (it.ke - it.kb + kCh - 1) / kCh;
   return it;
 }
@@ -196,6 +197,23 @@ __device__ __forceinline__ void finish_split(const TcParams& p, const int32_t* p
       store_from_float(p.out, (int64_t(qi) * p.hq + qh) * D + lane + 32 * e, p.out_dtype, acc[e] * inv);
   }
   if (lane == 0) *ctr = 0;  // self-cleaning: the plan buffer can be replayed
+}
+
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;\n" ::: "memory");
+}
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+// a float in the shared memory of CTA `rank` of this cluster (DSMEM)
+__device__ __forceinline__ float ld_dsmem(const float* local, uint32_t rank) {
+  uint32_t a = static_cast<uint32_t>(__cvta_generic_to_shared(local)), ra;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(a), "r"(rank));
+  float v;
+  asm volatile("ld.shared::cluster.f32 %0, [%1];" : "=f"(v) : "r"(ra) : "memory");
+  return v;
 }
 
 __device__ __forceinline__ void named_bar(int id, int threads) {
@@ -271,6 +289,9 @@ __global__ void __launch_bounds__(kThreadsTc, 1) decode_tc_kernel(const __grid_c
 
   extern __shared__ __align__(1024) unsigned char smem[];
   __shared__ int s_flag[kWarpsTc];  // per head: this CTA's piece merges the split
+  // cluster mode: this CTA's piece (unnormalised O rows, row max, row sum)
+  __shared__ float s_cl_o[kMergeRows * 128];
+  __shared__ float s_cl_ml[kMergeRows * 2];
   __shared__ int32_t s_cta_items[kCtaItemsSmem * kItemInts];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const bool trace_on = g_trace_on != 0;
@@ -300,6 +321,7 @@ __global__ void __launch_bounds__(kThreadsTc, 1) decode_tc_kernel(const __grid_c
     pv.row = src + o_row(nq);
     pv.hb = src[H_HB];
     pv.wph = src[H_WPH];
+    pv.cluster = src[H_CLUSTER];
     pv.qgs = src[H_QGS];
     pv.qgroups = src[H_QGROUPS];
     pv.nq = nq;
@@ -407,6 +429,7 @@ __global__ void __launch_bounds__(kThreadsTc, 1) decode_tc_kernel(const __grid_c
   long long gcons = 0;
   const float qscale = p.qscale;
   const int head_local = warp / pv.wph;
+  const int cluster = pv.cluster;
   for (int64_t k = 0;; ++k) {
     const Item C = make_item(static_cast<int>(k), pv, p, warp);
     if (!C.valid) break;
@@ -621,7 +644,13 @@ __global__ void __launch_bounds__(kThreadsTc, 1) decode_tc_kernel(const __grid_c
         den += wgt * s_ml[(w * kMergeRows + r) * 2 + 1];
         acc += wgt * s_mo[(w * kMergeRows + r) * D + d];
       }
-      if (C.slot < 0) {
+      if (cluster > 1) {  // cluster mode: stage the piece for the DSMEM merge
+        s_cl_o[e] = acc;
+        if (d == 0) {
+          s_cl_ml[2 * r] = mx;
+          s_cl_ml[2 * r + 1] = den;
+        }
+      } else if (C.slot < 0) {
         store_from_float(p.out, out_base + int64_t(r) * D + d, p.out_dtype, acc / den);
       } else {
         __stcg(p.ws_o + (pslot + r) * D + d, acc);
@@ -629,6 +658,30 @@ __global__ void __launch_bounds__(kThreadsTc, 1) decode_tc_kernel(const __grid_c
       }
     }
     trace(28);
+    if (cluster > 1) {
+      // Cluster mode (small batches): the unit's pieces are the CTAs of this
+      // cluster.  Each CTA merges a 1/cluster slice of the rows x D outputs
+      // straight from its peers' shared memory (DSMEM), in rank order.
+      cluster_sync_all();
+      const int E = C.rows * D;
+      const int rank = static_cast<int>(cluster_rank());
+      const int e0 = rank * E / cluster, e1 = (rank + 1) * E / cluster;
+      for (int e = e0 + static_cast<int>(threadIdx.x); e < e1; e += kThreadsTc) {
+        const int r = e / D;
+        float mx = -INFINITY;
+        for (int c = 0; c < cluster; ++c) mx = fmaxf(mx, ld_dsmem(&s_cl_ml[2 * r], c));
+        float den = 0.f, acc = 0.f;
+        for (int c = 0; c < cluster; ++c) {
+          const float mw = ld_dsmem(&s_cl_ml[2 * r], c);
+          const float w = mw == -INFINITY ? 0.f : exp2f(mw - mx);
+          den += w * ld_dsmem(&s_cl_ml[2 * r + 1], c);
+          acc += w * ld_dsmem(&s_cl_o[e], c);
+        }
+        store_from_float(p.out, out_base + e, p.out_dtype, acc / den);
+      }
+      cluster_sync_all();  // peers' shared memory must outlive the reads
+      break;               // one item per CTA in cluster mode
+    }
     if (C.slot >= 0) finish_split_group<D>(p, p.plan, C.comb, head_local, C.qi, C.qh0, C.rows, tt, grp, bar_id,
                                            &s_flag[head_local]);
     named_bar(bar_id, grp);  // the head's merge slots are free for its next item
@@ -656,6 +709,43 @@ int64_t decode_plan_ints(int64_t nq, int hq) {
   const int64_t units = nq * hq;  // head items per query <= hq
   return o_cta(nq) + (kMaxGrid + 1) + (units + 2 * kMaxGrid) * kItemInts +
          (kMaxGrid + 1) * (kCombInts + kWarpsTc);
+}
+
+// Co-resident clusters of `c` CTAs of the decode kernel (one CTA per SM):
+// queried from the device once (bf16, head_dim 128 instance, full smem),
+// else the measured B200 figures scaled to num_sms.
+int cluster_capacity(int c, int num_sms) {
+  static int cached[17] = {0};
+  if (c < 2 || c > 16) return 0;
+  if (!cached[c]) {
+    int n = 0;
+    int dev_count = 0;
+    if (cudaGetDeviceCount(&dev_count) == cudaSuccess && dev_count > 0) {
+      auto fn = decode_tc_kernel<__nv_bfloat16, 128, false, false>;
+      const int smem = 214016;
+      cudaFuncSetAttribute(reinterpret_cast<const void*>(fn), cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+      cudaFuncSetAttribute(reinterpret_cast<const void*>(fn), cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+      cudaLaunchConfig_t cfg = {};
+      cfg.gridDim = dim3(static_cast<unsigned>(c));
+      cfg.blockDim = dim3(kThreadsTc);
+      cfg.dynamicSmemBytes = smem;
+      cudaLaunchAttribute attr[1];
+      attr[0].id = cudaLaunchAttributeClusterDimension;
+      attr[0].val.clusterDim.x = static_cast<unsigned>(c);
+      attr[0].val.clusterDim.y = 1;
+      attr[0].val.clusterDim.z = 1;
+      cfg.attrs = attr;
+      cfg.numAttrs = 1;
+      if (cudaOccupancyMaxActiveClusters(&n, fn, &cfg) != cudaSuccess) n = 0;
+      cudaGetLastError();
+    }
+    if (n <= 0) {
+      const int b200[17] = {0, 0, 74, 0, 33, 0, 0, 0, 15, 0, 0, 0, 0, 0, 0, 0, 7};
+      n = b200[c] * num_sms / 148;
+    }
+    cached[c] = n;
+  }
+  return cached[c];
 }
 
 // Host planner ("stream-K" for paged decode).  The work of every (query,
@@ -703,7 +793,28 @@ int plan_decode(const int32_t* nk, const int32_t* row, int64_t nq, int page_size
   int grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(num_sms, total_pages * head_items / min_piece)));
   const double seg = double(line) / grid;
 
+  // Cluster mode (small batches, one kv head per CTA): every (query, head
+  // item) unit gets a cluster of C CTAs that split its pages evenly and merge
+  // through distributed shared memory — no global partials, no arrival
+  // counters, no last-arriver latency.
+  // Used only when every cluster is resident at once (the GPC structure caps
+  // co-resident clusters below num_sms / C: 7 x 16, 15 x 8, 33 x 4, 74 x 2 on
+  // a 148-SM B200) and the clusters cover >= 80% of the SMs (measured: a
+  // 65% cover loses more bandwidth than the DSMEM merge saves).
+  int cluster = 1;
+  if (hb == 1 && waves >= 0) {
+    const int64_t units_c = nq * head_items;
+    int64_t max_pages = 0;
+    for (int64_t i = 0; i < nq; ++i) max_pages = std::max<int64_t>(max_pages, (int64_t(nk[i]) + ps - 1) / ps);
+    for (int c = 16; c >= 2; c >>= 1) {
+      if (units_c <= cluster_capacity(c, num_sms) && units_c * c * 10 >= int64_t(num_sms) * 8 && max_pages >= 2 * c) {
+        cluster = c;
+        break;
+      }
+    }
+  }
   int32_t* o = out;
+  o[H_CLUSTER] = cluster;
   o[H_HB] = hb;
   o[H_WPH] = wph;
   o[H_QGS] = qgs;
@@ -713,6 +824,39 @@ int plan_decode(const int32_t* nk, const int32_t* row, int64_t nq, int page_size
   for (int64_t i = 0; i < nq; ++i) {
     o[o_nk(nq) + i] = nk[i];
     o[o_row(nq) + i] = row[i];
+  }
+  if (cluster > 1) {
+    const int64_t units_c = nq * head_items;
+    const int gridc = static_cast<int>(units_c * cluster);
+    int32_t* ctac = o + o_cta(nq);
+    const int64_t ipos = o_cta(nq) + gridc + 1;
+    if (ipos + int64_t(gridc) * kItemInts > cap) return fail(PKV_VALUE_ERROR, "plan buffer too small");
+    int32_t* it = o + ipos;
+    int64_t n = 0;
+    for (int64_t q = 0; q < nq; ++q) {
+      const int64_t pages = (int64_t(nk[q]) + ps - 1) / ps;
+      for (int h = 0; h < head_items; ++h)
+        for (int c = 0; c < cluster; ++c, ++n) {
+          ctac[n] = static_cast<int32_t>(n);
+          int32_t* r = it + n * kItemInts;
+          r[0] = static_cast<int32_t>(q);
+          r[1] = h;
+          r[2] = static_cast<int32_t>(pages * c / cluster);
+          r[3] = static_cast<int32_t>(pages * (c + 1) / cluster);
+          r[4] = -1;
+          r[5] = -1;
+        }
+    }
+    ctac[gridc] = static_cast<int32_t>(n);
+    o[H_TOTAL_ITEMS] = static_cast<int32_t>(n);
+    o[H_NCOMB] = 0;
+    o[H_GRID] = gridc;
+    o[H_CTA_OFF] = static_cast<int32_t>(o_cta(nq));
+    o[H_ITEMS] = static_cast<int32_t>(ipos);
+    o[H_COMB] = static_cast<int32_t>(ipos + n * kItemInts);
+    o[H_CTR] = o[H_COMB];
+    if (n_out) *n_out = ipos + n * kItemInts;
+    return PKV_OK;
   }
   int32_t* cta = o + o_cta(nq);
   const int64_t items_pos = o_cta(nq) + grid + 1;
@@ -823,9 +967,38 @@ int launch_decode_tc(TcParams p, const int32_t* plan_host, int kv_dtype, int hea
       return fail(PKV_CUDA_ERROR, "decode_tc smem attribute (%d B): %s", smem, cudaGetErrorString(e));
     configured[key] = smem;
   }
-  const int grid = plan_host[H_GRID];  // the planner's LPT assignment is per CTA
-  fn<<<grid, kThreadsTc, smem, stream>>>(p);
-  cudaError_t e = cudaGetLastError();
+  const int grid = plan_host[H_GRID];  // the planner's assignment is per CTA
+  const int cluster = plan_host[H_CLUSTER];
+  cudaError_t e;
+  if (cluster > 1) {
+    static bool nonportable[16] = {false};
+    if (!nonportable[key]) {
+      cudaFuncSetAttribute(reinterpret_cast<const void*>(fn), cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+      nonportable[key] = true;
+    }
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(static_cast<unsigned>(grid));
+    cfg.blockDim = dim3(kThreadsTc);
+    cfg.dynamicSmemBytes = static_cast<size_t>(smem);
+    cfg.stream = stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = static_cast<unsigned>(cluster);
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    if (std::getenv("PKV_DEBUG_CLUSTER")) {
+      int n = -1;
+      cudaError_t oe = cudaOccupancyMaxActiveClusters(&n, fn, &cfg);
+      std::fprintf(stderr, "pkv: cluster %d grid %d smem %d -> max active clusters %d (%s)\n", cluster, grid, smem,
+                   n, cudaGetErrorString(oe));
+    }
+    e = cudaLaunchKernelEx(&cfg, fn, p);
+  } else {
+    fn<<<grid, kThreadsTc, smem, stream>>>(p);
+    e = cudaGetLastError();
+  }
   if (e != cudaSuccess) return fail(PKV_CUDA_ERROR, "decode_tc launch: %s", cudaGetErrorString(e));
   return PKV_OK;
 }

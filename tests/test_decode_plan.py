@@ -9,17 +9,18 @@ import pytest
 from paper_2506_07311_b200 import _lib
 from paper_2506_07311_b200.workloads import config_lengths
 
-HDR = 13
+HDR = 14
 
 
 def parse(plan):
-    hb, wph, qgs, qgroups, head_items, total, ncomb, nq, grid, cta_off, items_off, comb_off, ctr_off = plan[:HDR]
+    hb, wph, qgs, qgroups, head_items, total, ncomb, nq, grid, cta_off, items_off, comb_off, ctr_off, cluster = plan[:HDR]
     nk = plan[HDR:HDR + nq]
     cta = plan[cta_off:cta_off + grid + 1]
     items = plan[items_off:items_off + 6 * total].reshape(-1, 6)
     assert (plan[ctr_off:ctr_off + 8 * ncomb] == 0).all() and ctr_off + 8 * ncomb == plan.size
     comb = plan[comb_off:comb_off + 4 * ncomb].reshape(-1, 4)
-    return dict(hb=hb, wph=wph, head_items=head_items, nq=nq, grid=grid, nk=nk, cta=cta, items=items, comb=comb)
+    return dict(hb=hb, wph=wph, head_items=head_items, nq=nq, grid=grid, nk=nk, cta=cta, items=items, comb=comb,
+                cluster=cluster)
 
 
 CASES = [
@@ -45,7 +46,7 @@ def test_segment_plan_covers_every_page_once(name, lengths, hq, hkv):
     pages = -(-nk.astype(np.int64) // ps)
     covered = {}
     for q, h, p0, p1, slot, ci in items:
-        assert 0 <= p0 < p1 <= pages[q]
+        assert 0 <= p0 <= p1 <= pages[q] and (p0 < p1 or P["cluster"] > 1)
         covered.setdefault((q, h), []).append((p0, p1, slot))
         assert (slot < 0) == (ci < 0) and (ci < 0 or tuple(comb[ci][:2]) == (q, h))
     assert len(covered) == nk.size * P["head_items"]
@@ -54,7 +55,9 @@ def test_segment_plan_covers_every_page_once(name, lengths, hq, hkv):
     for (q, h), pieces in covered.items():
         assert pieces[0][0] == 0 and pieces[-1][1] == pages[q]
         assert all(a[1] == b[0] for a, b in zip(pieces, pieces[1:]))  # contiguous, in order
-        if len(pieces) == 1:
+        if P["cluster"] > 1:  # one cluster of CTAs per unit, merged through DSMEM
+            assert len(pieces) == P["cluster"] and all(p[2] == -1 for p in pieces)
+        elif len(pieces) == 1:
             assert pieces[0][2] == -1 and (q, h) not in comb_map
         else:
             s0, n = comb_map[(q, h)]
@@ -66,7 +69,9 @@ def test_segment_plan_covers_every_page_once(name, lengths, hq, hkv):
     for c in range(P["grid"]):
         for q, h, p0, p1, _, _ in items[cta[c]:cta[c + 1]]:
             load[c] += p1 - p0
-    if P["grid"] > 1:
+    if P["grid"] > 1 and P["cluster"] == 1:
         assert load.max() <= load.mean() * 1.15 + 64, (load.max(), load.mean())
+    if P["cluster"] > 1:
+        assert P["grid"] == len(items) <= 148 and P["grid"] % P["cluster"] == 0
     # few items per CTA
     assert len(items) <= nk.size * P["head_items"] + 2 * P["grid"]
