@@ -799,17 +799,32 @@ int plan_decode(const int32_t* nk, const int32_t* row, int64_t nq, int page_size
   // counters, no last-arriver latency.
   // Used only when every cluster is resident at once (the GPC structure caps
   // co-resident clusters below num_sms / C: 7 x 16, 15 x 8, 33 x 4, 74 x 2 on
-  // a 148-SM B200) and the clusters cover >= 80% of the SMs (measured: a
-  // 65% cover loses more bandwidth than the DSMEM merge saves).
+  // a 148-SM B200) and a simple time model predicts a win over the
+  // segment schedule (fewer streaming CTAs vs a much cheaper merge).
   int cluster = 1;
   if (hb == 1 && waves >= 0) {
     const int64_t units_c = nq * head_items;
     int64_t max_pages = 0;
     for (int64_t i = 0; i < nq; ++i) max_pages = std::max<int64_t>(max_pages, (int64_t(nk[i]) + ps - 1) / ps);
+    // time model (us): streaming at ~45 GB/s per CTA plus the merge — a
+    // DSMEM cluster merge ~1 us, the global last-arriver merge ~2 us + 0.4 us
+    // per piece of a unit (measured)
+    const double bytes_per_head_page = double(ps) * 128 * 2 * 2;
+    const double stream_us = double(total_pages) * head_items * bytes_per_head_page / 45e3;
+    const int64_t reg_grid = std::min<int64_t>(num_sms, std::max<int64_t>(1, total_pages * head_items / 16));
+    const double reg_us = stream_us / double(reg_grid) + 2.0 + 0.4 * double((reg_grid + units_c - 1) / units_c);
+    double best = reg_us;
     for (int c = 16; c >= 2; c >>= 1) {
-      if (units_c <= cluster_capacity(c, num_sms) && units_c * c * 10 >= int64_t(num_sms) * 8 && max_pages >= 2 * c) {
+      if (units_c > cluster_capacity(c, num_sms) || units_c * c > num_sms || max_pages < 2 * c) continue;
+      const double t = stream_us / double(units_c * c) + 1.0;
+      // >= 80% SM cover: measured to beat the segment schedule (B = 4-8)
+      if (units_c * c * 10 >= int64_t(num_sms) * 8) {
         cluster = c;
         break;
+      }
+      if (t < best) {
+        best = t;
+        cluster = c;
       }
     }
   }
