@@ -213,7 +213,9 @@ def _check_queries(queries, meta: MaskMeta, config: AttentionConfig):
 
 
 class _Workspace:
-    """Per-device scratch for split partials (and the CUDA-core device plan)."""
+    """Scratch for split partials (and the CUDA-core device plan), one buffer
+    per (device, stream): launches on one stream are ordered, so they may
+    share it; concurrent streams must not."""
 
     _bufs: dict = {}
 
@@ -221,10 +223,11 @@ class _Workspace:
     def get(cls, device, nbytes: int):
         import torch
 
-        buf = cls._bufs.get(device)
+        key = (device, torch.cuda.current_stream(device).cuda_stream)
+        buf = cls._bufs.get(key)
         if buf is None or buf.numel() < nbytes:
             buf = torch.empty(max(nbytes, 1 << 20), dtype=torch.uint8, device=device)
-            cls._bufs[device] = buf
+            cls._bufs[key] = buf
         return buf
 
 

@@ -1,6 +1,6 @@
 // K2-TC: split-K paged decode on the tensor cores (mma.sync m16n8k16, bf16 /
-// fp16 operands, fp32 accumulation) for 16-bit KV caches, plus its split
-// combine (K2c) and the host-side planner.
+// fp16 operands, fp32 accumulation) for 16-bit KV caches, with the split
+// merge done inside the kernel, and its host-side planner.
 //
 // Replaces the reference streaming kernel (attention.py:259-329) for bf16
 // stores.  Decode is HBM bound (GQA-4 bf16: 4 flop/B, far below the ridge), so
@@ -11,39 +11,36 @@
 // (SURVEY.md §2.3).
 //
 // Work decomposition (planned on the host, like any serving scheduler: the
-// per-query key counts are host metadata).  A work item is (query, key split,
-// block of HB kv heads, group of query heads) and is processed by one CTA of 8
-// warps, one CTA per SM.  Each kv head of the block gets WPH = 8/HB warps:
-//   * large batches: HB = 8, WPH = 1 — one warp streams one kv head over the
-//     whole split, no intra-CTA merging at all;
-//   * small batches: HB < 8, WPH > 1 — the warps of a head take its 16-key
-//     chunks round-robin and merge through shared memory (asynchronously: the
-//     last warp to arrive merges in warp order), which keeps the number of
-//     global splits per query small.
-// Items are sorted by size and dealt to CTAs in snake order (LPT balance), so
-// every CTA knows its item sequence up front and every warp runs a producer
-// that streams its chunks through a private 3-stage cp.async ring (16-byte
-// XOR swizzle -> conflict-free LDSM; zero-fill past the valid keys) straight
-// across item boundaries.  The G grouped query heads are the M rows of the
-// MMA, so every K/V byte is read from HBM once per query-head group.
+// per-query key counts are host metadata).  A unit is (query, block of HB kv
+// heads, group of query heads); each CTA (8 warps, one per SM) gives every kv
+// head of the block WPH = 8/HB warps:
+//   * large batches: HB = 8, WPH = 1 — one warp streams one kv head;
+//   * small batches: HB < 8, WPH > 1 — the head's warps take its 16-key
+//     chunks round-robin and merge in parallel through shared memory at a
+//     named barrier.
+// Schedule ("stream-K" for paged decode, plan_decode): all units are laid on
+// one line (pages + a per-item overhead) and cut into one equal segment per
+// SM, so every CTA streams the same bytes and runs only ~units/SMs + 1 items;
+// a unit cut between CTAs is merged by the last of its pieces to finish
+// (arrival counters in the per-call plan upload, self-resetting), in page
+// order — deterministic.  Small batches use cluster mode instead: each unit
+// gets a thread-block cluster whose CTAs split its pages and merge through
+// distributed shared memory.  Every warp runs a producer that streams its
+// chunks through a private 3-stage cp.async ring (16-byte XOR swizzle ->
+// conflict-free LDSM; zero-fill past the valid keys) straight across item
+// boundaries.  The G grouped query heads are the M rows of the MMA, so every
+// K/V byte is read from HBM once per query-head group.
 //
 // Numerics: scores accumulate unscaled in fp32 and the softmax scale (times
 // log2 e) is folded into the exp2 argument; P is rounded to the operand type
 // for the P@V MMA and the denominator sums the *rounded* P.  fp32 queries are
-// split hi+lo into two MMAs (fp32-accurate scores).
-//
-// Splits of a query write (m, l, O) partials; the combine kernel (launched
-// with programmatic dependent launch, so its launch overlaps the decode tail)
-// merges them in ascending split order: deterministic, no atomics in the hot
-// loop.  Optional fused append: with k_new/v_new the last split of each query
-// reads the new token from the input and writes it into its page
-// (reshape-and-cache folded into the decode launch).
+// split hi+lo into two MMAs (fp32-accurate scores).  Optional fused append:
+// with k_new/v_new the piece holding a query's final token reads it from the
+// input and writes it into its page (reshape-and-cache folded into the
+// decode launch).
 #include <algorithm>
 #include <cstdio>
 #include <cstdlib>
-#include <functional>
-#include <numeric>
-#include <queue>
 #include <vector>
 
 #include "common.cuh"
@@ -955,7 +952,6 @@ int plan_decode(const int32_t* nk, const int32_t* row, int64_t nq, int page_size
   return PKV_OK;
 }
 
-int64_t decode_plan_max_splits(int64_t nq) { return nq * 256 + nq; }
 
 int launch_decode_tc(TcParams p, const int32_t* plan_host, int kv_dtype, int head_dim, int num_sms,
                      cudaStream_t stream) {
