@@ -31,7 +31,7 @@ class DecodeBatch:
     for a single layer).
     """
 
-    def __init__(self, stores, seq_ids, config: AttentionConfig):
+    def __init__(self, stores, seq_ids, config: AttentionConfig, capacity: int | None = None):
         import torch
 
         self.stores = list(stores) if isinstance(stores, (list, tuple)) else [stores]
@@ -40,49 +40,63 @@ class DecodeBatch:
         if any(s.pool is not self.pool for s in self.stores):
             raise ValueError("all stores of a DecodeBatch must share one pool")
         self.config = config
+        self._lib = _lib.load()
+        self._qcodes = {torch.float32: _lib.PKV_F32, torch.float16: _lib.PKV_F16,
+                        torch.bfloat16: _lib.PKV_BF16}
+        self._used = C.c_int64()
+        self._used_p = C.byref(self._used)
+        self._n_pages = C.c_int64()
+        self._n_pages_p = C.byref(self._n_pages)
+        self._cap = 0
+        self.last_launches = 0
+        # one persistent argument block; step() updates the per-call fields
+        self._args = _lib.AttentionArgs(
+            seq_start=None, hq=config.head_count, hkv=config.kv_head_count, head_dim=config.head_dim,
+            scale=float(config.scale), num_sms=0, target_waves=0, prof_start=None, prof_stop=None)
+        self._args_p = C.byref(self._args)
+        self.set_sequences(seq_ids, capacity)
+
+    def set_sequences(self, seq_ids, capacity: int | None = None) -> None:
+        """Change the batch membership (continuous batching): later steps
+        advance exactly these sequences.  Staging buffers are reused while
+        the batch fits the current capacity and regrown (x2) otherwise."""
+        import torch
+
         self.seq_ids = list(seq_ids)
-        self.handles = np.asarray([self.pool.table(s)._handle for s in self.seq_ids], dtype=np.int64)
         self.n = len(self.seq_ids)
-        self._copies = np.empty(2 * self.n, dtype=np.int64)
-        self._pages = np.empty(2 * self.n + 1, dtype=np.uint32)
-        self._plan_len = int(_lib.load().pkv_attention_plan_ints(self.n, config.head_count))
-        # packed per-step metadata [q_seq | nkeys | rows | plan]: a ring of
-        # pinned staging buffers, each reused only after its upload completed
-        width = 3 * self.n + self._plan_len
-        self._ring = []
-        for _ in range(4):
-            host = torch.empty(width, dtype=torch.int32).pin_memory()
-            dev = torch.empty(width, dtype=torch.int32, device=self.device)
-            self._ring.append((host, dev, torch.cuda.Event()))
+        self.handles = np.asarray([self.pool.table(s)._handle for s in self.seq_ids], dtype=np.int64)
+        self._handles_p = self.handles.ctypes.data_as(C.POINTER(C.c_int64))
+        need = max(self.n, int(capacity or 0), 1)
+        if need > self._cap:
+            cap = max(need, 2 * self._cap)
+            cfg = self.config
+            self._copies = np.empty(2 * cap, dtype=np.int64)
+            self._pages = np.empty(2 * cap + 1, dtype=np.uint32)
+            self._pages_p = self._pages.ctypes.data_as(C.POINTER(C.c_uint32))
+            self._copies_p = self._copies.ctypes.data_as(C.POINTER(C.c_int64))
+            # packed per-step metadata [q_seq | nkeys | rows | plan]: a ring of
+            # pinned staging buffers, each reused only after its upload landed
+            width = 3 * cap + int(self._lib.pkv_attention_plan_ints(cap, cfg.head_count))
+            self._ring = []
+            for _ in range(4):
+                host = torch.empty(width, dtype=torch.int32).pin_memory()
+                dev = torch.empty(width, dtype=torch.int32, device=self.device)
+                self._ring.append((host, dev, torch.cuda.Event()))
+            ws_bytes = self._lib.pkv_attention_workspace_bytes(cap, cfg.head_count, cfg.head_dim)
+            self._ws = _Workspace.get(self.device, ws_bytes)
+            self._cap = cap
         self._slot = 0
         self._cur = None
         self._uploaded = False
-        self._used = C.c_int64()
-        self._used_p = C.byref(self._used)
-        self.last_launches = 0
-        i64p, u32p = C.POINTER(C.c_int64), C.POINTER(C.c_uint32)
-        self._handles_p = self.handles.ctypes.data_as(i64p)
-        self._pages_p = self._pages.ctypes.data_as(u32p)
-        self._copies_p = self._copies.ctypes.data_as(i64p)
-        self._n_pages = C.c_int64()
-        self._n_pages_p = C.byref(self._n_pages)
-        self._lib = _lib.load()
-        ws_bytes = self._lib.pkv_attention_workspace_bytes(self.n, config.head_count, config.head_dim)
-        self._ws = _Workspace.get(self.device, ws_bytes)
-        self._qcodes = {torch.float32: _lib.PKV_F32, torch.float16: _lib.PKV_F16,
-                        torch.bfloat16: _lib.PKV_BF16}
-        # one persistent argument block; step() updates the per-call fields
-        self._args = _lib.AttentionArgs(
-            n_queries=self.n, seq_start=None, hq=config.head_count, hkv=config.kv_head_count,
-            head_dim=config.head_dim, scale=float(config.scale), num_sms=0, target_waves=0,
-            prof_start=None, prof_stop=None)
-        self._args_p = C.byref(self._args)
+        self._args.n_queries = self.n
 
     def prepare(self) -> int:
         """Host work of one token step: one native call does the allocator
         bookkeeping (grow, copy-on-write, logical_len) and writes the packed
         metadata [q_seq | nkeys | rows | plan] into a pinned staging slot.
         Returns the number of page clear/copy launches it caused."""
+        if self.n == 0:
+            raise ValueError("the decode batch is empty")
         slot = self._slot
         self._slot = (slot + 1) % len(self._ring)
         host, dev, done = self._ring[slot]
@@ -101,7 +115,7 @@ class DecodeBatch:
         if n_pages:
             self.pool._clear_pages(self._pages[:n_pages].tolist())
             launches += len(self.pool._stores)
-        pairs = self._copies.reshape(-1, 2)
+        pairs = self._copies[: 2 * self.n].reshape(-1, 2)
         cow = pairs[:, 1] >= 0
         if cow.any():  # copy-on-write pages: one batched K0b launch per store
             sel = pairs[cow]

@@ -220,3 +220,46 @@ def test_random_shapes_stress(seed):
         p = torch.softmax(torch.einsum("hd,lhd->hl", q[i].double(), k) * cfg.scale, -1)
         ref = torch.einsum("hl,lhd->hd", p, v)
         assert relative_error(as_numpy(out[i]), ref.cpu().numpy()) <= 6e-3, (seed, i)
+
+
+def test_continuous_batching_membership_changes():
+    """DecodeBatch.set_sequences (continuous batching): sequences join and
+    leave between steps; every step matches float64 over each sequence's
+    full context (prompt + every token appended so far)."""
+    hq, hkv, d, ps = 8, 2, 128, 16
+    pool = PagePool(256, ps)
+    store = KvStore(pool, hkv, d, dtype=torch.bfloat16)
+    cfg = AttentionConfig(head_count=hq, head_dim=d, page_size=ps, kv_head_count=hkv)
+    gen = torch.Generator(device="cuda").manual_seed(3)
+    ctx = {}
+
+    def admit(s, n):
+        pool.reserve(s, n)
+        k = torch.randn((n, hkv, d), generator=gen, device="cuda").bfloat16()
+        v = torch.randn((n, hkv, d), generator=gen, device="cuda").bfloat16()
+        store.assign(s, np.arange(n), k, v)
+        ctx[s] = [k, v]
+
+    for s, n in enumerate([30, 100, 17]):
+        admit(s, n)
+    batch = DecodeBatch(store, [0, 1, 2], cfg, capacity=2)  # grows past its initial capacity
+    schedule = [[0, 1, 2], [0, 1, 2], [1, 2, 3], [2, 3, 4, 5, 6], [3, 6]]
+    for step, ids in enumerate(schedule):
+        for s in ids:
+            if s not in ctx:
+                admit(s, 20 + 13 * s)
+        batch.set_sequences(ids)
+        B = len(ids)
+        q = torch.randn((B, hq, d), generator=gen, device="cuda").bfloat16()
+        kn = torch.randn((B, hkv, d), generator=gen, device="cuda").bfloat16()
+        vn = torch.randn((B, hkv, d), generator=gen, device="cuda").bfloat16()
+        out = batch.step(q, kn, vn)
+        for i, s in enumerate(ids):
+            ctx[s][0] = torch.cat([ctx[s][0], kn[i:i + 1]])
+            ctx[s][1] = torch.cat([ctx[s][1], vn[i:i + 1]])
+            k = ctx[s][0].double().repeat_interleave(hq // hkv, 1)
+            v = ctx[s][1].double().repeat_interleave(hq // hkv, 1)
+            p = torch.softmax(torch.einsum("hd,lhd->hl", q[i].double(), k) * cfg.scale, -1)
+            ref = torch.einsum("hl,lhd->hd", p, v)
+            assert relative_error(as_numpy(out[i]), ref.cpu().numpy()) <= 6e-3, (step, s)
+        assert all(pool.table(s).logical_len == ctx[s][0].shape[0] for s in ids)
