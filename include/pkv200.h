@@ -244,6 +244,45 @@ int pkv_decode_step_prepare(pkv_pool* pool, const int64_t* seqs, int64_t n, int3
                             int64_t* meta_used, uint32_t* pages_out, int64_t pages_cap,
                             int64_t* n_pages_out, int64_t* copies_out);
 
+/* The whole host half of a batched decode step in one call (the serving-loop
+ * form of DecodeSession.step, decoder.py:263-284): waits for the staging
+ * slot, runs pkv_decode_step_prepare into meta_host, appends the granted
+ * pages, copy-on-write triples and dirty mirror pairs, uploads everything
+ * with one cudaMemcpyAsync to meta_dev (recording slot_event), then launches
+ * the page clears / copies in every attached store (clear-on-grant,
+ * pool.py:122-126; copy-on-write, store.py:143-145) and the mirror update.
+ * If the device mirror's shape changed (or it is absent) needs_resync is set:
+ * the caller re-exports the mirror before launching attention.  The
+ * attention metadata (meta_used int32) sits at the start of meta_dev. */
+typedef struct pkv_step_stage_args {
+  pkv_pool* pool;
+  const int64_t* seqs;
+  int64_t n;
+  int32_t page_size;
+  int32_t hq;
+  int32_t hkv;
+  int32_t* meta_host;   /* pinned */
+  int32_t* meta_dev;
+  int64_t meta_cap;     /* int32 entries of both slots */
+  void* slot_event;     /* cudaEvent_t or NULL */
+  int32_t n_stores;
+  void* const* k_caches;
+  void* const* v_caches;
+  int64_t row_bytes;
+  int32_t* mirror_dev;
+  int64_t mirror_rows;
+  int64_t mirror_cols;
+  int64_t meta_used;    /* out */
+  int32_t needs_resync; /* out */
+  int32_t launches;     /* out */
+  int64_t n_granted;    /* out: granted pages at meta_host[granted_off ...] */
+  int64_t granted_off;
+  int64_t n_copies;     /* out: (src, dst, rows) triples at meta_host[copies_off ...] */
+  int64_t copies_off;
+} pkv_step_stage_args;
+int64_t pkv_decode_step_stage_ints(int64_t n, int32_t hq);
+int pkv_decode_step_stage(pkv_step_stage_args* args, void* stream);
+
 /* Workspace bound: the split planner never creates more than
  * n_queries + 8192 key splits, so the bound depends only on the query count. */
 int64_t pkv_attention_workspace_bytes(int64_t n_queries, int32_t hq, int32_t head_dim);

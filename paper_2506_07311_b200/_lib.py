@@ -65,6 +65,17 @@ class PrefillArgs(C.Structure):
     ]
 
 
+class StepStageArgs(C.Structure):
+    _fields_ = [
+        ("pool", _vp), ("seqs", _vp), ("n", _i64), ("page_size", _i32), ("hq", _i32), ("hkv", _i32),
+        ("meta_host", _vp), ("meta_dev", _vp), ("meta_cap", _i64), ("slot_event", _vp),
+        ("n_stores", _i32), ("k_caches", _vp), ("v_caches", _vp), ("row_bytes", _i64),
+        ("mirror_dev", _vp), ("mirror_rows", _i64), ("mirror_cols", _i64),
+        ("meta_used", _i64), ("needs_resync", _i32), ("launches", _i32),
+        ("n_granted", _i64), ("granted_off", _i64), ("n_copies", _i64), ("copies_off", _i64),
+    ]
+
+
 # name -> (restype, argtypes); every symbol the header declares
 SIGNATURES = {
     "pkv_last_error": (C.c_char_p, []),
@@ -101,6 +112,8 @@ SIGNATURES = {
     "pkv_page_copy": (C.c_int, [_vp, _vp, _vp, _i64, _i64, _i32, _vp]),
     "pkv_kv_append": (C.c_int, [_vp, _vp, _i64, _vp, _i32, _vp, _vp, _i64, _i32, _vp, _vp, _i64, _vp]),
     "pkv_attention_workspace_bytes": (_i64, [_i64, _i32, _i32]),
+    "pkv_decode_step_stage_ints": (_i64, [_i64, _i32]),
+    "pkv_decode_step_stage": (C.c_int, [_P(StepStageArgs), _vp]),
     "pkv_decode_step_prepare": (C.c_int, [_vp, _vp, _i64, _i32, _i32, _i32, _vp, _i64, _P(_i64), _vp, _i64,
                                           _P(_i64), _vp]),
     "pkv_attention_plan_ints": (_i64, [_i64, _i32]),

@@ -45,8 +45,6 @@ class DecodeBatch:
                         torch.bfloat16: _lib.PKV_BF16}
         self._used = C.c_int64()
         self._used_p = C.byref(self._used)
-        self._n_pages = C.c_int64()
-        self._n_pages_p = C.byref(self._n_pages)
         self._cap = 0
         self.last_launches = 0
         # one persistent argument block; step() updates the per-call fields
@@ -54,6 +52,9 @@ class DecodeBatch:
             seq_start=None, hq=config.head_count, hkv=config.kv_head_count, head_dim=config.head_dim,
             scale=float(config.scale), num_sms=0, target_waves=0, prof_start=None, prof_stop=None)
         self._args_p = C.byref(self._args)
+        self._stage = _lib.StepStageArgs()
+        self._stage_p = C.byref(self._stage)
+        self._stage_stores = None
         self.set_sequences(seq_ids, capacity)
 
     def set_sequences(self, seq_ids, capacity: int | None = None) -> None:
@@ -70,57 +71,70 @@ class DecodeBatch:
         if need > self._cap:
             cap = max(need, 2 * self._cap)
             cfg = self.config
-            self._copies = np.empty(2 * cap, dtype=np.int64)
-            self._pages = np.empty(2 * cap + 1, dtype=np.uint32)
-            self._pages_p = self._pages.ctypes.data_as(C.POINTER(C.c_uint32))
-            self._copies_p = self._copies.ctypes.data_as(C.POINTER(C.c_int64))
             # packed per-step metadata [q_seq | nkeys | rows | plan]: a ring of
             # pinned staging buffers, each reused only after its upload landed
-            width = 3 * cap + int(self._lib.pkv_attention_plan_ints(cap, cfg.head_count))
+            width = int(self._lib.pkv_decode_step_stage_ints(cap, cfg.head_count))
             self._ring = []
             for _ in range(4):
                 host = torch.empty(width, dtype=torch.int32).pin_memory()
                 dev = torch.empty(width, dtype=torch.int32, device=self.device)
-                self._ring.append((host, dev, torch.cuda.Event()))
+                ev = torch.cuda.Event()
+                ev.record()  # materialise the cudaEvent_t handle
+                self._ring.append((host, dev, ev))
             ws_bytes = self._lib.pkv_attention_workspace_bytes(cap, cfg.head_count, cfg.head_dim)
             self._ws = _Workspace.get(self.device, ws_bytes)
             self._cap = cap
         self._slot = 0
         self._cur = None
-        self._uploaded = False
         self._args.n_queries = self.n
 
     def prepare(self) -> int:
-        """Host work of one token step: one native call does the allocator
-        bookkeeping (grow, copy-on-write, logical_len) and writes the packed
-        metadata [q_seq | nkeys | rows | plan] into a pinned staging slot.
-        Returns the number of page clear/copy launches it caused."""
+        """Host work of one token step in one native call
+        (pkv_decode_step_stage): allocator bookkeeping (grow, copy-on-write,
+        logical_len), the packed metadata + work plan, their upload, the page
+        clears / copies in every attached store and the block-table mirror
+        update.  Returns the number of auxiliary kernels it launched."""
         if self.n == 0:
             raise ValueError("the decode batch is empty")
         slot = self._slot
         self._slot = (slot + 1) % len(self._ring)
         host, dev, done = self._ring[slot]
-        done.synchronize()  # the previous upload from this slot has landed
-        cfg = self.config
-        st = self._lib.pkv_decode_step_prepare(
-            self.pool._h, self._handles_p, self.n, self.pool.page_size, cfg.head_count, cfg.kv_head_count,
-            host.data_ptr(), host.numel(), self._used_p, self._pages_p, self._pages.size, self._n_pages_p,
-            self._copies_p)
+        stores = self.pool._stores
+        row_bytes = {s.row_bytes for s in stores}
+        native_pages = len(row_bytes) == 1
+        if native_pages and self._stage_stores != [id(s) for s in stores]:
+            self._kc = (C.c_void_p * len(stores))(*[s.keys.data_ptr() for s in stores])
+            self._vc = (C.c_void_p * len(stores))(*[s.values.data_ptr() for s in stores])
+            self._stage_stores = [id(s) for s in stores]
+        mirror = self.pool._mirror
+        if mirror is None or mirror.device != self.device:
+            mirror = self.pool.device_table(self.device)
+        a = self._stage
+        a.pool, a.seqs, a.n = self.pool._h, self.handles.ctypes.data, self.n
+        a.page_size, a.hq, a.hkv = self.pool.page_size, self.config.head_count, self.config.kv_head_count
+        a.meta_host, a.meta_dev, a.meta_cap = host.data_ptr(), dev.data_ptr(), host.numel()
+        a.slot_event = done.cuda_event
+        a.n_stores = len(stores) if native_pages else 0
+        a.k_caches = C.cast(self._kc, C.c_void_p) if native_pages else None
+        a.v_caches = C.cast(self._vc, C.c_void_p) if native_pages else None
+        a.row_bytes = next(iter(row_bytes)) if native_pages else 0
+        a.mirror_dev, a.mirror_rows, a.mirror_cols = mirror.data_ptr(), mirror.shape[0], mirror.shape[1]
+        st = self._lib.pkv_decode_step_stage(self._stage_p, _stream(self.device))
         if st:
-            _lib.check(st, "pkv_decode_step_prepare")
+            _lib.check(st, "pkv_decode_step_stage")
+        launches = a.launches
+        if not native_pages:  # stores of different row sizes: page work through the stores
+            meta = host.numpy()
+            if a.n_granted:
+                self.pool._clear_pages(meta[a.granted_off:a.granted_off + a.n_granted].tolist())
+                launches += len(stores)
+            if a.n_copies:
+                self.pool._copy_pages(meta[a.copies_off:a.copies_off + 3 * a.n_copies].reshape(-1, 3))
+                launches += len(stores)
+        if a.needs_resync:
+            self.pool.device_table(self.device)  # shape change: full re-export
         self._cur = slot
-        self._uploaded = False
-        launches = 0
-        n_pages = self._n_pages.value
-        if n_pages:
-            self.pool._clear_pages(self._pages[:n_pages].tolist())
-            launches += len(self.pool._stores)
-        pairs = self._copies[: 2 * self.n].reshape(-1, 2)
-        cow = pairs[:, 1] >= 0
-        if cow.any():  # copy-on-write pages: one batched K0b launch per store
-            sel = pairs[cow]
-            self.pool._copy_pages(np.column_stack([sel, np.full(len(sel), self.pool.page_size)]))
-            launches += len(self.pool._stores)
+        self._used.value = a.meta_used
         return launches
 
     def step(self, queries, k_new, v_new, *, out_dtype=None, layer: int = 0, advance: bool = True,
@@ -165,18 +179,14 @@ class DecodeBatch:
         a.mode = PRECISION_MODES[precision]
         a.k_new, a.v_new = k.data_ptr(), v.data_ptr()
         a.plan, a.plan_host = md + 12 * n, hp + 12 * n
-        # the first layer of a token uploads the packed metadata on the stream
-        a.meta_host = None if self._uploaded else hp
+        a.meta_host = None  # uploaded by prepare() (pkv_decode_step_stage)
         a.meta_dev = md
-        a.meta_bytes = 4 * self._used.value
+        a.meta_bytes = 0
         # K1 append is fused into the decode launch (the last split of every
         # sequence reads the new token from k/v and writes it into its page)
         st = self._lib.pkv_paged_attention(self._args_p, _stream(self.device))
         if st:
             _lib.check(st, "pkv_paged_attention")
-        if not self._uploaded:
-            done.record()
-            self._uploaded = True
         tensor = (store.dtype_code == _lib.PKV_BF16 and precision != "exact") or precision == "tensor"
         # tensor-core path: one launch (append fused, split merge in-kernel)
         self.last_launches = launches + (1 if tensor else 4)

@@ -27,6 +27,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <vector>
 #include <cstdint>
 
 #include "common.cuh"
@@ -660,6 +661,91 @@ int pkv_decode_step_prepare(pkv_pool* pool, const int64_t* seqs, int64_t n, int3
                           meta_cap - 3 * n, &used);
   if (st) return st;
   *meta_used = 3 * n + used;
+  return PKV_OK;
+}
+
+int64_t pkv_decode_step_stage_ints(int64_t n, int32_t hq) {
+  return 3 * n + pkv_attention_plan_ints(n, hq) + 16 * n + 64;
+}
+
+int pkv_decode_step_stage(pkv_step_stage_args* a, void* stream_) {
+  if (!a || !a->pool) return pkv::fail(PKV_VALUE_ERROR, "null args");
+  cudaStream_t stream = static_cast<cudaStream_t>(stream_);
+  a->meta_used = 0;
+  a->needs_resync = 0;
+  a->launches = 0;
+  if (a->slot_event) {  // the slot's previous upload has landed
+    cudaError_t e = cudaEventSynchronize(static_cast<cudaEvent_t>(a->slot_event));
+    if (e != cudaSuccess) return pkv::fail(PKV_CUDA_ERROR, "slot event: %s", cudaGetErrorString(e));
+  }
+  const int64_t n = a->n;
+  const int64_t extra = 16 * n + 64;
+  if (a->meta_cap < 3 * n + pkv_attention_plan_ints(n, a->hq) + extra)
+    return pkv::fail(PKV_VALUE_ERROR, "metadata slot too small");
+  // 1) allocator + attention metadata + plan
+  std::vector<uint32_t> pages(2 * n + 1);
+  std::vector<int64_t> copies(2 * n);
+  int64_t n_pages = 0, used = 0;
+  int st = pkv_decode_step_prepare(a->pool, a->seqs, n, a->page_size, a->hq, a->hkv, a->meta_host,
+                                   a->meta_cap - extra, &used, pages.data(), static_cast<int64_t>(pages.size()),
+                                   &n_pages, copies.data());
+  if (st) return st;
+  // 2) side blocks behind it: granted pages | copy triples | mirror pairs
+  int32_t* side = a->meta_host + used;
+  int64_t off = 0;
+  const int64_t pages_off = used + off;
+  for (int64_t i = 0; i < n_pages; ++i) side[off++] = static_cast<int32_t>(pages[i]);
+  const int64_t trip_off = used + off;
+  int64_t n_copies = 0;
+  for (int64_t i = 0; i < n; ++i)
+    if (copies[2 * i + 1] >= 0) {
+      side[off++] = static_cast<int32_t>(copies[2 * i]);
+      side[off++] = static_cast<int32_t>(copies[2 * i + 1]);
+      side[off++] = a->page_size;
+      ++n_copies;
+    }
+  int64_t rows = 0, cols = 0, pending = 0, n_pairs = 0;
+  int32_t full = 0;
+  pkv_pool_mirror_shape(a->pool, &rows, &cols);
+  pkv_pool_mirror_pending(a->pool, &pending, &full);
+  const int64_t room = (a->meta_cap - used - off) / 2;
+  const bool mirror_ok = a->mirror_dev && !full && rows == a->mirror_rows && cols == a->mirror_cols && pending <= room;
+  const int64_t pairs_off = used + off;
+  if (mirror_ok && pending) {
+    pkv_pool_mirror_drain(a->pool, side + off, room, &n_pairs, &full);
+    off += 2 * n_pairs;
+  }
+  a->needs_resync = mirror_ok ? 0 : 1;
+  // 3) one upload of everything, then the page / mirror kernels
+  const int64_t total = used + off;
+  cudaError_t e = cudaMemcpyAsync(a->meta_dev, a->meta_host, static_cast<size_t>(total) * 4,
+                                  cudaMemcpyHostToDevice, stream);
+  if (e != cudaSuccess) return pkv::fail(PKV_CUDA_ERROR, "step metadata upload: %s", cudaGetErrorString(e));
+  if (a->slot_event) cudaEventRecord(static_cast<cudaEvent_t>(a->slot_event), stream);
+  for (int32_t s = 0; s < a->n_stores; ++s) {
+    if (n_pages) {
+      st = pkv_page_zero(a->k_caches[s], a->v_caches[s], a->meta_dev + pages_off, n_pages,
+                         a->row_bytes * a->page_size, stream);
+      if (st) return st;
+      ++a->launches;
+    }
+    if (n_copies) {
+      st = pkv_page_copy(a->k_caches[s], a->v_caches[s], a->meta_dev + trip_off, n_copies, a->row_bytes,
+                         a->page_size, stream);
+      if (st) return st;
+      ++a->launches;
+    }
+  }
+  if (n_pairs) {
+    st = pkv_mirror_apply(a->mirror_dev, a->meta_dev + pairs_off, n_pairs, stream);
+    if (st) return st;
+    ++a->launches;
+  }
+  a->meta_used = used;
+  a->n_granted = n_pages;
+  a->granted_off = pages_off;
+  a->n_copies = n_copies;
+  a->copies_off = trip_off;
   return PKV_OK;
 }
 
