@@ -783,8 +783,16 @@ int plan_decode(const int32_t* nk, const int32_t* row, int64_t nq, int page_size
     const char* e = std::getenv("PKV_DECODE_ITEM_KB");
     return e ? std::max<int64_t>(1, std::atoll(e)) : int64_t(400);  // measured optimum (C2, C3, C5)
   }();
-  const int64_t ovh = std::max<int64_t>(1, (ovh_kb << 10) / page_bytes) * (waves > 0 ? waves : 1);
-  const int64_t min_piece = std::max<int64_t>(ovh / 2, (2 * kCh * wph + ps - 1) / ps);
+  // per-item cost charged on the line (pipeline refill, query load, partial
+  // store; ~400 KB of stream, measured) and the smallest piece a cut may
+  // leave; both tunable for experiments
+  static const int64_t cost_kb = [] {
+    const char* e = std::getenv("PKV_DECODE_COST_KB");
+    return e ? std::max<int64_t>(0, std::atoll(e)) : int64_t(400);
+  }();
+  const int64_t ovh = ((cost_kb << 10) / page_bytes) * (waves > 0 ? waves : 1);
+  const int64_t min_piece = std::max<int64_t>(
+      std::max<int64_t>(1, (ovh_kb << 10) / page_bytes) / 2, (2 * kCh * wph + ps - 1) / ps);
   const int64_t units = nq * head_items;
   const int64_t line = total_pages * head_items + ovh * units;
   int grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(num_sms, total_pages * head_items / min_piece)));
@@ -877,63 +885,76 @@ int plan_decode(const int32_t* nk, const int32_t* row, int64_t nq, int page_size
   int64_t n_items = 0, n_slots = 0;
   std::vector<int32_t> comb;
   const int64_t item_cap = (cap - items_pos) / kItemInts;
-  // remaining work on the line (pages + one overhead per unit or piece);
-  // each CTA's budget is the remaining work over the remaining CTAs, so
-  // rounding and snapped cuts never pile up on the last CTA
-  double remaining = double(line + ovh * (grid - 1));  // ~one cut per CTA boundary
-  int c = 0;           // current CTA
-  double budget = remaining / grid, used = 0.0;
-  cta[0] = 0;
-  auto next_cta = [&]() {
-    ++c;
-    cta[c] = static_cast<int32_t>(n_items);
-    budget = remaining / std::max(1, grid - c);
-    used = 0.0;
-  };
-  for (int64_t q = 0; q < nq; ++q) {
-    const int64_t pages = (int64_t(nk[q]) + ps - 1) / ps;
-    for (int h = 0; h < head_items; ++h) {
-      int64_t p0 = 0;
-      const int64_t first_item = n_items;
-      int npieces = 0;
-      while (p0 < pages) {
-        int64_t take = pages - p0;
-        const double room = budget - used - double(ovh);  // pages that still fit here
-        if (c < grid - 1 && room < double(take)) {
-          int64_t fit = static_cast<int64_t>(room + 0.5);
-          if (fit < min_piece) fit = 0;               // too small: start in the next CTA
-          if (take - fit < min_piece) fit = take;     // remainder too small: keep it here
-          take = fit;
+  // Fill CTAs in line order up to a capacity T (pages + one overhead per
+  // piece); the smallest T that fits in `grid` CTAs is found by bisection,
+  // so the heaviest CTA carries as little as the snapping rules allow and no
+  // CTA is left starved at the end of the line.
+  bool overflow = false;
+  auto fill = [&](double T, bool emit) -> int64_t {
+    int64_t c = 0;
+    double used = 0.0;
+    if (emit) cta[0] = 0;
+    auto next = [&]() {
+      ++c;
+      used = 0.0;
+      if (emit && c <= grid) cta[c] = static_cast<int32_t>(n_items);
+    };
+    for (int64_t q = 0; q < nq; ++q) {
+      const int64_t pages = (int64_t(nk[q]) + ps - 1) / ps;
+      for (int h = 0; h < head_items; ++h) {
+        int64_t p0 = 0;
+        const int64_t first_item = n_items;
+        int npieces = 0;
+        while (p0 < pages) {
+          int64_t take = pages - p0;
+          const double room = T - used - double(ovh);  // pages that still fit here
+          if (room < double(take) && (!emit || c < grid - 1)) {
+            int64_t fit = static_cast<int64_t>(room + 0.5);
+            if (fit < min_piece) fit = 0;               // too small: start in the next CTA
+            if (take - fit < min_piece) fit = take;     // remainder too small: keep it here
+            take = fit;
+          }
+          if (take > 0) {
+            if (emit && n_items >= item_cap) overflow = true;
+            if (emit && !overflow) {
+              int32_t* r = items + n_items * kItemInts;
+              r[0] = static_cast<int32_t>(q);
+              r[1] = h;
+              r[2] = static_cast<int32_t>(p0);
+              r[3] = static_cast<int32_t>(p0 + take);
+              r[4] = -1;
+              r[5] = -1;
+              ++n_items;
+            }
+            ++npieces;
+            p0 += take;
+            used += double(take + ovh);
+          }
+          if (p0 < pages) next();
         }
-        if (take > 0) {
-          if (n_items >= item_cap) return fail(PKV_VALUE_ERROR, "plan buffer too small for items");
-          int32_t* r = items + n_items * kItemInts;
-          r[0] = static_cast<int32_t>(q);
-          r[1] = h;
-          r[2] = static_cast<int32_t>(p0);
-          r[3] = static_cast<int32_t>(p0 + take);
-          r[4] = -1;
-          r[5] = -1;
-          ++n_items;
-          ++npieces;
-          p0 += take;
-          used += double(take + ovh);
-          remaining -= double(take + ovh);
+        if (emit && npieces > 1) {
+          const int32_t comb_idx = static_cast<int32_t>(comb.size() / kCombInts);
+          for (int k = 0; k < npieces; ++k) {
+            items[(first_item + k) * kItemInts + 4] = static_cast<int32_t>(n_slots++);
+            items[(first_item + k) * kItemInts + 5] = comb_idx;
+          }
+          comb.insert(comb.end(), {static_cast<int32_t>(q), h, static_cast<int32_t>(n_slots - npieces), npieces});
         }
-        if (p0 < pages) next_cta();
+        if (used >= T - 0.5 && (!emit || c < grid - 1)) next();  // segment filled
       }
-      if (npieces > 1) {
-        const int32_t comb_idx = static_cast<int32_t>(comb.size() / kCombInts);
-        for (int k = 0; k < npieces; ++k) {
-          items[(first_item + k) * kItemInts + 4] = static_cast<int32_t>(n_slots++);
-          items[(first_item + k) * kItemInts + 5] = comb_idx;
-        }
-        comb.insert(comb.end(), {static_cast<int32_t>(q), h, static_cast<int32_t>(n_slots - npieces), npieces});
-      }
-      if (c < grid - 1 && used >= budget - 0.5) next_cta();  // segment filled exactly
     }
+    return c + (used > 0.0 ? 1 : 0);
+  };
+  double lo = double(line) / grid, hi = lo * 2.0 + double(ovh + min_piece) * 2.0;
+  for (int64_t g2 = fill(hi, false); g2 > grid; g2 = fill(hi, false)) hi *= 1.5;
+  for (int it = 0; it < 40 && hi - lo > 0.25; ++it) {
+    const double mid = 0.5 * (lo + hi);
+    if (fill(mid, false) <= grid) hi = mid; else lo = mid;
   }
-  while (c < grid) cta[++c] = static_cast<int32_t>(n_items);
+  int64_t used_ctas = fill(hi, true);
+  if (overflow) return fail(PKV_VALUE_ERROR, "plan buffer too small for items");
+  int c = static_cast<int>(std::min<int64_t>(used_ctas, grid));
+  for (int cc = c; cc <= grid; ++cc) cta[cc] = static_cast<int32_t>(n_items);
   if (n_slots > 2 * int64_t(kMaxGrid)) return fail(PKV_CONFIG_ERROR, "too many partial slots");
   const int64_t comb_pos = items_pos + n_items * kItemInts;
   const int64_t ncomb = static_cast<int64_t>(comb.size() / kCombInts);

@@ -82,3 +82,31 @@ for c in [0, int(np.argsort(ends)[len(ends) // 2]), int(np.nanargmax(ends))]:
             items.append("[%.1f f%.1f d%.1f s%.1f]" % (s, f, d, st))
         print("  w%d" % w, " ".join(items), "merged %.1f stored %.1f finished %.1f end %.1f" % (
             rel[c, w, 28], rel[c, w, 29], rel[c, w, 30], rel[c, w, 31]))
+
+# per-CTA correlation with the plan: items, pages, cut pieces
+if os.environ.get("CORR"):
+    sys.path.insert(0, "tests")
+    from test_decode_plan import parse
+    lens_now = [int(x) for x in meta.view.lengths]
+    rows_now = [int(pool.table(b).mirror_row) for b in range(B)]
+    P = parse(_lib.attention_plan(np.asarray(lens_now, np.int32), np.asarray(rows_now, np.int32), 16,
+                                  cfg.head_count, cfg.kv_head_count))
+    cta, items = P["cta"], P["items"]
+    recs = []
+    for c in range(min(148, P["grid"])):
+        its = items[cta[c]:cta[c + 1]]
+        pages = int(sum(r[3] - r[2] for r in its))
+        cuts = int(sum(1 for r in its if r[4] >= 0))
+        recs.append((ends[c], c, len(its), pages, cuts))
+    recs.sort()
+    print("fastest:", [(round(e, 1), c, n, p, k) for e, c, n, p, k in recs[:6]])
+    print("slowest:", [(round(e, 1), c, n, p, k) for e, c, n, p, k in recs[-10:]])
+    import collections
+    by_items = collections.defaultdict(list)
+    for e, c, n, p, k in recs:
+        by_items[n].append(e)
+    print("end time by item count:", {n: round(float(np.mean(v)), 1) for n, v in sorted(by_items.items())})
+    by_cuts = collections.defaultdict(list)
+    for e, c, n, p, k in recs:
+        by_cuts[k].append(e)
+    print("end time by cut pieces:", {n: round(float(np.mean(v)), 1) for n, v in sorted(by_cuts.items())})
