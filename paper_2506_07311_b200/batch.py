@@ -55,6 +55,7 @@ class DecodeBatch:
         self._stage = _lib.StepStageArgs()
         self._stage_p = C.byref(self._stage)
         self._stage_stores = None
+        self._store_ptrs = {}
         self.set_sequences(seq_ids, capacity)
 
     def set_sequences(self, seq_ids, capacity: int | None = None) -> None:
@@ -83,12 +84,13 @@ class DecodeBatch:
                 self._ring.append((host, dev, ev))
             ws_bytes = self._lib.pkv_attention_workspace_bytes(cap, cfg.head_count, cfg.head_dim)
             self._ws = _Workspace.get(self.device, ws_bytes)
+            self._args.workspace, self._args.workspace_bytes = self._ws.data_ptr(), self._ws.numel()
             self._cap = cap
         self._slot = 0
         self._cur = None
         self._args.n_queries = self.n
 
-    def prepare(self) -> int:
+    def prepare(self, _sp=None) -> int:
         """Host work of one token step in one native call
         (pkv_decode_step_stage): allocator bookkeeping (grow, copy-on-write,
         logical_len), the packed metadata + work plan, their upload, the page
@@ -119,7 +121,7 @@ class DecodeBatch:
         a.v_caches = C.cast(self._vc, C.c_void_p) if native_pages else None
         a.row_bytes = next(iter(row_bytes)) if native_pages else 0
         a.mirror_dev, a.mirror_rows, a.mirror_cols = mirror.data_ptr(), mirror.shape[0], mirror.shape[1]
-        st = self._lib.pkv_decode_step_stage(self._stage_p, _stream(self.device))
+        st = self._lib.pkv_decode_step_stage(self._stage_p, _sp if _sp is not None else _stream(self.device))
         if st:
             _lib.check(st, "pkv_decode_step_stage")
         launches = a.launches
@@ -145,7 +147,8 @@ class DecodeBatch:
         device)."""
         import torch
 
-        launches = self.prepare() if advance else 0
+        sp = _stream(self.device)
+        launches = self.prepare(sp) if advance else 0
         if self._cur is None:
             raise ValueError("call prepare() before step(advance=False)")
         store: KvStore = self.stores[layer]
@@ -153,29 +156,32 @@ class DecodeBatch:
         n = self.n
         host, dev, done = self._ring[self._cur]
         mirror = self.pool.device_table(self.device)  # applies any pending table edits
+        kv_t = store.torch_dtype
         k = k_new if isinstance(k_new, torch.Tensor) else torch.from_numpy(np.ascontiguousarray(k_new))
         v = v_new if isinstance(v_new, torch.Tensor) else torch.from_numpy(np.ascontiguousarray(v_new))
-        if k.device != self.device or k.dtype != store.torch_dtype or not k.is_contiguous():
-            k = k.to(device=self.device, dtype=store.torch_dtype, non_blocking=True).contiguous()
-        if v.device != self.device or v.dtype != store.torch_dtype or not v.is_contiguous():
-            v = v.to(device=self.device, dtype=store.torch_dtype, non_blocking=True).contiguous()
+        if k.device != self.device or k.dtype != kv_t or not k.is_contiguous():
+            k = k.to(device=self.device, dtype=kv_t, non_blocking=True).contiguous()
+        if v.device != self.device or v.dtype != kv_t or not v.is_contiguous():
+            v = v.to(device=self.device, dtype=kv_t, non_blocking=True).contiguous()
         if isinstance(queries, torch.Tensor) and queries.device == self.device and queries.is_contiguous() \
                 and queries.dtype in self._qcodes:
             q, qcode = queries, self._qcodes[queries.dtype]
         else:
             q, qcode = _q_tensor(queries, self.device)
-        out_t, out_code = torch_dtype(out_dtype or torch.float32)
+        out_t, out_code = (torch.float32, _lib.PKV_F32) if out_dtype is None else torch_dtype(out_dtype)
         out = torch.empty((n, cfg.head_count, cfg.head_dim), dtype=out_t, device=self.device)
         md = dev.data_ptr()
         hp = host.data_ptr()
+        ptrs = self._store_ptrs.get(id(store))
+        if ptrs is None:
+            ptrs = (store.keys.data_ptr(), store.values.data_ptr(), store.dtype_code, store.page_size)
+            self._store_ptrs[id(store)] = ptrs
         a = self._args
         a.q, a.q_dtype = q.data_ptr(), qcode
         a.q_seq, a.q_nkeys, a.seq_row = md, md + 4 * n, md + 8 * n
-        a.k_cache, a.v_cache, a.kv_dtype = store.keys.data_ptr(), store.values.data_ptr(), store.dtype_code
+        a.k_cache, a.v_cache, a.kv_dtype, a.page_size = ptrs
         a.block_table, a.bt_stride = mirror.data_ptr(), mirror.shape[1]
-        a.page_size = store.page_size
         a.out, a.out_dtype = out.data_ptr(), out_code
-        a.workspace, a.workspace_bytes = self._ws.data_ptr(), self._ws.numel()
         a.mode = PRECISION_MODES[precision]
         a.k_new, a.v_new = k.data_ptr(), v.data_ptr()
         a.plan, a.plan_host = md + 12 * n, hp + 12 * n
@@ -184,7 +190,7 @@ class DecodeBatch:
         a.meta_bytes = 0
         # K1 append is fused into the decode launch (the last split of every
         # sequence reads the new token from k/v and writes it into its page)
-        st = self._lib.pkv_paged_attention(self._args_p, _stream(self.device))
+        st = self._lib.pkv_paged_attention(self._args_p, sp)
         if st:
             _lib.check(st, "pkv_paged_attention")
         tensor = (store.dtype_code == _lib.PKV_BF16 and precision != "exact") or precision == "tensor"
