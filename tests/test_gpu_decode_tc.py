@@ -263,3 +263,48 @@ def test_continuous_batching_membership_changes():
             ref = torch.einsum("hl,lhd->hd", p, v)
             assert relative_error(as_numpy(out[i]), ref.cpu().numpy()) <= 6e-3, (step, s)
         assert all(pool.table(s).logical_len == ctx[s][0].shape[0] for s in ids)
+
+
+def test_multi_layer_decode_batch_prepare_once():
+    """A layer stack on one pool: prepare() once per token (allocator +
+    metadata + page clears in every layer's store), then step(layer=i,
+    advance=False) per layer — each layer's fused append + decode matches
+    float64 over its own context."""
+    layers, hq, hkv, d, ps = 3, 8, 2, 64, 16
+    pool = PagePool(64, ps)
+    stores = [KvStore(pool, hkv, d, dtype=torch.bfloat16) for _ in range(layers)]
+    cfg = AttentionConfig(head_count=hq, head_dim=d, page_size=ps, kv_head_count=hkv)
+    gen = torch.Generator(device="cuda").manual_seed(13)
+    lengths = [15, 33]  # both cross a page boundary on the first step
+    ctx = {}
+    for s, n in enumerate(lengths):
+        pool.reserve(s, n)
+        for li, st in enumerate(stores):
+            k = torch.randn((n, hkv, d), generator=gen, device="cuda").bfloat16()
+            v = torch.randn((n, hkv, d), generator=gen, device="cuda").bfloat16()
+            st.assign(s, np.arange(n), k, v)
+            ctx[(li, s)] = [k, v]
+    batch = DecodeBatch(stores, [0, 1], cfg)
+    for step in range(3):
+        batch.prepare()
+        for li in range(layers):
+            q = torch.randn((2, hq, d), generator=gen, device="cuda").bfloat16()
+            kn = torch.randn((2, hkv, d), generator=gen, device="cuda").bfloat16()
+            vn = torch.randn((2, hkv, d), generator=gen, device="cuda").bfloat16()
+            out = batch.step(q, kn, vn, layer=li, advance=False)
+            for i in range(2):
+                c = ctx[(li, i)]
+                c[0] = torch.cat([c[0], kn[i:i + 1]])
+                c[1] = torch.cat([c[1], vn[i:i + 1]])
+                k = c[0].double().repeat_interleave(hq // hkv, 1)
+                v = c[1].double().repeat_interleave(hq // hkv, 1)
+                p = torch.softmax(torch.einsum("hd,lhd->hl", q[i].double(), k) * cfg.scale, -1)
+                ref = torch.einsum("hl,lhd->hd", p, v)
+                assert relative_error(as_numpy(out[i]), ref.cpu().numpy()) <= 6e-3, (step, li, i)
+    # clear-on-grant reached every layer: sequence 0 (15 tokens + 3 steps)
+    # got a fresh page at position 16; it holds the 2 rows appended there and
+    # zeros after them
+    page = pool.table(0).entries[1]
+    for st in stores:
+        rows = st.keys[page * ps:(page + 1) * ps].float()
+        assert (rows[2:] == 0).all() and (rows[:2] != 0).any(dim=(1, 2)).all()
