@@ -327,7 +327,8 @@ def run_ours(args, rank, world, device):
 
 def run_e2e(args, pool, store, cfg, lengths, device, flush, world):
     """Same metric through the public API: DecodeBatch.step with pinned host
-    inputs; H2D of q/k/v and D2H of the attention output are timed."""
+    q/k/v and a pinned host output (one native pkv_decode_step call per
+    step); the H2D of the inputs and the D2H of the output are timed."""
     import torch
     import torch.distributed as dist
 
@@ -356,17 +357,15 @@ def run_e2e(args, pool, store, cfg, lengths, device, flush, world):
         flush.zero_()
         torch.cuda.synchronize(device)
         t0 = time.perf_counter()
-        qd = q.to(device, non_blocking=True)
-        kd = k.to(device, non_blocking=True)
-        vd = v.to(device, non_blocking=True)
-        o = batch.step(qd, kd, vd)
-        out_host.copy_(o, non_blocking=True)
+        # one native call: H2D q/k/v, allocator + plan, fused append +
+        # decode, D2H of the output (pkv_decode_step)
+        batch.step(q, k, v, out=out_host)
         torch.cuda.current_stream(device).synchronize()
         dt = time.perf_counter() - t0
         if i >= W:
             times.append(dt)
             launches += batch.last_launches
-            h2d += q.numel() * 2 + k.numel() * 2 + v.numel() * 2 + 4 * 4 * B
+            h2d += q.numel() * 2 + k.numel() * 2 + v.numel() * 2 + 4 * batch._stage.meta_used
             d2h += out_host.numel() * 4
     kv = 0
     for i in range(K):

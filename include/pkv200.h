@@ -288,6 +288,34 @@ int pkv_decode_step_stage(pkv_step_stage_args* args, void* stream);
 int64_t pkv_attention_workspace_bytes(int64_t n_queries, int32_t hq, int32_t head_dim);
 int pkv_paged_attention(const pkv_attention_args* args, void* stream);
 
+/* One whole decode token step in one call — the serving-loop form of
+ * DecodeSession.step (decoder.py:263-284) for a batch, and the entry a
+ * foreign binding drives with HOST buffers:
+ *   [H2D q / k_new / v_new from q_host / k_host / v_host (each optional)]
+ *   -> pkv_decode_step_stage(stage) -> pkv_paged_attention(attn, K1 fused)
+ *   -> [D2H of attn->out into out_host (optional)]
+ * all on `stream`.  attn->q / k_new / v_new / out are the DEVICE buffers the
+ * copies land in / read from; attn's metadata pointers (q_seq, q_nkeys,
+ * seq_row, plan, plan_host, n_queries) are filled here from the stage slot.
+ * Page work needs the stores attached (stage->n_stores > 0).  When the
+ * allocator changed the block-table shape (stage->needs_resync) nothing is
+ * launched after the stage and io->launched = 0: attn's metadata pointers are
+ * filled, the caller re-exports the mirror, sets attn->block_table /
+ * bt_stride and launches pkv_paged_attention(attn) itself.  Host buffers should be
+ * pinned for the copies to be asynchronous. */
+typedef struct pkv_decode_io {
+  const void* q_host;   /* NULL: attn->q already holds the queries */
+  const void* k_host;
+  const void* v_host;
+  void* out_host;       /* NULL: leave the output on the device */
+  int64_t q_bytes;
+  int64_t kv_bytes;     /* each of k and v */
+  int64_t out_bytes;
+  int32_t launched;     /* out: 1 = attention launched (and D2H issued) */
+  int32_t launches;     /* out: kernels launched by this call */
+} pkv_decode_io;
+int pkv_decode_step(pkv_step_stage_args* stage, pkv_attention_args* attn, pkv_decode_io* io, void* stream);
+
 /* K3   causal / suffix prefill on tcgen05 tensor cores (16-bit caches).
  * Replaces _streaming_attention (attention.py:259-329) under the
  * self-attention and suffix metas (attention.py:81-84, 98-110): the queries

@@ -76,6 +76,13 @@ class StepStageArgs(C.Structure):
     ]
 
 
+class DecodeIO(C.Structure):
+    _fields_ = [
+        ("q_host", _vp), ("k_host", _vp), ("v_host", _vp), ("out_host", _vp),
+        ("q_bytes", _i64), ("kv_bytes", _i64), ("out_bytes", _i64), ("launched", _i32), ("launches", _i32),
+    ]
+
+
 # name -> (restype, argtypes); every symbol the header declares
 SIGNATURES = {
     "pkv_last_error": (C.c_char_p, []),
@@ -119,6 +126,7 @@ SIGNATURES = {
     "pkv_attention_plan_ints": (_i64, [_i64, _i32]),
     "pkv_attention_plan": (C.c_int, [_vp, _vp, _i64, _i32, _i32, _i32, _i32, _i32, _vp, _i64, _P(_i64)]),
     "pkv_paged_attention": (C.c_int, [_P(AttentionArgs), _vp]),
+    "pkv_decode_step": (C.c_int, [_P(StepStageArgs), _P(AttentionArgs), _P(DecodeIO), _vp]),
     "pkv_prefill_supported": (C.c_int, [_i32, _i32, _i32, _i32, _i32]),
     "pkv_prefill_plan_ints": (_i64, [_vp, _i64, _i32, _i32]),
     "pkv_prefill_plan": (C.c_int, [_vp, _vp, _vp, _vp, _i64, _i32, _i32, _i32, _vp, _i64, _P(_i64)]),

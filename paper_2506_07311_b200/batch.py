@@ -20,6 +20,7 @@ import numpy as np
 from . import _lib
 from .attention import PRECISION_MODES, AttentionConfig, _Workspace, _q_tensor
 from .store import KvStore, _stream, torch_dtype
+from .errors import ShapeMismatch
 
 
 class DecodeBatch:
@@ -55,6 +56,13 @@ class DecodeBatch:
         self._stage = _lib.StepStageArgs()
         self._stage_p = C.byref(self._stage)
         self._stage_stores = None
+        self._uniform = False
+        self._stage_fixed = None
+        self._stage_mirror = None
+        self._io = _lib.DecodeIO()
+        self._io_p = C.byref(self._io)
+        self._bufs = {}
+        self._keep = []
         self._store_ptrs = {}
         self.set_sequences(seq_ids, capacity)
 
@@ -75,6 +83,9 @@ class DecodeBatch:
             # packed per-step metadata [q_seq | nkeys | rows | plan]: a ring of
             # pinned staging buffers, each reused only after its upload landed
             width = int(self._lib.pkv_decode_step_stage_ints(cap, cfg.head_count))
+            if self._cap:  # in-flight copies may still read the old ring / host sources
+                torch.cuda.current_stream(self.device).synchronize()
+            self._keep_slot = [None] * 4
             self._ring = []
             for _ in range(4):
                 host = torch.empty(width, dtype=torch.int32).pin_memory()
@@ -86,47 +97,63 @@ class DecodeBatch:
             self._ws = _Workspace.get(self.device, ws_bytes)
             self._args.workspace, self._args.workspace_bytes = self._ws.data_ptr(), self._ws.numel()
             self._cap = cap
+            self._bufs = {}
+        self._ring_ptrs = [(h.data_ptr(), d.data_ptr(), e.cuda_event) for h, d, e in self._ring]
+        self._members = object()  # invalidates the cached stage fields
         self._slot = 0
         self._cur = None
         self._args.n_queries = self.n
 
-    def prepare(self, _sp=None) -> int:
-        """Host work of one token step in one native call
-        (pkv_decode_step_stage): allocator bookkeeping (grow, copy-on-write,
-        logical_len), the packed metadata + work plan, their upload, the page
-        clears / copies in every attached store and the block-table mirror
-        update.  Returns the number of auxiliary kernels it launched."""
+    def _native_pages(self) -> bool:
+        """All attached stores share one row size, so the native stage does
+        the page clears / copies for every store."""
+        stores = self.pool._stores
+        key = [id(s) for s in stores]
+        if self._stage_stores != key:
+            self._uniform = len({s.row_bytes for s in stores}) == 1
+            if self._uniform:
+                self._kc = (C.c_void_p * len(stores))(*[s.keys.data_ptr() for s in stores])
+                self._vc = (C.c_void_p * len(stores))(*[s.values.data_ptr() for s in stores])
+            self._stage_stores = key
+        return self._uniform
+
+    def _stage_setup(self):
+        """Fill the stage arguments for the next ring slot; returns the slot.
+        Fields that only change with the membership, the attached stores or
+        the mirror tensor are rewritten only when those change."""
         if self.n == 0:
             raise ValueError("the decode batch is empty")
         slot = self._slot
         self._slot = (slot + 1) % len(self._ring)
-        host, dev, done = self._ring[slot]
-        stores = self.pool._stores
-        row_bytes = {s.row_bytes for s in stores}
-        native_pages = len(row_bytes) == 1
-        if native_pages and self._stage_stores != [id(s) for s in stores]:
-            self._kc = (C.c_void_p * len(stores))(*[s.keys.data_ptr() for s in stores])
-            self._vc = (C.c_void_p * len(stores))(*[s.values.data_ptr() for s in stores])
-            self._stage_stores = [id(s) for s in stores]
+        a = self._stage
+        a.meta_host, a.meta_dev, a.slot_event = self._ring_ptrs[slot]
+        native_pages = self._native_pages()
+        if self._stage_fixed != (self._stage_stores, self._members):
+            stores = self.pool._stores
+            a.pool, a.seqs, a.n = self.pool._h, self.handles.ctypes.data, self.n
+            a.page_size, a.hq, a.hkv = self.pool.page_size, self.config.head_count, self.config.kv_head_count
+            a.meta_cap = self._ring[0][0].numel()
+            a.n_stores = len(stores) if native_pages else 0
+            a.k_caches = C.cast(self._kc, C.c_void_p) if native_pages else None
+            a.v_caches = C.cast(self._vc, C.c_void_p) if native_pages else None
+            a.row_bytes = stores[0].row_bytes if native_pages else 0
+            self._stage_fixed = (self._stage_stores, self._members)
         mirror = self.pool._mirror
         if mirror is None or mirror.device != self.device:
             mirror = self.pool.device_table(self.device)
+        if mirror is not self._stage_mirror:
+            a.mirror_dev, a.mirror_rows, a.mirror_cols = mirror.data_ptr(), mirror.shape[0], mirror.shape[1]
+            self._stage_mirror = mirror
+        return slot
+
+    def _stage_finish(self, slot) -> int:
+        """Page work the native stage could not do (mixed row sizes) and the
+        full mirror re-export after a block-table shape change."""
         a = self._stage
-        a.pool, a.seqs, a.n = self.pool._h, self.handles.ctypes.data, self.n
-        a.page_size, a.hq, a.hkv = self.pool.page_size, self.config.head_count, self.config.kv_head_count
-        a.meta_host, a.meta_dev, a.meta_cap = host.data_ptr(), dev.data_ptr(), host.numel()
-        a.slot_event = done.cuda_event
-        a.n_stores = len(stores) if native_pages else 0
-        a.k_caches = C.cast(self._kc, C.c_void_p) if native_pages else None
-        a.v_caches = C.cast(self._vc, C.c_void_p) if native_pages else None
-        a.row_bytes = next(iter(row_bytes)) if native_pages else 0
-        a.mirror_dev, a.mirror_rows, a.mirror_cols = mirror.data_ptr(), mirror.shape[0], mirror.shape[1]
-        st = self._lib.pkv_decode_step_stage(self._stage_p, _sp if _sp is not None else _stream(self.device))
-        if st:
-            _lib.check(st, "pkv_decode_step_stage")
         launches = a.launches
-        if not native_pages:  # stores of different row sizes: page work through the stores
-            meta = host.numpy()
+        if not a.n_stores:  # stores of different row sizes: page work through the stores
+            stores = self.pool._stores
+            meta = self._ring[slot][0].numpy()
             if a.n_granted:
                 self.pool._clear_pages(meta[a.granted_off:a.granted_off + a.n_granted].tolist())
                 launches += len(stores)
@@ -139,15 +166,144 @@ class DecodeBatch:
         self._used.value = a.meta_used
         return launches
 
-    def step(self, queries, k_new, v_new, *, out_dtype=None, layer: int = 0, advance: bool = True,
+    def prepare(self, _sp=None) -> int:
+        """Host work of one token step in one native call
+        (pkv_decode_step_stage): allocator bookkeeping (grow, copy-on-write,
+        logical_len), the packed metadata + work plan, their upload, the page
+        clears / copies in every attached store and the block-table mirror
+        update.  Returns the number of auxiliary kernels it launched."""
+        slot = self._stage_setup()
+        st = self._lib.pkv_decode_step_stage(self._stage_p, _sp if _sp is not None else _stream(self.device))
+        if st:
+            _lib.check(st, "pkv_decode_step_stage")
+        return self._stage_finish(slot)
+
+    def _buffer(self, name, shape, dtype):
+        """Persistent device buffer (capacity-sized) for host-side inputs /
+        outputs; a view of the first n rows is returned."""
+        import torch
+
+        key = (name, dtype, shape)
+        view = self._bufs.get(key)
+        if view is None:  # a capacity-sized buffer per (name, dtype, row shape); cached n-row view
+            base = self._bufs.get((name, dtype, shape[1:], self._cap))
+            if base is None:
+                base = torch.empty((self._cap,) + tuple(shape[1:]), dtype=dtype, device=self.device)
+                self._bufs[(name, dtype, shape[1:], self._cap)] = base
+            view = self._bufs[key] = base[:shape[0]]
+        return view
+
+    def _input(self, x, dtype, shape, name):
+        """-> (device tensor, host pointer or None, bytes).  CPU inputs are
+        copied by the native step into a persistent device buffer (pin them
+        for an asynchronous copy); device inputs are used in place."""
+        import torch
+
+        if type(x) is torch.Tensor and x.dtype is dtype and not x.is_cuda and x.shape == shape \
+                and x.is_contiguous():  # fast path: a host tensor ready to copy
+            self._keep.append(x)
+            return self._buffer(name, shape, dtype), x.data_ptr(), x.nbytes
+        if not isinstance(x, torch.Tensor):
+            x = torch.from_numpy(np.ascontiguousarray(x))
+        if tuple(x.shape) != shape:
+            raise ShapeMismatch(f"{name} has shape {tuple(x.shape)}, expected {shape}")
+        if x.device.type == "cpu":
+            if x.dtype != dtype or not x.is_contiguous():
+                x = x.to(dtype).contiguous()
+            self._keep.append(x)
+            return self._buffer(name, shape, dtype), x.data_ptr(), x.numel() * x.element_size()
+        if x.device != self.device or x.dtype != dtype or not x.is_contiguous():
+            x = x.to(device=self.device, dtype=dtype, non_blocking=True).contiguous()
+        return x, None, 0
+
+    def step(self, queries, k_new, v_new, *, out=None, out_dtype=None, layer: int = 0, advance: bool = True,
              precision: str = "auto"):
         """Append one token per sequence into `stores[layer]` and attend.
 
         queries [B, Hq, D]; k_new / v_new [B, Hkv, D] (numpy or torch, any
-        device)."""
+        device).  With `advance` (the default) the whole step — copies of CPU
+        inputs, allocator + plan + metadata upload, page work, the fused
+        append + decode launch and the copy into a CPU `out` — is ONE native
+        call (pkv_decode_step).  `out` (optional) is a [B, Hq, D] tensor the
+        result is written to: on the device, or on the host (pinned: the
+        copy is asynchronous on the current stream, synchronise before
+        reading it, as with a non_blocking torch copy)."""
         import torch
 
         sp = _stream(self.device)
+        if not advance or not self._native_pages():
+            return self._step_split(queries, k_new, v_new, out=out, out_dtype=out_dtype, layer=layer,
+                                    advance=advance, precision=precision, sp=sp)
+        store: KvStore = self.stores[layer]
+        cfg = self.config
+        n = self.n
+        self._keep = []
+        qd = queries.dtype if isinstance(queries, torch.Tensor) else None
+        q_t = qd if qd in self._qcodes else torch.float32
+        q, q_host, q_bytes = self._input(queries, q_t, (n, cfg.head_count, cfg.head_dim), "queries")
+        kv_shape = (n, cfg.kv_head_count, cfg.head_dim)
+        k, k_host, kv_bytes = self._input(k_new, store.torch_dtype, kv_shape, "k_new")
+        v, v_host, _ = self._input(v_new, store.torch_dtype, kv_shape, "v_new")
+        out_host = None
+        if out is None:
+            out_t, out_code = (torch.float32, _lib.PKV_F32) if out_dtype is None else torch_dtype(out_dtype)
+            o = torch.empty((n, cfg.head_count, cfg.head_dim), dtype=out_t, device=self.device)
+            result = o
+        else:
+            if tuple(out.shape) != (n, cfg.head_count, cfg.head_dim) or not out.is_contiguous() \
+                    or out.dtype not in self._qcodes:
+                raise ShapeMismatch("out must be a contiguous [B, Hq, D] float32/float16/bfloat16 tensor")
+            out_code = self._qcodes[out.dtype]
+            if out.device.type == "cpu":
+                o = self._buffer("out", tuple(out.shape), out.dtype)
+                out_host = out
+            else:
+                o = out
+            result = out
+        slot = self._stage_setup()
+        ptrs = self._store_ptrs.get(id(store))
+        if ptrs is None:
+            ptrs = (store.keys.data_ptr(), store.values.data_ptr(), store.dtype_code, store.page_size)
+            self._store_ptrs[id(store)] = ptrs
+        a = self._args
+        a.q, a.q_dtype = q.data_ptr(), self._qcodes[q.dtype]
+        a.k_cache, a.v_cache, a.kv_dtype, a.page_size = ptrs
+        a.block_table, a.bt_stride = self._stage.mirror_dev, self._stage.mirror_cols
+        a.out, a.out_dtype = o.data_ptr(), out_code
+        a.mode = PRECISION_MODES[precision]
+        a.k_new, a.v_new = k.data_ptr(), v.data_ptr()
+        io = self._io
+        io.q_host, io.k_host, io.v_host = q_host, k_host, v_host
+        io.q_bytes, io.kv_bytes = q_bytes, kv_bytes
+        io.out_host = out_host.data_ptr() if out_host is not None else None
+        io.out_bytes = out_host.numel() * out_host.element_size() if out_host is not None else 0
+        st = self._lib.pkv_decode_step(self._stage_p, self._args_p, self._io_p, sp)
+        # host sources stay referenced until this slot's event (recorded after
+        # their copies) has been waited on by the call that reuses the slot
+        self._keep_slot[slot] = self._keep
+        if st:
+            _lib.check(st, "pkv_decode_step")
+        launches = self._stage_finish(slot)
+        if not io.launched:  # block-table shape changed: launch on the re-exported mirror
+            mirror = self.pool.device_table(self.device)
+            a.block_table, a.bt_stride = mirror.data_ptr(), mirror.shape[1]
+            st = self._lib.pkv_paged_attention(self._args_p, sp)
+            if st:
+                _lib.check(st, "pkv_paged_attention")
+            if out_host is not None:
+                out_host.copy_(o, non_blocking=True)
+            tensor = (store.dtype_code == _lib.PKV_BF16 and precision != "exact") or precision == "tensor"
+            launches += 1 if tensor else 4
+        else:
+            launches = io.launches
+        self.last_launches = launches
+        return result
+
+    def _step_split(self, queries, k_new, v_new, *, out, out_dtype, layer, advance, precision, sp):
+        """prepare() (when advancing) + the attention launch as two calls:
+        the multi-layer form (advance=False) and stores of mixed row sizes."""
+        import torch
+
         launches = self.prepare(sp) if advance else 0
         if self._cur is None:
             raise ValueError("call prepare() before step(advance=False)")
@@ -168,8 +324,18 @@ class DecodeBatch:
             q, qcode = queries, self._qcodes[queries.dtype]
         else:
             q, qcode = _q_tensor(queries, self.device)
-        out_t, out_code = (torch.float32, _lib.PKV_F32) if out_dtype is None else torch_dtype(out_dtype)
-        out = torch.empty((n, cfg.head_count, cfg.head_dim), dtype=out_t, device=self.device)
+        host_out = None
+        if out is not None and out.device.type == "cpu":
+            host_out, out = out, None
+            out_dtype = host_out.dtype
+        if out is None:
+            out_t, out_code = (torch.float32, _lib.PKV_F32) if out_dtype is None else torch_dtype(out_dtype)
+            out = torch.empty((n, cfg.head_count, cfg.head_dim), dtype=out_t, device=self.device)
+        else:
+            if tuple(out.shape) != (n, cfg.head_count, cfg.head_dim) or not out.is_contiguous() \
+                    or out.dtype not in self._qcodes:
+                raise ShapeMismatch("out must be a contiguous [B, Hq, D] float32/float16/bfloat16 tensor")
+            out_code = self._qcodes[out.dtype]
         md = dev.data_ptr()
         hp = host.data_ptr()
         ptrs = self._store_ptrs.get(id(store))
@@ -196,4 +362,7 @@ class DecodeBatch:
         tensor = (store.dtype_code == _lib.PKV_BF16 and precision != "exact") or precision == "tensor"
         # tensor-core path: one launch (append fused, split merge in-kernel)
         self.last_launches = launches + (1 if tensor else 4)
+        if host_out is not None:
+            host_out.copy_(out, non_blocking=True)
+            return host_out
         return out

@@ -945,8 +945,13 @@ int plan_decode(const int32_t* nk, const int32_t* row, int64_t nq, int page_size
     }
     return c + (used > 0.0 ? 1 : 0);
   };
-  double lo = double(line) / grid, hi = lo * 2.0 + double(ovh + min_piece) * 2.0;
-  for (int64_t g2 = fill(hi, false); g2 > grid; g2 = fill(hi, false)) hi *= 1.5;
+  // the optimum sits just above the even split line/grid: start with a tight
+  // bracket and widen only if it is infeasible (halves the fill passes)
+  double lo = double(line) / grid, hi = lo * 1.04 + double(ovh + min_piece) * 2.0;
+  for (int64_t g2 = fill(hi, false); g2 > grid; g2 = fill(hi, false)) {
+    lo = hi;
+    hi *= 1.5;
+  }
   for (int it = 0; it < 40 && hi - lo > 0.25; ++it) {
     const double mid = 0.5 * (lo + hi);
     if (fill(mid, false) <= grid) hi = mid; else lo = mid;

@@ -29,6 +29,7 @@
 #include <algorithm>
 #include <vector>
 #include <cstdint>
+#include <cstring>
 
 #include "common.cuh"
 #include "decode_tc.h"
@@ -71,6 +72,40 @@ __global__ void page_copy_kernel(char* k, char* v, const int32_t* triples, int64
     zero_bytes(k + dst * pb + keep, pb - keep, threadIdx.x, blockDim.x);
     zero_bytes(v + dst * pb + keep, pb - keep, threadIdx.x, blockDim.x);
   }
+}
+
+// All page work of one decode step in ONE launch, for every attached store:
+// blocks [0, n_stores * (n_zero + n_copy)) each clear or copy one page of one
+// store, and every block also applies a slice of the block-table mirror pairs.
+// Copy destinations are removed from the zero list on the host (a copy writes
+// the whole destination page), so no two blocks touch the same bytes.
+__global__ void step_aux_kernel(const uint64_t* __restrict__ caches, int n_stores,
+                                const int32_t* __restrict__ zero_pages, int64_t n_zero,
+                                const int32_t* __restrict__ triples, int64_t n_copy,
+                                int32_t* __restrict__ mirror, const int32_t* __restrict__ pairs,
+                                int64_t n_pairs, int64_t row_bytes, int page_size) {
+  const int64_t pb = row_bytes * page_size;
+  const int64_t per_store = n_zero + n_copy;
+  for (int64_t w = blockIdx.x; w < per_store * n_stores; w += gridDim.x) {
+    const int64_t st = w / per_store, i = w % per_store;
+    char* k = reinterpret_cast<char*>(caches[2 * st]);
+    char* v = reinterpret_cast<char*>(caches[2 * st + 1]);
+    if (i < n_zero) {
+      const int64_t off = int64_t(zero_pages[i]) * pb;
+      zero_bytes(k + off, pb, threadIdx.x, blockDim.x);
+      zero_bytes(v + off, pb, threadIdx.x, blockDim.x);
+    } else {
+      const int32_t* t = triples + 3 * (i - n_zero);
+      const int64_t src = t[0], dst = t[1], keep = int64_t(t[2]) * row_bytes;
+      copy_bytes(k + dst * pb, k + src * pb, keep, threadIdx.x, blockDim.x);
+      copy_bytes(v + dst * pb, v + src * pb, keep, threadIdx.x, blockDim.x);
+      zero_bytes(k + dst * pb + keep, pb - keep, threadIdx.x, blockDim.x);
+      zero_bytes(v + dst * pb + keep, pb - keep, threadIdx.x, blockDim.x);
+    }
+  }
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n_pairs;
+       i += int64_t(gridDim.x) * blockDim.x)
+    mirror[pairs[2 * i]] = pairs[2 * i + 1];
 }
 
 // one CTA per token (grid-stride); the slot is resolved in-kernel from the
@@ -664,8 +699,13 @@ int pkv_decode_step_prepare(pkv_pool* pool, const int64_t* seqs, int64_t n, int3
   return PKV_OK;
 }
 
+// side blocks behind the plan: granted pages, copy triples, mirror pairs, the
+// zero list and the per-store cache pointer table (up to kMaxStageStores)
+constexpr int64_t kMaxStageStores = 256;
+static int64_t stage_extra(int64_t n) { return 24 * n + 4 * kMaxStageStores + 64; }
+
 int64_t pkv_decode_step_stage_ints(int64_t n, int32_t hq) {
-  return 3 * n + pkv_attention_plan_ints(n, hq) + 16 * n + 64;
+  return 3 * n + pkv_attention_plan_ints(n, hq) + stage_extra(n);
 }
 
 int pkv_decode_step_stage(pkv_step_stage_args* a, void* stream_) {
@@ -679,7 +719,9 @@ int pkv_decode_step_stage(pkv_step_stage_args* a, void* stream_) {
     if (e != cudaSuccess) return pkv::fail(PKV_CUDA_ERROR, "slot event: %s", cudaGetErrorString(e));
   }
   const int64_t n = a->n;
-  const int64_t extra = 16 * n + 64;
+  const int64_t extra = stage_extra(n);
+  if (a->n_stores > kMaxStageStores)
+    return pkv::fail(PKV_CONFIG_ERROR, "more than %d stores on one pool", static_cast<int>(kMaxStageStores));
   if (a->meta_cap < 3 * n + pkv_attention_plan_ints(n, a->hq) + extra)
     return pkv::fail(PKV_VALUE_ERROR, "metadata slot too small");
   // 1) allocator + attention metadata + plan
@@ -690,7 +732,8 @@ int pkv_decode_step_stage(pkv_step_stage_args* a, void* stream_) {
                                    a->meta_cap - extra, &used, pages.data(), static_cast<int64_t>(pages.size()),
                                    &n_pages, copies.data());
   if (st) return st;
-  // 2) side blocks behind it: granted pages | copy triples | mirror pairs
+  // 2) side blocks behind it: granted pages | copy triples | mirror pairs |
+  //    zero list (granted minus copy destinations) | cache pointers
   int32_t* side = a->meta_host + used;
   int64_t off = 0;
   const int64_t pages_off = used + off;
@@ -708,7 +751,8 @@ int pkv_decode_step_stage(pkv_step_stage_args* a, void* stream_) {
   int32_t full = 0;
   pkv_pool_mirror_shape(a->pool, &rows, &cols);
   pkv_pool_mirror_pending(a->pool, &pending, &full);
-  const int64_t room = (a->meta_cap - used - off) / 2;
+  const int64_t aux_ints = n_pages + 4 * int64_t(a->n_stores) + 1;  // zero list + pointer table + alignment
+  const int64_t room = (a->meta_cap - used - off - aux_ints) / 2;
   const bool mirror_ok = a->mirror_dev && !full && rows == a->mirror_rows && cols == a->mirror_cols && pending <= room;
   const int64_t pairs_off = used + off;
   if (mirror_ok && pending) {
@@ -716,29 +760,42 @@ int pkv_decode_step_stage(pkv_step_stage_args* a, void* stream_) {
     off += 2 * n_pairs;
   }
   a->needs_resync = mirror_ok ? 0 : 1;
-  // 3) one upload of everything, then the page / mirror kernels
+  const bool page_work = a->n_stores > 0 && (n_pages || n_copies);
+  int64_t zero_off = 0, n_zero = 0, ptr_off = 0;
+  if (page_work) {
+    zero_off = used + off;
+    for (int64_t i = 0; i < n_pages; ++i) {
+      bool is_dst = false;
+      for (int64_t c = 0; c < n_copies && !is_dst; ++c) is_dst = side[trip_off - used + 3 * c + 1] == side[i];
+      if (!is_dst) side[off++] = side[i];
+    }
+    n_zero = used + off - zero_off;
+    if ((used + off) & 1) side[off++] = 0;  // 8-byte alignment of the pointer table
+    ptr_off = used + off;
+    for (int32_t st2 = 0; st2 < a->n_stores; ++st2) {
+      const uint64_t kp = reinterpret_cast<uint64_t>(a->k_caches[st2]);
+      const uint64_t vp = reinterpret_cast<uint64_t>(a->v_caches[st2]);
+      std::memcpy(side + off, &kp, 8);
+      std::memcpy(side + off + 2, &vp, 8);
+      off += 4;
+    }
+  }
+  // 3) one upload of everything, then ONE page / mirror kernel
   const int64_t total = used + off;
+  if (total > a->meta_cap) return pkv::fail(PKV_VALUE_ERROR, "metadata slot too small");
   cudaError_t e = cudaMemcpyAsync(a->meta_dev, a->meta_host, static_cast<size_t>(total) * 4,
                                   cudaMemcpyHostToDevice, stream);
   if (e != cudaSuccess) return pkv::fail(PKV_CUDA_ERROR, "step metadata upload: %s", cudaGetErrorString(e));
   if (a->slot_event) cudaEventRecord(static_cast<cudaEvent_t>(a->slot_event), stream);
-  for (int32_t s = 0; s < a->n_stores; ++s) {
-    if (n_pages) {
-      st = pkv_page_zero(a->k_caches[s], a->v_caches[s], a->meta_dev + pages_off, n_pages,
-                         a->row_bytes * a->page_size, stream);
-      if (st) return st;
-      ++a->launches;
-    }
-    if (n_copies) {
-      st = pkv_page_copy(a->k_caches[s], a->v_caches[s], a->meta_dev + trip_off, n_copies, a->row_bytes,
-                         a->page_size, stream);
-      if (st) return st;
-      ++a->launches;
-    }
-  }
-  if (n_pairs) {
-    st = pkv_mirror_apply(a->mirror_dev, a->meta_dev + pairs_off, n_pairs, stream);
-    if (st) return st;
+  if (page_work || n_pairs) {
+    if (a->row_bytes & 1) return pkv::fail(PKV_CONFIG_ERROR, "row bytes must be even");
+    const int n_st = page_work ? a->n_stores : 0;
+    const int64_t blocks = std::max<int64_t>(n_st * (n_zero + n_copies), (n_pairs + 255) / 256);
+    step_aux_kernel<<<static_cast<unsigned>(std::min<int64_t>(std::max<int64_t>(blocks, 1), 65535)), 256, 0,
+                      stream>>>(reinterpret_cast<const uint64_t*>(a->meta_dev + ptr_off), n_st,
+                                a->meta_dev + zero_off, n_zero, a->meta_dev + trip_off, n_copies,
+                                a->mirror_dev, a->meta_dev + pairs_off, n_pairs, a->row_bytes, a->page_size);
+    PKV_CHECK_LAUNCH();
     ++a->launches;
   }
   a->meta_used = used;
@@ -906,6 +963,58 @@ int pkv_paged_attention(const pkv_attention_args* a, void* stream_) {
                    stream>>>(plan, a->n_queries, a->hq, a->head_dim, ws_ml, ws_o, a->out,
                              a->out_dtype);
   PKV_CHECK_LAUNCH();
+  return PKV_OK;
+}
+
+int pkv_decode_step(pkv_step_stage_args* stage, pkv_attention_args* attn, pkv_decode_io* io, void* stream_) {
+  if (!stage || !attn) return pkv::fail(PKV_VALUE_ERROR, "null args");
+  cudaStream_t stream = static_cast<cudaStream_t>(stream_);
+  if (io) io->launched = io->launches = 0;
+  // the input copies go first so they overlap the host-side allocator / plan
+  auto h2d = [&](const void* src, const void* dst, int64_t bytes, const char* what) -> int {
+    if (!src) return PKV_OK;
+    if (!dst || bytes <= 0) return pkv::fail(PKV_VALUE_ERROR, "%s: host source without device buffer", what);
+    cudaError_t e = cudaMemcpyAsync(const_cast<void*>(dst), src, static_cast<size_t>(bytes),
+                                    cudaMemcpyHostToDevice, stream);
+    return e == cudaSuccess ? PKV_OK : pkv::fail(PKV_CUDA_ERROR, "%s upload: %s", what, cudaGetErrorString(e));
+  };
+  if (io) {
+    int st = h2d(io->q_host, attn->q, io->q_bytes, "q");
+    if (!st) st = h2d(io->k_host, attn->k_new, io->kv_bytes, "k_new");
+    if (!st) st = h2d(io->v_host, attn->v_new, io->kv_bytes, "v_new");
+    if (st) return st;
+  }
+  int st = pkv_decode_step_stage(stage, stream_);
+  if (st) return st;
+  if (stage->n_stores == 0 && (stage->n_granted || stage->n_copies))
+    return pkv::fail(PKV_VALUE_ERROR, "decode step needs the stores attached for page clears / copies");
+  if (io) io->launches = stage->launches;
+  const int64_t n = stage->n;
+  int32_t* md = stage->meta_dev;
+  attn->n_queries = n;
+  attn->q_seq = md;
+  attn->q_nkeys = md + n;
+  attn->seq_row = md + 2 * n;
+  attn->plan = md + 3 * n;
+  attn->plan_host = stage->meta_host + 3 * n;
+  attn->meta_host = nullptr;
+  attn->meta_bytes = 0;
+  // block-table shape changed: the caller re-exports the mirror, points
+  // attn->block_table at it and launches pkv_paged_attention(attn) itself
+  if (stage->needs_resync) return PKV_OK;
+  st = pkv_paged_attention(attn, stream_);
+  if (st) return st;
+  const bool tensor = attn->mode == 2 || (attn->mode == 0 && attn->kv_dtype == PKV_BF16);
+  if (io) {
+    io->launches += tensor ? 1 : 4;
+    if (io->out_host) {
+      if (io->out_bytes <= 0) return pkv::fail(PKV_VALUE_ERROR, "out_host without out_bytes");
+      cudaError_t e = cudaMemcpyAsync(io->out_host, attn->out, static_cast<size_t>(io->out_bytes),
+                                      cudaMemcpyDeviceToHost, stream);
+      if (e != cudaSuccess) return pkv::fail(PKV_CUDA_ERROR, "output download: %s", cudaGetErrorString(e));
+    }
+    io->launched = 1;
+  }
   return PKV_OK;
 }
 

@@ -308,3 +308,78 @@ def test_multi_layer_decode_batch_prepare_once():
     for st in stores:
         rows = st.keys[page * ps:(page + 1) * ps].float()
         assert (rows[2:] == 0).all() and (rows[:2] != 0).any(dim=(1, 2)).all()
+
+
+@pytest.mark.parametrize("dtype", [torch.bfloat16, torch.float16])
+def test_host_buffer_step_single_native_call(dtype):
+    """DecodeBatch.step with pinned HOST q/k/v and a pinned host `out`: the
+    copies, allocator, plan, page work, fused append + decode and the D2H are
+    one native call (pkv_decode_step).  Covers page crossings (granted pages
+    cleared natively), a block-table shape change mid-run (the re-export
+    path), a device `out`, and numpy inputs."""
+    hq, hkv, d, ps = 16, 4, 128, 8
+    pool = PagePool(512, ps)
+    store = KvStore(pool, hkv, d, dtype=dtype)
+    cfg = AttentionConfig(head_count=hq, head_dim=d, page_size=ps, kv_head_count=hkv)
+    gen = torch.Generator(device="cuda").manual_seed(21)
+    lengths = [6, 15, 40]  # cross page boundaries on the first steps
+    ctx = []
+    for s, n in enumerate(lengths):
+        pool.reserve(s, n)
+        k = torch.randn((n, hkv, d), generator=gen, device="cuda").to(dtype)
+        v = torch.randn((n, hkv, d), generator=gen, device="cuda").to(dtype)
+        store.assign(s, np.arange(n), k, v)
+        ctx.append([k, v])
+    batch = DecodeBatch(store, list(range(3)), cfg)
+    B = 3
+    out_h = torch.empty((B, hq, d), dtype=torch.float32).pin_memory()
+    for step in range(40):  # 40 + 40 tokens -> the mirror's column count grows
+        q = torch.randn((B, hq, d), generator=gen, device="cuda").to(dtype)
+        kn = torch.randn((B, hkv, d), generator=gen, device="cuda").to(dtype)
+        vn = torch.randn((B, hkv, d), generator=gen, device="cuda").to(dtype)
+        if step % 3 == 0:
+            res = batch.step(q.cpu().pin_memory(), kn.cpu().pin_memory(), vn.cpu().pin_memory(), out=out_h)
+            assert res is out_h
+            torch.cuda.current_stream().synchronize()
+            got = out_h.clone()
+        elif step % 3 == 1:
+            dev_out = torch.empty((B, hq, d), dtype=torch.float32, device="cuda")
+            res = batch.step(q, kn.cpu().float().numpy(), vn.cpu().float().numpy(), out=dev_out)
+            assert res is dev_out
+            got = dev_out.cpu()
+        else:
+            got = batch.step(q, kn, vn).cpu()
+        assert batch.last_launches >= 1
+        for i in range(B):
+            ctx[i][0] = torch.cat([ctx[i][0], kn[i:i + 1]])
+            ctx[i][1] = torch.cat([ctx[i][1], vn[i:i + 1]])
+            k = ctx[i][0].double().repeat_interleave(hq // hkv, 1)
+            v = ctx[i][1].double().repeat_interleave(hq // hkv, 1)
+            p = torch.softmax(torch.einsum("hd,lhd->hl", q[i].double(), k) * cfg.scale, -1)
+            ref = torch.einsum("hl,lhd->hd", p, v)
+            assert relative_error(got[i].numpy(), ref.cpu().numpy()) <= 6e-3, (step, i)
+    for i in range(B):  # the cache holds exactly the appended tokens
+        kk, vv = store.gather(i, ctx[i][0].shape[0])
+        assert torch.equal(kk, ctx[i][0]) and torch.equal(vv, ctx[i][1])
+
+
+def test_step_mixed_row_sizes_uses_split_path():
+    """Stores of different row sizes on one pool: step() falls back to the
+    two-call form (page work through the stores) and stays correct."""
+    hq, hkv, d, ps = 8, 2, 64, 16
+    pool = PagePool(64, ps)
+    store = KvStore(pool, hkv, d, dtype=torch.bfloat16)
+    KvStore(pool, hkv, 2 * d, dtype=torch.bfloat16)  # second layer with a different row size
+    cfg = AttentionConfig(head_count=hq, head_dim=d, page_size=ps, kv_head_count=hkv)
+    pool.reserve(0, 16)
+    k = torch.randn((16, hkv, d), device="cuda").bfloat16()
+    store.assign(0, np.arange(16), k, k)
+    batch = DecodeBatch(store, [0], cfg)
+    q = torch.randn((1, hq, d), device="cuda").bfloat16()
+    kn = torch.randn((1, hkv, d), device="cuda").bfloat16()
+    out = batch.step(q, kn, kn)
+    kk = torch.cat([k, kn]).double().repeat_interleave(hq // hkv, 1)
+    p = torch.softmax(torch.einsum("hd,lhd->hl", q[0].double(), kk) * cfg.scale, -1)
+    ref = torch.einsum("hl,lhd->hd", p, kk)
+    assert relative_error(as_numpy(out[0]), ref.cpu().numpy()) <= 6e-3
+    assert pool.table(0).logical_len == 17

@@ -6,6 +6,7 @@ reference metric verify.py:40-43) and 2e-2 for bf16 outputs.
 """
 
 import math
+import os
 
 import numpy as np
 import pytest
@@ -426,3 +427,23 @@ def test_attention_weights_diagnostic():
     assert relative_error(out.cpu().numpy(), o.cpu().numpy()) <= 1e-5
     # a future key of query 0 (sequence 0, position 33) has zero weight
     assert float(w[0, :, 34:37].abs().max()) == 0.0
+
+
+def test_pure_c_abi_client(tmp_path):
+    """tests/abi_decode.cpp drives the engine through the C ABI only
+    (allocator, K1 append, plan, fused append + decode) and checks the output
+    against its own CPU reference — the boundary a foreign binding uses."""
+    import subprocess
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    lib_dir = os.path.join(root, "paper_2506_07311_b200")
+    exe = str(tmp_path / "abi_decode")
+    build = subprocess.run(
+        ["g++", "-O2", "-std=c++17", "-I", os.path.join(root, "include"), "-I", "/usr/local/cuda/include",
+         os.path.join(root, "tests", "abi_decode.cpp"), "-L", lib_dir, "-lpkv200", "-L", "/usr/local/cuda/lib64",
+         "-lcudart", f"-Wl,-rpath,{lib_dir}", "-Wl,-rpath,/usr/local/cuda/lib64", "-o", exe],
+        capture_output=True, text=True)
+    assert build.returncode == 0, build.stderr[-3000:]
+    run = subprocess.run([exe], capture_output=True, text=True, timeout=120)
+    assert run.returncode == 0, run.stdout + run.stderr
+    assert run.stdout.startswith("abi ok")
