@@ -208,3 +208,54 @@ class HeadShard:
         if self.world > 1 and dist.is_available() and dist.is_initialized():
             return head_shard_gather(out, group)
         return out
+
+
+def _event_seqs(ev):
+    from .workload import ForkEvent
+
+    return (ev.parent, ev.child) if isinstance(ev, ForkEvent) else (ev.seq,)
+
+
+def shard_trace(trace, world: int) -> list:
+    """Split a workload trace (its JSONL form is the sharder's wire format,
+    reference workload.py:61-85) into `world` per-rank traces.
+
+    Sequences linked by forks share pages, so each fork family stays on one
+    rank; families are placed by LPT on the tokens they bring (prompts,
+    decode bursts, fork prefixes).  Every rank keeps the events of its
+    families in trace order, so its replay is exactly the global trace
+    restricted to its sequences.  Deterministic: every rank computes the
+    same split from the same document without communicating."""
+    parent = {}
+
+    def find(x):
+        parent.setdefault(x, x)
+        while parent[x] != x:
+            parent[x] = parent[parent[x]]
+            x = parent[x]
+        return x
+
+    for ev in trace.events:
+        seqs = _event_seqs(ev)
+        roots = [find(s) for s in seqs]
+        for r in roots[1:]:
+            if r != roots[0]:
+                parent[r] = roots[0]
+    fams, weight = {}, []
+    for ev in trace.events:
+        f = find(_event_seqs(ev)[0])
+        if f not in fams:
+            fams[f] = len(weight)
+            weight.append(0)
+        n = getattr(ev, "prompt_len", None)
+        n = getattr(ev, "n_tokens", n) if n is None else n
+        n = getattr(ev, "prefix_len", n) if n is None else n
+        weight[fams[f]] += int(n or 0)
+    rank_of = [0] * len(weight)
+    for r, part in enumerate(lpt_partition(weight, world)):
+        for i in part:
+            rank_of[i] = r
+    out = [type(trace)(name=f"{trace.name}@{r}/{world}", seed=trace.seed, events=[]) for r in range(world)]
+    for ev in trace.events:
+        out[rank_of[fams[find(_event_seqs(ev)[0])]]].events.append(ev)
+    return out

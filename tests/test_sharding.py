@@ -85,3 +85,58 @@ def test_lpt_balance_and_overhead_numbers():
     with pytest.raises(ValueError):
         head_shard_range(32, 8, 0, 3)
     assert lpt_partition([5, 5, 5], 2) == [[0, 2], [1]]
+
+
+def _trace_worker(rank, world, port, q):
+    from paper_2506_07311_b200 import workload as W
+    from paper_2506_07311_b200.sharding import shard_trace
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        # rank 0 owns the trace; the JSONL document is the wire format
+        doc = [None]
+        if rank == 0:
+            t = W.gen_mixed_batch(11, "uniform", count=24)
+            fam = W.Trace("f", None, [W.Arrive("root", 1000), W.ForkEvent("root", "a", 1000),
+                                      W.ForkEvent("a", "b", 515), W.Decode("b", 40), W.Finish("root"),
+                                      W.Finish("a"), W.Finish("b")])
+            t.events = fam.events[:3] + t.events + fam.events[3:]
+            doc = [t.to_jsonl()]
+        dist.broadcast_object_list(doc, src=0)
+        trace = W.Trace.from_jsonl(doc[0])
+        mine = shard_trace(trace, world)[rank]
+        acct = W.account(mine, W.PagedModel(16), W.KvBytesConfig())  # replays cleanly on its own
+        seqs = sorted({s for ev in mine.events for s in
+                       ((ev.parent, ev.child) if isinstance(ev, W.ForkEvent) else (ev.seq,))})
+        rep = {"tokens": mine.total_tokens(), "seqs": seqs, "peak": acct.peak_live_tokens,
+               "events": len(mine.events), "hash": trace.stable_hash()}
+        reps = [None] * world
+        dist.all_gather_object(reps, rep)
+        q.put((rank, reps, trace.total_tokens(), len(trace.events)))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_two_rank_trace_sharding_over_the_jsonl_wire():
+    """A trace is broadcast as JSONL, every rank derives the same shard
+    split (fork families kept whole), replays and audits its shard alone."""
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_trace_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    results = [q.get(timeout=120) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    for rank, reps, total, n_events in results:
+        assert len({r["hash"] for r in reps}) == 1
+        assert sum(r["tokens"] for r in reps) == total
+        assert sum(r["events"] for r in reps) == n_events
+        s0, s1 = set(reps[0]["seqs"]), set(reps[1]["seqs"])
+        assert not (s0 & s1) and len(s0 | s1) == 24 + 3
+        assert {"root", "a", "b"} <= s0 or {"root", "a", "b"} <= s1  # the fork family stays together
+        assert min(r["tokens"] for r in reps) > 0.3 * total  # LPT balance
