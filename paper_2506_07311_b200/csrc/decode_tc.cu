@@ -196,8 +196,17 @@ __device__ __forceinline__ void finish_split(const TcParams& p, const int32_t* p
   if (lane == 0) *ctr = 0;  // self-cleaning: the plan buffer can be replayed
 }
 
-__device__ __forceinline__ void cluster_sync_all() {
-  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;\n" ::: "memory");
+// split-phase cluster barrier (all threads of every CTA of the cluster)
+__device__ __forceinline__ void cluster_arrive_relaxed() {
+  asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void cluster_wait() { asm volatile("barrier.cluster.wait.aligned;" ::: "memory"); }
+// remote (DSMEM) store into CTA `rank`'s copy of `local`; fire-and-forget,
+// made visible by the next barrier.cluster.arrive.release / wait.acquire
+__device__ __forceinline__ void st_dsmem(float* local, uint32_t rank, float v) {
+  uint32_t a = static_cast<uint32_t>(__cvta_generic_to_shared(local)), ra;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(a), "r"(rank));
+  asm volatile("st.shared::cluster.f32 [%0], %1;" ::"r"(ra), "f"(v) : "memory");
 }
 __device__ __forceinline__ uint32_t cluster_rank() {
   uint32_t r;
@@ -205,14 +214,6 @@ __device__ __forceinline__ uint32_t cluster_rank() {
   return r;
 }
 // a float in the shared memory of CTA `rank` of this cluster (DSMEM)
-__device__ __forceinline__ float ld_dsmem(const float* local, uint32_t rank) {
-  uint32_t a = static_cast<uint32_t>(__cvta_generic_to_shared(local)), ra;
-  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(a), "r"(rank));
-  float v;
-  asm volatile("ld.shared::cluster.f32 %0, [%1];" : "=f"(v) : "r"(ra) : "memory");
-  return v;
-}
-
 __device__ __forceinline__ void named_bar(int id, int threads) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(threads) : "memory");
 }
@@ -286,9 +287,10 @@ __global__ void __launch_bounds__(kThreadsTc, 1) decode_tc_kernel(const __grid_c
 
   extern __shared__ __align__(1024) unsigned char smem[];
   __shared__ int s_flag[kWarpsTc];  // per head: this CTA's piece merges the split
-  // cluster mode: this CTA's piece (unnormalised O rows, row max, row sum)
-  __shared__ float s_cl_o[kMergeRows * 128];
-  __shared__ float s_cl_ml[kMergeRows * 2];
+  // cluster mode: the slices of the unit's pieces pushed here by every CTA of
+  // the cluster (unnormalised O, then row max / row sum per piece)
+  __shared__ float r_o[kMergeRows * 128 + 16];
+  __shared__ float r_ml[16 * kMergeRows * 2];
   __shared__ int32_t s_cta_items[kCtaItemsSmem * kItemInts];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const bool trace_on = g_trace_on != 0;
@@ -323,6 +325,9 @@ __global__ void __launch_bounds__(kThreadsTc, 1) decode_tc_kernel(const __grid_c
     pv.qgroups = src[H_QGROUPS];
     pv.nq = nq;
   }
+  // cluster mode: announce that this CTA runs (its shared memory may receive
+  // peer stores once every CTA has arrived; waited on before the first push)
+  if (pv.cluster > 1) cluster_arrive_relaxed();
   trace(1);
   float* s_mo = reinterpret_cast<float*>(smem + p.merge_offset);  // [W][4][D]
   float* s_ml = s_mo + kWarpsTc * kMergeRows * D;                 // [W][4][2]
@@ -629,8 +634,12 @@ __global__ void __launch_bounds__(kThreadsTc, 1) decode_tc_kernel(const __grid_c
     named_bar(bar_id, grp);
     trace(5 + 4 * int(k));
     const int w0 = head_local * pv.wph;
+    const int E = C.rows * D;
+    const int slice = cluster > 1 ? (E + cluster - 1) / cluster : E;
+    const uint32_t my_rank = cluster > 1 ? cluster_rank() : 0u;
+    if (cluster > 1) cluster_wait();  // every peer runs: its shared memory may be written
 #pragma unroll 1
-    for (int e = tt; e < C.rows * D; e += grp) {
+    for (int e = tt; e < E; e += grp) {
       const int r = e / D, d = e - r * D;
       float mx = -INFINITY;
       for (int w = w0; w < w0 + pv.wph; ++w) mx = fmaxf(mx, s_ml[(w * kMergeRows + r) * 2]);
@@ -641,12 +650,14 @@ __global__ void __launch_bounds__(kThreadsTc, 1) decode_tc_kernel(const __grid_c
         den += wgt * s_ml[(w * kMergeRows + r) * 2 + 1];
         acc += wgt * s_mo[(w * kMergeRows + r) * D + d];
       }
-      if (cluster > 1) {  // cluster mode: stage the piece for the DSMEM merge
-        s_cl_o[e] = acc;
-        if (d == 0) {
-          s_cl_ml[2 * r] = mx;
-          s_cl_ml[2 * r + 1] = den;
-        }
+      if (cluster > 1) {  // push the element to the CTA that merges its slice
+        const int owner = e / slice;
+        st_dsmem(&r_o[my_rank * slice + (e - owner * slice)], owner, acc);
+        if (d == 0)  // and the row's max / sum to every peer
+          for (int c = 0; c < cluster; ++c) {
+            st_dsmem(&r_ml[(my_rank * kMergeRows + r) * 2], c, mx);
+            st_dsmem(&r_ml[(my_rank * kMergeRows + r) * 2 + 1], c, den);
+          }
       } else if (C.slot < 0) {
         store_from_float(p.out, out_base + int64_t(r) * D + d, p.out_dtype, acc / den);
       } else {
@@ -657,27 +668,26 @@ __global__ void __launch_bounds__(kThreadsTc, 1) decode_tc_kernel(const __grid_c
     trace(28);
     if (cluster > 1) {
       // Cluster mode (small batches): the unit's pieces are the CTAs of this
-      // cluster.  Each CTA merges a 1/cluster slice of the rows x D outputs
-      // straight from its peers' shared memory (DSMEM), in rank order.
-      cluster_sync_all();
-      const int E = C.rows * D;
-      const int rank = static_cast<int>(cluster_rank());
-      const int e0 = rank * E / cluster, e1 = (rank + 1) * E / cluster;
+      // cluster.  Every CTA pushed its slice-e values into the owner's shared
+      // memory above; after one cluster barrier each CTA merges its own
+      // 1/cluster slice of the rows x D outputs from LOCAL shared memory, in
+      // rank order.  No peer touches this CTA's memory after the barrier.
+      asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;\n" ::: "memory");
+      const int e0 = static_cast<int>(my_rank) * slice, e1 = min(E, e0 + slice);
       for (int e = e0 + static_cast<int>(threadIdx.x); e < e1; e += kThreadsTc) {
         const int r = e / D;
         float mx = -INFINITY;
-        for (int c = 0; c < cluster; ++c) mx = fmaxf(mx, ld_dsmem(&s_cl_ml[2 * r], c));
+        for (int c = 0; c < cluster; ++c) mx = fmaxf(mx, r_ml[(c * kMergeRows + r) * 2]);
         float den = 0.f, acc = 0.f;
         for (int c = 0; c < cluster; ++c) {
-          const float mw = ld_dsmem(&s_cl_ml[2 * r], c);
+          const float mw = r_ml[(c * kMergeRows + r) * 2];
           const float w = mw == -INFINITY ? 0.f : exp2f(mw - mx);
-          den += w * ld_dsmem(&s_cl_ml[2 * r + 1], c);
-          acc += w * ld_dsmem(&s_cl_o[e], c);
+          den += w * r_ml[(c * kMergeRows + r) * 2 + 1];
+          acc += w * r_o[c * slice + (e - e0)];
         }
         store_from_float(p.out, out_base + e, p.out_dtype, acc / den);
       }
-      cluster_sync_all();  // peers' shared memory must outlive the reads
-      break;               // one item per CTA in cluster mode
+      break;  // one item per CTA in cluster mode
     }
     if (C.slot >= 0) finish_split_group<D>(p, p.plan, C.comb, head_local, C.qi, C.qh0, C.rows, tt, grp, bar_id,
                                            &s_flag[head_local]);

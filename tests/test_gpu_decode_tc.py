@@ -383,3 +383,24 @@ def test_step_mixed_row_sizes_uses_split_path():
     ref = torch.einsum("hl,lhd->hd", p, kk)
     assert relative_error(as_numpy(out[0]), ref.cpu().numpy()) <= 6e-3
     assert pool.table(0).logical_len == 17
+
+
+@pytest.mark.parametrize("lengths", [[2048], [5000], [3000, 40, 2000, 17], [2048] * 8, [700, 2100]])
+def test_cluster_mode_dsmem_merge(lengths):
+    """Small batches take the cluster schedule (one unit per cluster of CTAs,
+    pieces merged through distributed shared memory); covers pieces with no
+    keys (short sequences split over many CTAs)."""
+    from paper_2506_07311_b200 import _lib
+
+    hq, hkv, d, ps = 32, 8, 128, 16
+    pool, store, keys, vals = build(lengths, hkv, d, ps, torch.bfloat16, seed=len(lengths))
+    cfg = AttentionConfig(head_count=hq, head_dim=d, page_size=ps, kv_head_count=hkv)
+    meta = MaskMeta.decode(store.batch_view(list(range(len(lengths)))))
+    rows = np.asarray([pool.table(i).mirror_row for i in range(len(lengths))], dtype=np.int32)
+    plan = _lib.attention_plan(np.asarray(lengths, dtype=np.int32), rows, ps, hq, hkv, 0)
+    assert plan[13] > 1, "expected the cluster schedule"  # H_CLUSTER
+    q = torch.randn((len(lengths), hq, d), device="cuda").bfloat16()
+    out = paged_attention(q, store, meta, cfg)
+    ref = dense_ref(q, keys, vals, lengths, lengths, hq // hkv, cfg.scale)
+    assert relative_error(as_numpy(out), ref.cpu().numpy()) <= 6e-3
+    assert torch.equal(out, paged_attention(q, store, meta, cfg))  # deterministic
