@@ -285,6 +285,12 @@ int pkv_decode_step_stage(pkv_step_stage_args* args, void* stream);
 
 /* Workspace bound: the split planner never creates more than
  * n_queries + 8192 key splits, so the bound depends only on the query count. */
+/* pkv_decode_step computes the NEXT step's plan (every key count + 1) while
+ * the GPU runs the current one and memoises it per host thread;
+ * pkv_attention_plan returns the memoised plan when its inputs match exactly
+ * (the plan is a pure function of them).  Reset drops the memo (tests). */
+void pkv_plan_memo_reset(void);
+
 int64_t pkv_attention_workspace_bytes(int64_t n_queries, int32_t hq, int32_t head_dim);
 int pkv_paged_attention(const pkv_attention_args* args, void* stream);
 

@@ -124,6 +124,7 @@ SIGNATURES = {
     "pkv_decode_step_prepare": (C.c_int, [_vp, _vp, _i64, _i32, _i32, _i32, _vp, _i64, _P(_i64), _vp, _i64,
                                           _P(_i64), _vp]),
     "pkv_attention_plan_ints": (_i64, [_i64, _i32]),
+    "pkv_plan_memo_reset": (None, []),
     "pkv_attention_plan": (C.c_int, [_vp, _vp, _i64, _i32, _i32, _i32, _i32, _i32, _vp, _i64, _P(_i64)]),
     "pkv_paged_attention": (C.c_int, [_P(AttentionArgs), _vp]),
     "pkv_decode_step": (C.c_int, [_P(StepStageArgs), _P(AttentionArgs), _P(DecodeIO), _vp]),

@@ -966,6 +966,8 @@ int pkv_paged_attention(const pkv_attention_args* a, void* stream_) {
   return PKV_OK;
 }
 
+static void plan_speculate(const int32_t* nk, const int32_t* row, int64_t n, int32_t ps, int32_t hq, int32_t hkv);
+
 int pkv_decode_step(pkv_step_stage_args* stage, pkv_attention_args* attn, pkv_decode_io* io, void* stream_) {
   if (!stage || !attn) return pkv::fail(PKV_VALUE_ERROR, "null args");
   cudaStream_t stream = static_cast<cudaStream_t>(stream_);
@@ -1015,6 +1017,8 @@ int pkv_decode_step(pkv_step_stage_args* stage, pkv_attention_args* attn, pkv_de
     }
     io->launched = 1;
   }
+  // the next step's plan, computed while the GPU runs this one
+  if (tensor) plan_speculate(stage->meta_host + n, stage->meta_host + 2 * n, n, attn->page_size, attn->hq, attn->hkv);
   return PKV_OK;
 }
 
@@ -1024,9 +1028,77 @@ extern "C" int64_t pkv_attention_plan_ints(int64_t n_queries, int32_t hq) {
   return pkv::decode_plan_ints(n_queries, hq);
 }
 
+// Plan memo (host, per thread): the decode plan is a pure function of its
+// inputs, and a serving loop asks for the plan of (key counts + 1) right after
+// launching the current step.  pkv_decode_step computes that next plan while
+// the GPU runs the current one (plan_speculate); the next prepare finds it here
+// and copies it instead of recomputing, taking the planner off the critical path.
+namespace {
+struct PlanMemo {
+  std::vector<int32_t> key, plan;
+};
+thread_local PlanMemo t_memo;
+thread_local std::vector<int32_t> t_key;
+
+void plan_key(std::vector<int32_t>& k, const int32_t* nk, const int32_t* row, int64_t n, int32_t ps,
+              int32_t hq, int32_t hkv, int32_t sms, int32_t waves, int32_t bump) {
+  k.resize(static_cast<size_t>(2 * n + 6));
+  k[0] = static_cast<int32_t>(n);
+  k[1] = ps;
+  k[2] = hq;
+  k[3] = hkv;
+  k[4] = sms;
+  k[5] = waves;
+  for (int64_t i = 0; i < n; ++i) {
+    k[6 + i] = nk[i] + bump;
+    k[6 + n + i] = row[i];
+  }
+}
+}  // namespace
+
+static int resolve_sms(int32_t num_sms) {
+  if (num_sms > 0) return num_sms;
+  if (!g_num_sms) {
+    int32_t n = 0;
+    pkv_device_sm_count(&n);
+    g_num_sms = n > 0 ? n : 148;
+  }
+  return g_num_sms;
+}
+
+// compute and memoise the plan of the next decode step (every key count + 1)
+static void plan_speculate(const int32_t* nk, const int32_t* row, int64_t n, int32_t ps, int32_t hq,
+                           int32_t hkv) {
+  const int sms = resolve_sms(0);
+  PlanMemo& m = t_memo;
+  plan_key(m.key, nk, row, n, ps, hq, hkv, sms, 0, 1);
+  m.plan.resize(static_cast<size_t>(pkv::decode_plan_ints(n, hq)));
+  std::vector<int32_t> nk1(m.key.begin() + 6, m.key.begin() + 6 + n);
+  int64_t used = 0;
+  if (pkv::plan_decode(nk1.data(), row, n, ps, hq, hkv, sms, 0, m.plan.data(),
+                       static_cast<int64_t>(m.plan.size()), &used) != PKV_OK) {
+    m.key.clear();
+    return;
+  }
+  m.plan.resize(static_cast<size_t>(used));
+}
+
+extern "C" void pkv_plan_memo_reset(void) {
+  t_memo.key.clear();
+  t_memo.plan.clear();
+}
+
 extern "C" int pkv_attention_plan(const int32_t* q_nkeys, const int32_t* q_row, int64_t n_queries,
                                   int32_t page_size, int32_t hq, int32_t hkv, int32_t num_sms,
                                   int32_t target_waves, int32_t* plan_out, int64_t cap, int64_t* n_out) {
+  if (n_queries > 0 && hq > 0 && hkv > 0 && !t_memo.key.empty()) {
+    plan_key(t_key, q_nkeys, q_row, n_queries, page_size, hq, hkv, resolve_sms(num_sms), target_waves, 0);
+    if (t_key == t_memo.key && cap >= static_cast<int64_t>(t_memo.plan.size())) {
+      std::copy(t_memo.plan.begin(), t_memo.plan.end(), plan_out);
+      if (n_out) *n_out = static_cast<int64_t>(t_memo.plan.size());
+      return PKV_OK;
+    }
+  }
   if (n_queries <= 0) return pkv::fail(PKV_VALUE_ERROR, "no queries");
   if (hq <= 0 || hkv <= 0 || hq % hkv) return pkv::fail(PKV_SHAPE_MISMATCH, "bad head counts");
   if (page_size <= 0 || (page_size & (page_size - 1)))

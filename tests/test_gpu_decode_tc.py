@@ -404,3 +404,36 @@ def test_cluster_mode_dsmem_merge(lengths):
     ref = dense_ref(q, keys, vals, lengths, lengths, hq // hkv, cfg.scale)
     assert relative_error(as_numpy(out), ref.cpu().numpy()) <= 6e-3
     assert torch.equal(out, paged_attention(q, store, meta, cfg))  # deterministic
+
+
+def test_speculative_plan_equals_a_fresh_plan():
+    """pkv_decode_step plans the next step while the GPU runs this one; the
+    memoised plan the next prepare uses must equal a freshly computed one."""
+    import threading
+
+    from paper_2506_07311_b200 import _lib
+
+    lengths = [37, 700, 1500, 16, 260]
+    hq, hkv, d, ps = 32, 8, 128, 16
+    pool, store, _, _ = build(lengths, hkv, d, ps, torch.bfloat16)
+    cfg = AttentionConfig(head_count=hq, head_dim=d, page_size=ps, kv_head_count=hkv)
+    batch = DecodeBatch(store, list(range(len(lengths))), cfg, capacity=8)
+    lib = _lib.load()
+    B = len(lengths)
+    for step in range(4):
+        q = torch.randn((B, hq, d), device="cuda").bfloat16()
+        kn = torch.randn((B, hkv, d), device="cuda").bfloat16()
+        batch.step(q, kn, kn)
+        torch.cuda.synchronize()
+        host = batch._ring[batch._cur][0].numpy()
+        nk = host[B:2 * B].copy()
+        rows = host[2 * B:3 * B].copy()
+        used = batch._stage.meta_used
+        # the memo is per host thread: a fresh thread recomputes from scratch
+        res = {}
+        t = threading.Thread(target=lambda: res.setdefault("p", _lib.attention_plan(nk, rows, ps, hq, hkv, 0)))
+        t.start()
+        t.join()
+        assert np.array_equal(host[3 * B:used], res["p"]), step
+        assert np.array_equal(nk, np.asarray([n + step + 1 for n in lengths], dtype=np.int32))
+    lib.pkv_plan_memo_reset()
