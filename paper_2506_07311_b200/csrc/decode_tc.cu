@@ -922,6 +922,10 @@ int plan_decode(const int32_t* nk, const int32_t* row, int64_t nq, int page_size
             int64_t fit = static_cast<int64_t>(room + 0.5);
             if (fit < min_piece) fit = 0;               // too small: start in the next CTA
             if (take - fit < min_piece) fit = take;     // remainder too small: keep it here
+            // a fresh CTA always takes something (else a capacity below
+            // ovh + min_piece would open empty CTAs forever)
+            if (fit == 0 && used == 0.0) fit = std::min<int64_t>(take, min_piece);
+            if (take - fit < min_piece) fit = take;
             take = fit;
           }
           if (take > 0) {
@@ -957,7 +961,8 @@ int plan_decode(const int32_t* nk, const int32_t* row, int64_t nq, int page_size
   };
   // the optimum sits just above the even split line/grid: start with a tight
   // bracket and widen only if it is infeasible (halves the fill passes)
-  double lo = double(line) / grid, hi = lo * 1.04 + double(ovh + min_piece) * 2.0;
+  double lo = std::max(double(line) / grid, double(ovh + min_piece) - 0.5);
+  double hi = lo * 1.04 + double(ovh + min_piece) * 2.0;
   for (int64_t g2 = fill(hi, false); g2 > grid; g2 = fill(hi, false)) {
     lo = hi;
     hi *= 1.5;
