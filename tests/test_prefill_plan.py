@@ -69,3 +69,31 @@ def test_supported_shapes():
     assert not lib.pkv_prefill_supported(8, 8, 96, 16, _lib.PKV_BF16)
     assert not lib.pkv_prefill_supported(8, 8, 128, 4, _lib.PKV_BF16)
     assert not lib.pkv_prefill_supported(8, 8, 128, 16, _lib.PKV_F32)
+
+
+@pytest.mark.timeout(300, method="thread")
+def test_prefill_plan_fuzz_covers_every_query_once():
+    """Random suffix metas (GQA groups 1-16, causal or not): every (query,
+    kv head) lands in exactly one item half, tile counts follow the mask."""
+    rng = np.random.default_rng(5)
+    for _ in range(200):
+        hkv = int(rng.choice([1, 2, 4, 8]))
+        g = int(rng.choice([1, 2, 4, 8, 16]))
+        causal = bool(rng.integers(2))
+        n = int(rng.integers(1, 9))
+        lens = np.maximum(1, np.exp(rng.uniform(0, np.log(6000), n))).astype(np.int32)
+        ql = np.asarray([int(rng.integers(1, x + 1)) for x in lens], dtype=np.int32)
+        qs = np.concatenate([[0], np.cumsum(ql)[:-1]]).astype(np.int64)
+        rows = rng.permutation(n).astype(np.int32)
+        plan = _lib.prefill_plan(qs, ql, lens, rows, hkv * g, hkv, causal=causal)
+        qt = 128 // g
+        cover = np.zeros((int(ql.sum()), hkv), dtype=np.int64)
+        for q_row0, cnt_a, cnt_b, pos0, kv_len, row, kvh, tiles_a, tiles_b, _ in plan:
+            s = int(np.searchsorted(qs, q_row0, side="right") - 1)
+            assert kv_len == lens[s] and row == rows[s]
+            for t, (cnt, tiles) in enumerate(((cnt_a, tiles_a), (cnt_b, tiles_b))):
+                cover[q_row0 + t * qt:q_row0 + t * qt + cnt, kvh] += 1
+                if cnt:
+                    keys = min(pos0 + t * qt + cnt, kv_len) if causal else kv_len
+                    assert tiles == -(-keys // 128)
+        assert (cover == 1).all()
