@@ -358,7 +358,8 @@ def run_e2e(args, pool, store, cfg, lengths, device, flush, world):
         torch.cuda.synchronize(device)
         t0 = time.perf_counter()
         # one native call: H2D q/k/v, allocator + plan, fused append +
-        # decode, D2H of the output (pkv_decode_step)
+        # decode (pkv_decode_step); the result crosses PCIe into the pinned
+        # host output (stored by the kernel through the mapped pointer)
         batch.step(q, k, v, out=out_host)
         torch.cuda.current_stream(device).synchronize()
         dt = time.perf_counter() - t0

