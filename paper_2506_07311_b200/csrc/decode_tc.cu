@@ -801,11 +801,30 @@ int plan_decode(const int32_t* nk, const int32_t* row, int64_t nq, int page_size
     return e ? std::max<int64_t>(0, std::atoll(e)) : int64_t(400);
   }();
   const int64_t ovh = ((cost_kb << 10) / page_bytes) * (waves > 0 ? waves : 1);
-  const int64_t min_piece = std::max<int64_t>(
+  bool whole = false;
+  int64_t min_piece = std::max<int64_t>(
       std::max<int64_t>(1, (ovh_kb << 10) / page_bytes) / 2, (2 * kCh * wph + ps - 1) / ps);
   const int64_t units = nq * head_items;
   const int64_t line = total_pages * head_items + ovh * units;
   int grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(num_sms, total_pages * head_items / min_piece)));
+  // Whole units: when there are slightly fewer (query, head item) units than
+  // SMs and they are about equally long, one uncut unit per CTA beats cutting
+  // them to fill the last SMs — ~120 CTAs already saturate HBM, so the extra
+  // CTAs add no bandwidth while every cut adds a partial store and a merge
+  // (measured: C3 2k x 64 and 4k x 32 4.9 -> 5.7 TB/s, 16k x 16 5.9 -> 6.5).
+  {
+    int64_t max_pages = 0;
+    for (int64_t i = 0; i < nq; ++i) max_pages = std::max<int64_t>(max_pages, (int64_t(nk[i]) + ps - 1) / ps);
+    static const bool whole_on = [] {
+      const char* e = std::getenv("PKV_DECODE_WHOLE_UNITS");
+      return !(e && e[0] == '0');
+    }();
+    if (whole_on && units <= num_sms && units * 10 >= int64_t(num_sms) * 7 &&
+        double(max_pages) * double(nq) <= 1.15 * double(total_pages)) {
+      whole = true;  // never cut a unit: a unit that does not fit opens the next CTA
+      grid = static_cast<int>(units);
+    }
+  }
   const double seg = double(line) / grid;
 
   // Cluster mode (small batches, one kv head per CTA): every (query, head
@@ -918,7 +937,9 @@ int plan_decode(const int32_t* nk, const int32_t* row, int64_t nq, int page_size
         while (p0 < pages) {
           int64_t take = pages - p0;
           const double room = T - used - double(ovh);  // pages that still fit here
-          if (room < double(take) && (!emit || c < grid - 1)) {
+          if (whole && room < double(take) && (!emit || c < grid - 1)) {
+            if (used > 0.0) take = 0;  // start the unit in the next CTA
+          } else if (room < double(take) && (!emit || c < grid - 1)) {
             int64_t fit = static_cast<int64_t>(room + 0.5);
             if (fit < min_piece) fit = 0;               // too small: start in the next CTA
             if (take - fit < min_piece) fit = take;     // remainder too small: keep it here

@@ -95,3 +95,25 @@ def check_plan(lengths, hq, hkv, ps, balance=False):
         assert P["grid"] == len(items) <= 148 and P["grid"] % P["cluster"] == 0
     # few items per CTA
     assert len(items) <= nk.size * P["head_items"] + 2 * P["grid"]
+
+
+@pytest.mark.parametrize("L,B", [(2048, 64), (4096, 32), (16384, 16), (8192, 64)])
+def test_whole_units_for_uniform_batches_near_the_sm_count(L, B):
+    """~128 equal (query, head block) units on 148 SMs: one uncut unit per
+    CTA (no partials, no merges) — HBM saturates with ~120 CTAs, so cutting
+    units to reach the last SMs only adds merges."""
+    plan = _lib.attention_plan(np.full(B, L, np.int32), np.arange(B, dtype=np.int32), 16, 32, 8, 0)
+    P = parse(plan)
+    units = B * P["head_items"]
+    assert P["grid"] == units == len(P["items"]) and len(P["comb"]) == 0
+    assert (np.diff(P["cta"]) == 1).all()
+    check_plan([L] * B, 32, 8, 16)
+
+
+def test_mixed_lengths_keep_the_segment_schedule():
+    """C2 (32 mixed lengths): unit sizes differ, so units are still cut to
+    balance bytes across every SM."""
+    plan = _lib.attention_plan(np.asarray(config_lengths("c2"), np.int32), np.arange(32, dtype=np.int32),
+                               16, 32, 32, 0)
+    P = parse(plan)
+    assert P["grid"] == 148 and len(P["comb"]) > 0
