@@ -1,6 +1,9 @@
-"""Batched decode step — B sequences advance one token through one
-allocator call, one metadata upload and one decode launch (+ the split
-combine when a sequence is split).
+"""Batched decode step — B sequences advance one token in ONE native call
+(pkv_decode_step): host→device copies of CPU inputs, the allocator step,
+the packed metadata + work plan upload, one aux kernel for page clears /
+copies / block-table edits (only when pages are granted), and the decode
+launch with the K1 append fused in; a pinned host output is written by the
+kernel itself.  The next step's plan is computed while the GPU runs.
 
 This is the serving-loop form of the reference's per-session
 `DecodeSession.step` (decoder.py:263-284): grow -> assign at `logical_len`

@@ -23,9 +23,13 @@
 // SM, so every CTA streams the same bytes and runs only ~units/SMs + 1 items;
 // a unit cut between CTAs is merged by the last of its pieces to finish
 // (arrival counters in the per-call plan upload, self-resetting), in page
-// order — deterministic.  Small batches use cluster mode instead: each unit
-// gets a thread-block cluster whose CTAs split its pages and merge through
-// distributed shared memory.  Every warp runs a producer that streams its
+// order — deterministic.  About 128 of the 148 CTAs already saturate HBM, so
+// with more units than SMs the line is cut into 128 segments, and a uniform
+// batch of 70-100% as many units as SMs runs one uncut unit per CTA (no
+// partials, no merges).  Small batches use cluster mode instead: each unit
+// gets a thread-block cluster whose CTAs split its pages, push their partials
+// into the owning peer's shared memory and merge there (DSMEM, one cluster
+// barrier).  Every warp runs a producer that streams its
 // chunks through a private 3-stage cp.async ring (16-byte XOR swizzle ->
 // conflict-free LDSM; zero-fill past the valid keys) straight across item
 // boundaries.  The G grouped query heads are the M rows of the MMA, so every
