@@ -437,3 +437,37 @@ def test_speculative_plan_equals_a_fresh_plan():
         assert np.array_equal(host[3 * B:used], res["p"]), step
         assert np.array_equal(nk, np.asarray([n + step + 1 for n in lengths], dtype=np.int32))
     lib.pkv_plan_memo_reset()
+
+
+@pytest.mark.parametrize("lengths", [[700] * 64, [300] * 32 + [301] * 32,
+                                     list(np.random.default_rng(4).integers(50, 900, 300))])
+def test_whole_unit_and_capped_grid_schedules(lengths):
+    """Uniform batches near the SM count take the whole-unit schedule (one
+    uncut unit per CTA); batches with more units than SMs the capped segment
+    grid.  Both through DecodeBatch (fused append) against float64."""
+    from paper_2506_07311_b200 import _lib
+
+    lengths = [int(x) for x in lengths]
+    hq, hkv, d, ps = 32, 8, 128, 16
+    pool, store, keys, vals = build(lengths, hkv, d, ps, torch.bfloat16, seed=len(lengths), scatter=False)
+    cfg = AttentionConfig(head_count=hq, head_dim=d, page_size=ps, kv_head_count=hkv)
+    B = len(lengths)
+    rows = np.asarray([pool.table(i).mirror_row for i in range(B)], dtype=np.int32)
+    plan = _lib.attention_plan(np.asarray(lengths, np.int32) + 1, rows, ps, hq, hkv, 0)
+    units = B * plan[4]
+    assert plan[8] == (units if units <= 148 else 128)  # H_GRID
+    for i in range(B):  # head room for the appended token
+        pool.grow(i, lengths[i] + 1)
+    batch = DecodeBatch(store, list(range(B)), cfg)
+    q = torch.randn((B, hq, d), device="cuda").bfloat16()
+    kn = torch.randn((B, hkv, d), device="cuda").bfloat16()
+    vn = torch.randn((B, hkv, d), device="cuda").bfloat16()
+    out = batch.step(q, kn, vn)
+    for j in range(0, B, max(1, B // 16)):  # a spread of sequences
+        n = lengths[j]
+        o = sum(lengths[:j])
+        k = torch.cat([keys[o:o + n], kn[j:j + 1]]).double().repeat_interleave(hq // hkv, 1)
+        v = torch.cat([vals[o:o + n], vn[j:j + 1]]).double().repeat_interleave(hq // hkv, 1)
+        p = torch.softmax(torch.einsum("hd,lhd->hl", q[j].double(), k) * cfg.scale, -1)
+        ref = torch.einsum("hl,lhd->hd", p, v)
+        assert relative_error(as_numpy(out[j]), ref.cpu().numpy()) <= 6e-3, j
