@@ -792,6 +792,11 @@ int plan_decode(const int32_t* nk, const int32_t* row, int64_t nq, int page_size
     hb = cand;
     if (units * 2 >= num_sms) break;
   }
+  static const int hb_env = [] {  // experiment knob: force the head block
+    const char* e = std::getenv("PKV_DECODE_HB");
+    return e ? std::atoi(e) : 0;
+  }();
+  if (hb_env > 0 && hkv % hb_env == 0 && kWarpsTc % hb_env == 0) hb = hb_env;
   const int wph = kWarpsTc / hb;
   const int qgs = wph == 1 ? 16 : kMergeRows;
   const int qgroups = (G + qgs - 1) / qgs;
