@@ -310,8 +310,9 @@ def test_multi_layer_decode_batch_prepare_once():
         assert (rows[2:] == 0).all() and (rows[:2] != 0).any(dim=(1, 2)).all()
 
 
-@pytest.mark.parametrize("dtype", [torch.bfloat16, torch.float16])
-def test_host_buffer_step_single_native_call(dtype):
+@pytest.mark.parametrize("dtype,precision", [(torch.bfloat16, "auto"), (torch.float16, "auto"),
+                                             (torch.float16, "exact")])
+def test_host_buffer_step_single_native_call(dtype, precision):
     """DecodeBatch.step with pinned HOST q/k/v and a pinned host `out`: the
     copies, allocator, plan, page work, fused append + decode and the D2H are
     one native call (pkv_decode_step).  Covers page crossings (granted pages
@@ -338,17 +339,19 @@ def test_host_buffer_step_single_native_call(dtype):
         kn = torch.randn((B, hkv, d), generator=gen, device="cuda").to(dtype)
         vn = torch.randn((B, hkv, d), generator=gen, device="cuda").to(dtype)
         if step % 3 == 0:
-            res = batch.step(q.cpu().pin_memory(), kn.cpu().pin_memory(), vn.cpu().pin_memory(), out=out_h)
+            res = batch.step(q.cpu().pin_memory(), kn.cpu().pin_memory(), vn.cpu().pin_memory(), out=out_h,
+                             precision=precision)
             assert res is out_h
             torch.cuda.current_stream().synchronize()
             got = out_h.clone()
         elif step % 3 == 1:
             dev_out = torch.empty((B, hq, d), dtype=torch.float32, device="cuda")
-            res = batch.step(q, kn.cpu().float().numpy(), vn.cpu().float().numpy(), out=dev_out)
+            res = batch.step(q, kn.cpu().float().numpy(), vn.cpu().float().numpy(), out=dev_out,
+                             precision=precision)
             assert res is dev_out
             got = dev_out.cpu()
         else:
-            got = batch.step(q, kn, vn).cpu()
+            got = batch.step(q, kn, vn, precision=precision).cpu()
         assert batch.last_launches >= 1
         for i in range(B):
             ctx[i][0] = torch.cat([ctx[i][0], kn[i:i + 1]])
