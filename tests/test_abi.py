@@ -63,3 +63,24 @@ def test_status_codes_map_to_reference_errors():
     with pytest.raises(ValueError):
         _lib.check(lib.pkv_pool_create(0, 16, ctypes.byref(h)))
     assert b"capacity_pages" in lib.pkv_last_error()
+
+
+def test_pure_c_client_compiles_and_links(tmp_path):
+    """tests/abi_decode.cpp — a client of the C ABI only (no Python, no
+    torch) — compiles against include/pkv200.h and links against
+    libpkv200.so on a CPU host (it runs in the GPU suite)."""
+    import os
+    import shutil
+    import subprocess
+
+    gxx = shutil.which("g++")
+    if gxx is None:
+        pytest.skip("g++ not available")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    lib_dir = os.path.join(root, "paper_2506_07311_b200")
+    exe = str(tmp_path / "abi_decode")
+    r = subprocess.run([gxx, "-O1", "-std=c++17", "-I", os.path.join(root, "include"), "-I", "/usr/local/cuda/include",
+                        os.path.join(root, "tests", "abi_decode.cpp"), "-L", lib_dir, "-lpkv200",
+                        "-L", "/usr/local/cuda/lib64", "-lcudart", f"-Wl,-rpath,{lib_dir}", "-o", exe],
+                       capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr[-3000:]
