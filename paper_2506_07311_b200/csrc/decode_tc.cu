@@ -841,7 +841,11 @@ int plan_decode(const int32_t* nk, const int32_t* row, int64_t nq, int page_size
       const char* e = std::getenv("PKV_DECODE_WHOLE_UNITS");
       return !(e && e[0] == '0');
     }();
-    if (whole_on && units <= num_sms && units * 10 >= int64_t(num_sms) * 7 &&
+    static const int whole_min_pct = [] {  // experiment knob: lowest units / SMs ratio (%)
+      const char* e = std::getenv("PKV_DECODE_WHOLE_MIN_PCT");
+      return e ? std::atoi(e) : 70;
+    }();
+    if (whole_on && units <= num_sms && units * 100 >= int64_t(num_sms) * whole_min_pct &&
         double(max_pages) * double(nq) <= 1.15 * double(total_pages)) {
       whole = true;  // never cut a unit: a unit that does not fit opens the next CTA
       grid = static_cast<int>(units);
