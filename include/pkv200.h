@@ -375,6 +375,15 @@ int pkv_device_sm_count(int32_t* out);
  * Synchronous. */
 int pkv_debug_trace(int32_t enable, uint64_t* out, int64_t n);
 
+/* Debug: make the next decode step fail at `site` (one shot; 0 disarms):
+ * PKV_FAIL_STEP_UPLOAD = the metadata upload of pkv_decode_step_stage,
+ * PKV_FAIL_STEP_LAUNCH = the attention launch of pkv_decode_step.  The step
+ * returns PKV_CUDA_ERROR and the allocator is rolled back (tests of the
+ * all-or-nothing contract, pool.py:143-148, 165-169). */
+#define PKV_FAIL_STEP_UPLOAD 1
+#define PKV_FAIL_STEP_LAUNCH 2
+int pkv_debug_inject_failure(int32_t site);
+
 #ifdef __cplusplus
 }
 #endif

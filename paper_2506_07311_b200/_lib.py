@@ -134,7 +134,10 @@ SIGNATURES = {
     "pkv_paged_prefill": (C.c_int, [_P(PrefillArgs), _vp]),
     "pkv_device_sm_count": (C.c_int, [_P(_i32)]),
     "pkv_debug_trace": (C.c_int, [_i32, _P(_u64), _i64]),
+    "pkv_debug_inject_failure": (C.c_int, [_i32]),
 }
+
+PKV_FAIL_STEP_UPLOAD, PKV_FAIL_STEP_LAUNCH = 1, 2
 
 _lib = None
 

@@ -29,7 +29,7 @@ import numpy as np
 
 from . import _lib
 from .errors import ConfigError, NoAllowedKeys, OutOfRange, ShapeMismatch
-from .store import BatchView, KvStore, _ptr, _stream, stage_upload, to_device, torch_dtype
+from .store import BatchView, KvStore, _ptr, _stream, on_device, stage_upload, to_device, torch_dtype
 
 
 class BlockKind(IntEnum):
@@ -245,6 +245,7 @@ def _q_tensor(queries, device):
 PRECISION_MODES = {"auto": 0, "exact": 1, "tensor": 2, "prefill": 2}
 
 
+@on_device(lambda *a, **k: k.get("device"))
 def _launch_attention(q, qcode, meta, config, nkeys, *, k, v, kv_code, bt, bt_stride, seq_row,
                       seq_start, out_dtype, device, precision="auto"):
     import torch
@@ -330,6 +331,7 @@ def _prefill_route(meta, config, kv_code, precision):
     return runs if runs[1].max(initial=0) >= PREFILL_MIN_RUN else None
 
 
+@on_device(lambda *a, **k: k.get("device"))
 def _launch_prefill(q, meta, config, runs, *, k, v, kv_code, bt, rows, out_dtype, device, prof=None):
     """K3: one tcgen05 launch over every sequence's query run.  Paged mode:
     `bt` is the device block-table mirror and `rows` the mirror row of each
@@ -364,6 +366,7 @@ def _launch_prefill(q, meta, config, runs, *, k, v, kv_code, bt, rows, out_dtype
     return out
 
 
+@on_device(lambda queries, store, *a, **k: store.device)
 def paged_attention(queries, store: KvStore, meta: MaskMeta, config: AttentionConfig, *,
                     stats: KernelStats | None = None, block_mask: BlockMask | None = None,
                     skip_empty: bool = True, out_dtype=None, precision: str = "auto"):

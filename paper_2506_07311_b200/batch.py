@@ -22,7 +22,7 @@ import numpy as np
 
 from . import _lib
 from .attention import PRECISION_MODES, AttentionConfig, _Workspace, _q_tensor
-from .store import KvStore, _stream, torch_dtype
+from .store import KvStore, _self_device, _stream, on_device, torch_dtype
 from .errors import ShapeMismatch
 
 import os as _os
@@ -177,6 +177,7 @@ class DecodeBatch:
         self._used.value = a.meta_used
         return launches
 
+    @on_device(_self_device)
     def prepare(self, _sp=None) -> int:
         """Host work of one token step in one native call
         (pkv_decode_step_stage): allocator bookkeeping (grow, copy-on-write,
@@ -227,6 +228,7 @@ class DecodeBatch:
             x = x.to(device=self.device, dtype=dtype, non_blocking=True).contiguous()
         return x, None, 0
 
+    @on_device(_self_device)
     def step(self, queries, k_new, v_new, *, out=None, out_dtype=None, layer: int = 0, advance: bool = True,
              precision: str = "auto"):
         """Append one token per sequence into `stores[layer]` and attend.

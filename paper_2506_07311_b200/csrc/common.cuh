@@ -21,6 +21,28 @@ namespace pkv {
 
 inline int elem_bytes(int dt) { return dt == PKV_F32 ? 4 : 2; }
 
+// Launch on the stream's device: entry points may be called while another
+// device is current (a store on cuda:1 driven from a thread whose current
+// device is cuda:0).  The legacy null stream has no device of its own and
+// keeps the current one.  Restores the caller's device on exit.
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(cudaStream_t s) {
+    if (!s) return;
+    int dev = 0, cur = 0;
+    if (cudaStreamGetDevice(s, &dev) != cudaSuccess || cudaGetDevice(&cur) != cudaSuccess) {
+      cudaGetLastError();
+      return;
+    }
+    if (dev != cur && cudaSetDevice(dev) == cudaSuccess) prev = cur;
+  }
+  ~DeviceGuard() {
+    if (prev >= 0) cudaSetDevice(prev);
+  }
+  DeviceGuard(const DeviceGuard&) = delete;
+  DeviceGuard& operator=(const DeviceGuard&) = delete;
+};
+
 // ---------------------------------------------------------------------------
 // small device helpers
 // ---------------------------------------------------------------------------

@@ -32,6 +32,7 @@
 #include <cstring>
 
 #include "common.cuh"
+#include "pool_internal.h"
 #include "decode_tc.h"
 #include "pkv200.h"
 #include "status.h"
@@ -615,6 +616,7 @@ int pkv_device_sm_count(int32_t* out) {
 
 int pkv_mirror_apply(int32_t* table, const int32_t* pairs, int64_t n_pairs, void* stream) {
   if (n_pairs <= 0) return PKV_OK;
+  pkv::DeviceGuard guard(static_cast<cudaStream_t>(stream));
   const int threads = 256;
   const int64_t blocks = (n_pairs + threads - 1) / threads;
   mirror_apply_kernel<<<static_cast<unsigned>(blocks < 4096 ? blocks : 4096), threads, 0,
@@ -626,6 +628,7 @@ int pkv_mirror_apply(int32_t* table, const int32_t* pairs, int64_t n_pairs, void
 int pkv_page_zero(void* k_cache, void* v_cache, const int32_t* pages, int64_t n,
                   int64_t page_bytes, void* stream) {
   if (n <= 0) return PKV_OK;
+  pkv::DeviceGuard guard(static_cast<cudaStream_t>(stream));
   if (page_bytes & 1) return pkv::fail(PKV_CONFIG_ERROR, "page bytes must be even");
   page_zero_kernel<<<static_cast<unsigned>(n < 65535 ? n : 65535), 256, 0,
                      static_cast<cudaStream_t>(stream)>>>(static_cast<char*>(k_cache),
@@ -638,6 +641,7 @@ int pkv_page_zero(void* k_cache, void* v_cache, const int32_t* pages, int64_t n,
 int pkv_page_copy(void* k_cache, void* v_cache, const int32_t* triples, int64_t n,
                   int64_t row_bytes, int32_t page_size, void* stream) {
   if (n <= 0) return PKV_OK;
+  pkv::DeviceGuard guard(static_cast<cudaStream_t>(stream));
   if (row_bytes & 1) return pkv::fail(PKV_CONFIG_ERROR, "row bytes must be even");
   page_copy_kernel<<<static_cast<unsigned>(n < 65535 ? n : 65535), 256, 0,
                      static_cast<cudaStream_t>(stream)>>>(static_cast<char*>(k_cache),
@@ -652,6 +656,7 @@ int pkv_kv_append(const void* k_new, const void* v_new, int64_t n_tok, const int
                   int64_t bt_stride, int32_t page_size, void* k_cache, void* v_cache,
                   int64_t row_bytes, void* stream) {
   if (n_tok <= 0) return PKV_OK;
+  pkv::DeviceGuard guard(static_cast<cudaStream_t>(stream));
   if (page_size <= 0 || (page_size & (page_size - 1)))
     return pkv::fail(PKV_VALUE_ERROR, "page_size must be a power of two");
   if (row_bytes & 1) return pkv::fail(PKV_CONFIG_ERROR, "row bytes must be even");
@@ -673,10 +678,16 @@ int64_t pkv_attention_workspace_bytes(int64_t n_queries, int32_t hq, int32_t hea
   return up(plan) + up(4 * splits * hq * 2) + up(4 * splits * hq * head_dim);
 }
 
-int pkv_decode_step_prepare(pkv_pool* pool, const int64_t* seqs, int64_t n, int32_t page_size,
-                            int32_t hq, int32_t hkv, int32_t* meta, int64_t meta_cap,
-                            int64_t* meta_used, uint32_t* pages_out, int64_t pages_cap,
-                            int64_t* n_pages_out, int64_t* copies_out) {
+}  // extern "C"
+
+// The allocator half of a decode step plus its metadata; on success *undo
+// holds the allocator's undo record (the caller commits or rolls it back),
+// on failure the allocator is unchanged.
+static int decode_step_prepare(pkv_pool* pool, const int64_t* seqs, int64_t n, int32_t page_size,
+                               int32_t hq, int32_t hkv, int32_t* meta, int64_t meta_cap,
+                               int64_t* meta_used, uint32_t* pages_out, int64_t pages_cap,
+                               int64_t* n_pages_out, int64_t* copies_out, pkv_append_undo** undo) {
+  *undo = nullptr;
   if (n <= 0) return pkv::fail(PKV_VALUE_ERROR, "no sequences");
   if (meta_cap < 3 * n + pkv_attention_plan_ints(n, hq))
     return pkv::fail(PKV_VALUE_ERROR, "metadata buffer too small");
@@ -684,8 +695,8 @@ int pkv_decode_step_prepare(pkv_pool* pool, const int64_t* seqs, int64_t n, int3
   int32_t* nkeys = meta + n;
   int32_t* rows = meta + 2 * n;
   // positions land in nkeys[] and become key counts (the appended token is attended)
-  int st = pkv_pool_prepare_append(pool, seqs, n, nkeys, rows, pages_out, pages_cap, n_pages_out,
-                                   copies_out);
+  int st = pkv_pool_prepare_append_undo(pool, seqs, n, nkeys, rows, pages_out, pages_cap, n_pages_out,
+                                        copies_out, undo);
   if (st) return st;
   for (int64_t i = 0; i < n; ++i) {
     q_seq[i] = static_cast<int32_t>(i);
@@ -694,9 +705,24 @@ int pkv_decode_step_prepare(pkv_pool* pool, const int64_t* seqs, int64_t n, int3
   int64_t used = 0;
   st = pkv_attention_plan(nkeys, rows, n, page_size, hq, hkv, 0, 0, meta + 3 * n,
                           meta_cap - 3 * n, &used);
-  if (st) return st;
+  if (st) {
+    pkv_pool_rollback_append(pool, *undo);
+    *undo = nullptr;
+    return st;
+  }
   *meta_used = 3 * n + used;
   return PKV_OK;
+}
+
+extern "C" int pkv_decode_step_prepare(pkv_pool* pool, const int64_t* seqs, int64_t n, int32_t page_size,
+                                       int32_t hq, int32_t hkv, int32_t* meta, int64_t meta_cap,
+                                       int64_t* meta_used, uint32_t* pages_out, int64_t pages_cap,
+                                       int64_t* n_pages_out, int64_t* copies_out) {
+  pkv_append_undo* undo = nullptr;
+  const int st = decode_step_prepare(pool, seqs, n, page_size, hq, hkv, meta, meta_cap, meta_used, pages_out,
+                                     pages_cap, n_pages_out, copies_out, &undo);
+  pkv_pool_release_undo(undo);
+  return st;
 }
 
 // side blocks behind the plan: granted pages, copy triples, mirror pairs, the
@@ -704,13 +730,25 @@ int pkv_decode_step_prepare(pkv_pool* pool, const int64_t* seqs, int64_t n, int3
 constexpr int64_t kMaxStageStores = 256;
 static int64_t stage_extra(int64_t n) { return 24 * n + 4 * kMaxStageStores + 64; }
 
-int64_t pkv_decode_step_stage_ints(int64_t n, int32_t hq) {
+extern "C" int64_t pkv_decode_step_stage_ints(int64_t n, int32_t hq) {
   return 3 * n + pkv_attention_plan_ints(n, hq) + stage_extra(n);
 }
 
-int pkv_decode_step_stage(pkv_step_stage_args* a, void* stream_) {
+static int decode_step_stage(pkv_step_stage_args* a, cudaStream_t stream, pkv_append_undo** undo);
+
+extern "C" int pkv_decode_step_stage(pkv_step_stage_args* a, void* stream_) {
+  pkv::DeviceGuard guard(static_cast<cudaStream_t>(stream_));
+  pkv_append_undo* undo = nullptr;
+  const int st = decode_step_stage(a, static_cast<cudaStream_t>(stream_), &undo);
+  pkv_pool_release_undo(undo);
+  return st;
+}
+
+// On failure the allocator is rolled back (the reference's all-or-nothing
+// contract: pool.py:143-148, 165-169); on success *undo is the caller's.
+static int decode_step_stage(pkv_step_stage_args* a, cudaStream_t stream, pkv_append_undo** undo) {
+  *undo = nullptr;
   if (!a || !a->pool) return pkv::fail(PKV_VALUE_ERROR, "null args");
-  cudaStream_t stream = static_cast<cudaStream_t>(stream_);
   a->meta_used = 0;
   a->needs_resync = 0;
   a->launches = 0;
@@ -728,10 +766,16 @@ int pkv_decode_step_stage(pkv_step_stage_args* a, void* stream_) {
   std::vector<uint32_t> pages(2 * n + 1);
   std::vector<int64_t> copies(2 * n);
   int64_t n_pages = 0, used = 0;
-  int st = pkv_decode_step_prepare(a->pool, a->seqs, n, a->page_size, a->hq, a->hkv, a->meta_host,
-                                   a->meta_cap - extra, &used, pages.data(), static_cast<int64_t>(pages.size()),
-                                   &n_pages, copies.data());
+  int st = decode_step_prepare(a->pool, a->seqs, n, a->page_size, a->hq, a->hkv, a->meta_host,
+                               a->meta_cap - extra, &used, pages.data(), static_cast<int64_t>(pages.size()),
+                               &n_pages, copies.data(), undo);
   if (st) return st;
+  // from here on a failure restores the allocator before returning
+  auto fail_back = [&](int code) {
+    pkv_pool_rollback_append(a->pool, *undo);
+    *undo = nullptr;
+    return code;
+  };
   // 2) side blocks behind it: granted pages | copy triples | mirror pairs |
   //    zero list (granted minus copy destinations) | cache pointers
   int32_t* side = a->meta_host + used;
@@ -782,20 +826,24 @@ int pkv_decode_step_stage(pkv_step_stage_args* a, void* stream_) {
   }
   // 3) one upload of everything, then ONE page / mirror kernel
   const int64_t total = used + off;
-  if (total > a->meta_cap) return pkv::fail(PKV_VALUE_ERROR, "metadata slot too small");
+  if (total > a->meta_cap) return fail_back(pkv::fail(PKV_VALUE_ERROR, "metadata slot too small"));
+  if (page_work && (a->row_bytes & 1)) return fail_back(pkv::fail(PKV_CONFIG_ERROR, "row bytes must be even"));
+  if (pkv_debug_should_fail(PKV_FAIL_STEP_UPLOAD))
+    return fail_back(pkv::fail(PKV_CUDA_ERROR, "step metadata upload: injected failure"));
   cudaError_t e = cudaMemcpyAsync(a->meta_dev, a->meta_host, static_cast<size_t>(total) * 4,
                                   cudaMemcpyHostToDevice, stream);
-  if (e != cudaSuccess) return pkv::fail(PKV_CUDA_ERROR, "step metadata upload: %s", cudaGetErrorString(e));
+  if (e != cudaSuccess)
+    return fail_back(pkv::fail(PKV_CUDA_ERROR, "step metadata upload: %s", cudaGetErrorString(e)));
   if (a->slot_event) cudaEventRecord(static_cast<cudaEvent_t>(a->slot_event), stream);
   if (page_work || n_pairs) {
-    if (a->row_bytes & 1) return pkv::fail(PKV_CONFIG_ERROR, "row bytes must be even");
     const int n_st = page_work ? a->n_stores : 0;
     const int64_t blocks = std::max<int64_t>(n_st * (n_zero + n_copies), (n_pairs + 255) / 256);
     step_aux_kernel<<<static_cast<unsigned>(std::min<int64_t>(std::max<int64_t>(blocks, 1), 65535)), 256, 0,
                       stream>>>(reinterpret_cast<const uint64_t*>(a->meta_dev + ptr_off), n_st,
                                 a->meta_dev + zero_off, n_zero, a->meta_dev + trip_off, n_copies,
                                 a->mirror_dev, a->meta_dev + pairs_off, n_pairs, a->row_bytes, a->page_size);
-    PKV_CHECK_LAUNCH();
+    const cudaError_t le = cudaGetLastError();
+    if (le != cudaSuccess) return fail_back(pkv::fail(PKV_CUDA_ERROR, "step aux kernel: %s", cudaGetErrorString(le)));
     ++a->launches;
   }
   a->meta_used = used;
@@ -806,9 +854,12 @@ int pkv_decode_step_stage(pkv_step_stage_args* a, void* stream_) {
   return PKV_OK;
 }
 
+extern "C" {
+
 int pkv_paged_attention(const pkv_attention_args* a, void* stream_) {
   if (!a) return pkv::fail(PKV_VALUE_ERROR, "null args");
   cudaStream_t stream = static_cast<cudaStream_t>(stream_);
+  pkv::DeviceGuard guard(stream);
   if (a->meta_host && a->meta_bytes > 0) {  // stage the packed metadata (pinned host -> device)
     if (!a->meta_dev) return pkv::fail(PKV_VALUE_ERROR, "meta_host without meta_dev");
     cudaError_t e = cudaMemcpyAsync(a->meta_dev, a->meta_host, static_cast<size_t>(a->meta_bytes),
@@ -971,6 +1022,7 @@ static void plan_speculate(const int32_t* nk, const int32_t* row, int64_t n, int
 int pkv_decode_step(pkv_step_stage_args* stage, pkv_attention_args* attn, pkv_decode_io* io, void* stream_) {
   if (!stage || !attn) return pkv::fail(PKV_VALUE_ERROR, "null args");
   cudaStream_t stream = static_cast<cudaStream_t>(stream_);
+  pkv::DeviceGuard guard(stream);
   if (io) io->launched = io->launches = 0;
   // the input copies go first so they overlap the host-side allocator / plan
   auto h2d = [&](const void* src, const void* dst, int64_t bytes, const char* what) -> int {
@@ -986,10 +1038,16 @@ int pkv_decode_step(pkv_step_stage_args* stage, pkv_attention_args* attn, pkv_de
     if (!st) st = h2d(io->v_host, attn->v_new, io->kv_bytes, "v_new");
     if (st) return st;
   }
-  int st = pkv_decode_step_stage(stage, stream_);
+  pkv_append_undo* undo = nullptr;
+  int st = decode_step_stage(stage, stream, &undo);
   if (st) return st;
+  // a failure past the stage puts the allocator back (all-or-nothing step)
+  auto fail_back = [&](int code) {
+    pkv_pool_rollback_append(stage->pool, undo);
+    return code;
+  };
   if (stage->n_stores == 0 && (stage->n_granted || stage->n_copies))
-    return pkv::fail(PKV_VALUE_ERROR, "decode step needs the stores attached for page clears / copies");
+    return fail_back(pkv::fail(PKV_VALUE_ERROR, "decode step needs the stores attached for page clears / copies"));
   if (io) io->launches = stage->launches;
   const int64_t n = stage->n;
   int32_t* md = stage->meta_dev;
@@ -1003,9 +1061,15 @@ int pkv_decode_step(pkv_step_stage_args* stage, pkv_attention_args* attn, pkv_de
   attn->meta_bytes = 0;
   // block-table shape changed: the caller re-exports the mirror, points
   // attn->block_table at it and launches pkv_paged_attention(attn) itself
-  if (stage->needs_resync) return PKV_OK;
+  if (stage->needs_resync) {
+    pkv_pool_release_undo(undo);
+    return PKV_OK;
+  }
+  if (pkv_debug_should_fail(PKV_FAIL_STEP_LAUNCH))
+    return fail_back(pkv::fail(PKV_CUDA_ERROR, "decode launch: injected failure"));
   st = pkv_paged_attention(attn, stream_);
-  if (st) return st;
+  if (st) return fail_back(st);
+  pkv_pool_release_undo(undo);
   const bool tensor = attn->mode == 2 || (attn->mode == 0 && attn->kv_dtype == PKV_BF16);
   if (io) {
     io->launches += tensor ? 1 : 4;

@@ -14,6 +14,7 @@
 #include <algorithm>
 #include <cstdint>
 #include <cstring>
+#include <memory>
 #include <mutex>
 #include <string>
 #include <unordered_map>
@@ -21,6 +22,7 @@
 
 #include "pkv200.h"
 #include "status.h"
+#include "pool_internal.h"
 
 namespace {
 
@@ -372,6 +374,35 @@ int pkv_pool_privatize_blocks(pkv_pool* pool, int64_t seq, const int64_t* blocks
 int pkv_pool_prepare_append(pkv_pool* pool, const int64_t* seqs, int64_t n, int32_t* positions_out,
                             int32_t* rows_out, uint32_t* pages_out, int64_t pages_cap,
                             int64_t* n_pages_out, int64_t* copies_out) {
+  return pkv_pool_prepare_append_undo(pool, seqs, n, positions_out, rows_out, pages_out, pages_cap,
+                                      n_pages_out, copies_out, nullptr);
+}
+
+}  // extern "C"
+
+// Undo record of one pkv_pool_prepare_append: everything phase 2 changed.
+// Phase 2 only pops the free stack / bumps (CoW releases never reach a zero
+// refcount), so restoring the popped tail and the raw bump counter puts the
+// free list back bit-exactly.
+struct pkv_append_undo {
+  std::vector<uint32_t> stack_tail;  // the free-stack tail phase 2 could pop
+  size_t stack_size = 0;
+  uint64_t bump_raw = 0;
+  struct Seq {
+    int64_t handle;
+    int64_t logical_len;
+    size_t n_entries;
+    int64_t cow_block;  // -1: no copy-on-write
+    uint32_t cow_old;
+  };
+  std::vector<Seq> seqs;
+  std::vector<uint32_t> granted;  // refcount 0 -> 1
+};
+
+int pkv_pool_prepare_append_undo(pkv_pool* pool, const int64_t* seqs, int64_t n, int32_t* positions_out,
+                                 int32_t* rows_out, uint32_t* pages_out, int64_t pages_cap,
+                                 int64_t* n_pages_out, int64_t* copies_out, pkv_append_undo** undo_out) {
+  if (undo_out) *undo_out = nullptr;
   LOCK(pool);
   *n_pages_out = 0;
   const int64_t ps = pool->page_size;
@@ -411,11 +442,21 @@ int pkv_pool_prepare_append(pkv_pool* pool, const int64_t* seqs, int64_t n, int3
                      static_cast<long long>(need), static_cast<long long>(avail));
   if (need > pages_cap) return pkv::fail(PKV_VALUE_ERROR, "pages_out too small");
   // phase 2: apply (cannot fail)
+  pkv_append_undo* undo = nullptr;
+  if (undo_out) {
+    undo = new pkv_append_undo;
+    undo->stack_size = pool->free_stack.size();
+    const size_t k = std::min<size_t>(static_cast<size_t>(need), undo->stack_size);
+    undo->stack_tail.assign(pool->free_stack.end() - k, pool->free_stack.end());
+    undo->bump_raw = pool->bump_raw;
+    undo->seqs.reserve(n);
+  }
   int64_t np = 0;
   std::vector<uint32_t> got;
   for (int64_t i = 0; i < n; ++i) {
     Table& t = *tabs[i];
     const int64_t pos = t.logical_len;
+    if (undo) undo->seqs.push_back({seqs[i], pos, t.entries.size(), -1, 0});
     copies_out[2 * i] = copies_out[2 * i + 1] = -1;
     const int64_t grow = pool->pages_for(pos + 1) - static_cast<int64_t>(t.entries.size());
     if (grow > 0) {
@@ -437,15 +478,53 @@ int pkv_pool_prepare_append(pkv_pool* pool, const int64_t* seqs, int64_t n, int3
         pool->release(std::vector<uint32_t>{old}, &dummy);
         copies_out[2 * i] = old;
         copies_out[2 * i + 1] = got[0];
+        if (undo) {
+          undo->seqs.back().cow_block = blk;
+          undo->seqs.back().cow_old = old;
+          undo->granted.push_back(got[0]);
+        }
       }
     }
     positions_out[i] = static_cast<int32_t>(pos);
     rows_out[i] = t.mirror_row;
     t.logical_len = pos + 1;
   }
+  if (undo) undo->granted.insert(undo->granted.end(), pages_out, pages_out + np);
   *n_pages_out = np;
+  if (undo_out) *undo_out = undo;
   return PKV_OK;
 }
+
+int pkv_pool_rollback_append(pkv_pool* pool, pkv_append_undo* undo) {
+  if (!undo) return PKV_OK;
+  std::unique_ptr<pkv_append_undo> hold(undo);
+  LOCK(pool);
+  for (auto it = undo->seqs.rbegin(); it != undo->seqs.rend(); ++it) {
+    Table* t = pool->find(it->handle);
+    if (!t) return pkv::fail(PKV_UNKNOWN_SEQUENCE, "rollback: table %lld vanished", static_cast<long long>(it->handle));
+    if (it->cow_block >= 0) {
+      pool->set_ref(it->cow_old, pool->ref(it->cow_old) + 1);
+      t->entries[it->cow_block] = it->cow_old;
+      pool->mark(*t, it->cow_block);
+    }
+    for (size_t c = it->n_entries; c < t->entries.size(); ++c) {  // clear the grown columns
+      const int64_t flat = t->mirror_row * pool->mcols + static_cast<int64_t>(c);
+      pool->mirror[flat] = 0;
+      if (!pool->full_resync) pool->dirty.push_back(flat);
+    }
+    t->entries.resize(it->n_entries);
+    t->logical_len = it->logical_len;
+  }
+  for (uint32_t p : undo->granted) pool->set_ref(p, 0);
+  pool->free_stack.resize(undo->stack_size - undo->stack_tail.size());
+  pool->free_stack.insert(pool->free_stack.end(), undo->stack_tail.begin(), undo->stack_tail.end());
+  pool->bump_raw = undo->bump_raw;
+  return PKV_OK;
+}
+
+void pkv_pool_release_undo(pkv_append_undo* undo) { delete undo; }
+
+extern "C" {
 
 int pkv_pool_translate(pkv_pool* pool, int64_t seq, int64_t position, uint32_t* page_out,
                        uint32_t* offset_out) {

@@ -685,6 +685,7 @@ extern "C" int pkv_paged_prefill(const pkv_prefill_args* a, void* stream_) {
   pp.items = a->plan;
   pp.dbg = static_cast<unsigned long long*>(a->debug);
   cudaStream_t stream = static_cast<cudaStream_t>(stream_);
+  pkv::DeviceGuard guard(stream);
   if (a->prof_start) cudaEventRecord(static_cast<cudaEvent_t>(a->prof_start), stream);
   int st;
   if (a->kv_dtype == PKV_BF16)

@@ -12,6 +12,7 @@ from __future__ import annotations
 
 import ctypes as C
 import itertools
+import threading
 from dataclasses import dataclass
 
 import numpy as np
@@ -155,6 +156,10 @@ class PagePool:
         self._stores: list = []
         self._mirror = None  # torch int32 [rows, cols] on the stores' device
         self._mq_pending, self._mq_full = C.c_int64(), C.c_int32()
+        # drain -> apply-enqueue is one critical section: a thread that finds
+        # nothing pending must not launch before another thread's apply of
+        # the cells it drained
+        self._mirror_lock = threading.RLock()
 
     def __del__(self):
         h = getattr(self, "_h", None)
@@ -212,7 +217,9 @@ class PagePool:
         """pool.py:154-174; granted pages are zeroed in every attached store."""
         existing = seq_id in self._ids
         h = self._ids[seq_id] if existing else next(self._handles)
-        n_max = max(self.pages_for(length), 1) if length >= 0 else 1
+        # the native side never grants more than the pool holds: an oversized
+        # request fails there with CapacityExhausted, not here with MemoryError
+        n_max = max(min(self.pages_for(length), self.capacity_pages), 1) if length >= 0 else 1
         buf = (C.c_uint32 * n_max)()
         n = C.c_int64()
         _lib.call("pkv_pool_reserve", self._h, h, int(length), buf, C.byref(n))
@@ -224,7 +231,7 @@ class PagePool:
     def grow(self, seq_id, new_len: int) -> list[int]:
         """pool.py:176-187; no-op when capacity already covers new_len."""
         h = self._handle_or_ghost(seq_id)
-        n_max = max(self.pages_for(new_len), 1)
+        n_max = max(min(self.pages_for(new_len), self.capacity_pages), 1)
         buf = (C.c_uint32 * n_max)()
         n = C.c_int64()
         _lib.call("pkv_pool_grow", self._h, h, int(new_len), buf, C.byref(n))
@@ -374,6 +381,15 @@ class PagePool:
 
         Dirty cells are drained from the native pool and applied by one small
         kernel; a shape change re-uploads the whole matrix."""
+        import torch
+
+        with self._mirror_lock:
+            if device.index is not None and torch.cuda.current_device() != device.index:
+                with torch.cuda.device(device):
+                    return self._device_table(device)
+            return self._device_table(device)
+
+    def _device_table(self, device):
         import torch
 
         lib = _lib.load()
