@@ -404,10 +404,10 @@ def paged_attention(queries, store: KvStore, meta: MaskMeta, config: AttentionCo
     runs = _prefill_route(meta, config, store.dtype_code, precision)
     mirror = store.pool.device_table(device)
     if runs is not None:
-        return _launch_prefill(q, meta, config, runs, k=store.keys, v=store.values,
+        return _launch_prefill(q, meta, config, runs, k=store.k_cache, v=store.v_cache,
                                kv_code=store.dtype_code, bt=mirror, rows=seq_row,
                                out_dtype=out_dtype or torch.float32, device=device)
-    return _launch_attention(q, qcode, meta, config, nkeys, k=store.keys, v=store.values,
+    return _launch_attention(q, qcode, meta, config, nkeys, k=store.k_cache, v=store.v_cache,
                              kv_code=store.dtype_code, bt=mirror, bt_stride=mirror.shape[1],
                              seq_row=seq_row, seq_start=None,
                              out_dtype=out_dtype or torch.float32, device=device,

@@ -123,8 +123,8 @@ class DecodeBatch:
         if self._stage_stores != key:
             self._uniform = len({s.row_bytes for s in stores}) == 1
             if self._uniform:
-                self._kc = (C.c_void_p * len(stores))(*[s.keys.data_ptr() for s in stores])
-                self._vc = (C.c_void_p * len(stores))(*[s.values.data_ptr() for s in stores])
+                self._kc = (C.c_void_p * len(stores))(*[s.k_cache.data_ptr() for s in stores])
+                self._vc = (C.c_void_p * len(stores))(*[s.v_cache.data_ptr() for s in stores])
             self._stage_stores = key
         return self._uniform
 
@@ -278,7 +278,7 @@ class DecodeBatch:
         slot = self._stage_setup()
         ptrs = self._store_ptrs.get(id(store))
         if ptrs is None:
-            ptrs = (store.keys.data_ptr(), store.values.data_ptr(), store.dtype_code, store.page_size)
+            ptrs = (store.k_cache.data_ptr(), store.v_cache.data_ptr(), store.dtype_code, store.page_size)
             self._store_ptrs[id(store)] = ptrs
         a = self._args
         a.q, a.q_dtype = q.data_ptr(), self._qcodes[q.dtype]
@@ -355,7 +355,7 @@ class DecodeBatch:
         hp = host.data_ptr()
         ptrs = self._store_ptrs.get(id(store))
         if ptrs is None:
-            ptrs = (store.keys.data_ptr(), store.values.data_ptr(), store.dtype_code, store.page_size)
+            ptrs = (store.k_cache.data_ptr(), store.v_cache.data_ptr(), store.dtype_code, store.page_size)
             self._store_ptrs[id(store)] = ptrs
         a = self._args
         a.q, a.q_dtype = q.data_ptr(), qcode
