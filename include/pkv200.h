@@ -163,6 +163,17 @@ int pkv_kv_append(const void* k_new, const void* v_new, int64_t n_tok, const int
                   int64_t bt_stride, int32_t page_size, void* k_cache, void* v_cache,
                   int64_t row_bytes, void* stream);
 
+/* K-gather: contiguous copies of paged rows — KvStore.gather / gather_view
+ * (store.py:152-161, 187-190).  For view sequence s (s < n_seq) with block
+ * table row seq_row[s], positions [0, cu_rows[s+1] - cu_rows[s]) land at
+ * output rows cu_rows[s] .. cu_rows[s+1]-1 (cu_rows: int32 exclusive prefix,
+ * n_seq + 1 entries, cu_rows[n_seq] == n_rows; device pointers).  K and V in
+ * one launch; bit-exact copies.  The caller validates lengths against the
+ * tables (OutOfRange) before the call. */
+int pkv_kv_gather(const void* k_cache, const void* v_cache, const int32_t* block_table, int64_t bt_stride,
+                  const int32_t* seq_row, const int32_t* cu_rows, int64_t n_seq, int64_t n_rows,
+                  int32_t page_size, int64_t row_bytes, void* k_out, void* v_out, void* stream);
+
 /* K2   paged_attention          attention.py:259-354 — split-K flash decode
  * over the block table with an online softmax, plus the K2c combine.
  * Query i belongs to view sequence q_seq[i] and attends keys 0..q_nkeys[i]-1

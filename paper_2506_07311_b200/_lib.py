@@ -118,6 +118,7 @@ SIGNATURES = {
     "pkv_page_zero": (C.c_int, [_vp, _vp, _vp, _i64, _i64, _vp]),
     "pkv_page_copy": (C.c_int, [_vp, _vp, _vp, _i64, _i64, _i32, _vp]),
     "pkv_kv_append": (C.c_int, [_vp, _vp, _i64, _vp, _i32, _vp, _vp, _i64, _i32, _vp, _vp, _i64, _vp]),
+    "pkv_kv_gather": (C.c_int, [_vp, _vp, _vp, _i64, _vp, _vp, _i64, _i64, _i32, _i64, _vp, _vp, _vp]),
     "pkv_attention_workspace_bytes": (_i64, [_i64, _i32, _i32]),
     "pkv_decode_step_stage_ints": (_i64, [_i64, _i32]),
     "pkv_decode_step_stage": (C.c_int, [_P(StepStageArgs), _vp]),

@@ -127,6 +127,34 @@ __global__ void kv_append_kernel(const char* __restrict__ kn, const char* __rest
   }
 }
 
+// K-gather (store.py:152-161, 187-190): out[t] = cache[slot(t)] for the
+// concatenated positions [0, len_s) of every view sequence s, in view order.
+// One warp per row (K and V), lanes stride over the row in 16/4/2-byte
+// units; the sequence of a row is found by binary search over the int32
+// exclusive prefix cu[0..n_seq] (cu[n_seq] = rows).
+__global__ void kv_gather_kernel(const char* __restrict__ kc, const char* __restrict__ vc,
+                                 const int32_t* __restrict__ bt, int64_t bt_stride,
+                                 const int32_t* __restrict__ seq_row, const int32_t* __restrict__ cu,
+                                 int n_seq, int log2ps, int64_t row_bytes, char* __restrict__ ko,
+                                 char* __restrict__ vo) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warps = int64_t(gridDim.x) * (blockDim.x >> 5);
+  const int64_t rows = cu[n_seq];
+  const int ps = 1 << log2ps;
+  for (int64_t t = blockIdx.x * int64_t(blockDim.x >> 5) + (threadIdx.x >> 5); t < rows; t += warps) {
+    int lo = 0, hi = n_seq - 1;  // last s with cu[s] <= t
+    while (lo < hi) {
+      const int mid = (lo + hi + 1) >> 1;
+      if (cu[mid] <= t) lo = mid; else hi = mid - 1;
+    }
+    const int64_t pos = t - cu[lo];
+    const int64_t page = bt[int64_t(seq_row[lo]) * bt_stride + (pos >> log2ps)];
+    const int64_t src = (page * ps + (pos & (ps - 1))) * row_bytes;
+    copy_bytes(ko + t * row_bytes, kc + src, row_bytes, lane, 32);
+    copy_bytes(vo + t * row_bytes, vc + src, row_bytes, lane, 32);
+  }
+}
+
 // decode-step append for the exact path: query i appends its token at
 // position q_nkeys[i]-1 of view sequence q_seq[i]
 __global__ void append_decode_kernel(const char* __restrict__ kn, const char* __restrict__ vn,
@@ -667,6 +695,27 @@ int pkv_kv_append(const void* k_new, const void* v_new, int64_t n_tok, const int
       static_cast<const char*>(k_new), static_cast<const char*>(v_new), n_tok, tok_row,
       tok_row_stride, tok_pos, block_table, bt_stride, __builtin_ctz(page_size),
       static_cast<char*>(k_cache), static_cast<char*>(v_cache), row_bytes);
+  PKV_CHECK_LAUNCH();
+  return PKV_OK;
+}
+
+int pkv_kv_gather(const void* k_cache, const void* v_cache, const int32_t* block_table, int64_t bt_stride,
+                  const int32_t* seq_row, const int32_t* cu_rows, int64_t n_seq, int64_t n_rows,
+                  int32_t page_size, int64_t row_bytes, void* k_out, void* v_out, void* stream) {
+  if (n_seq <= 0 || n_rows <= 0) return PKV_OK;
+  if (page_size <= 0 || (page_size & (page_size - 1)))
+    return pkv::fail(PKV_VALUE_ERROR, "page_size must be a power of two");
+  if (row_bytes & 1) return pkv::fail(PKV_CONFIG_ERROR, "row bytes must be even");
+  if (n_seq >= (int64_t(1) << 31) || n_rows >= (int64_t(1) << 31))
+    return pkv::fail(PKV_CONFIG_ERROR, "gather of more than 2^31 rows");
+  pkv::DeviceGuard guard(static_cast<cudaStream_t>(stream));
+  const int threads = 256;
+  const int64_t want = (n_rows + 7) / 8;
+  const int64_t blocks = want < 148 * 16 ? want : 148 * 16;
+  kv_gather_kernel<<<static_cast<unsigned>(blocks), threads, 0, static_cast<cudaStream_t>(stream)>>>(
+      static_cast<const char*>(k_cache), static_cast<const char*>(v_cache), block_table, bt_stride, seq_row,
+      cu_rows, static_cast<int>(n_seq), __builtin_ctz(page_size), row_bytes, static_cast<char*>(k_out),
+      static_cast<char*>(v_out));
   PKV_CHECK_LAUNCH();
   return PKV_OK;
 }

@@ -447,3 +447,37 @@ def test_pure_c_abi_client(tmp_path):
     run = subprocess.run([exe], capture_output=True, text=True, timeout=120)
     assert run.returncode == 0, run.stdout + run.stderr
     assert run.stdout.startswith("abi ok")
+
+
+@pytest.mark.parametrize("dtype,heads,dim,ps", [(np.float32, 2, 3, 4), (np.float16, 3, 5, 16),
+                                                ("bf16", 8, 128, 16), (np.float32, 8, 64, 64)])
+def test_gather_kernel_bit_exact(dtype, heads, dim, ps):
+    """K-gather (pkv_kv_gather, store.py:152-161 / 187-190) against a host
+    row-index gather of the same pages: bit-exact, any row size (16 / 4 /
+    2-byte units), scattered and reused pages, zero-length members."""
+    dt = torch.bfloat16 if dtype == "bf16" else dtype
+    rng = np.random.default_rng(3)
+    pool = PagePool(512, page_size=ps)
+    store = KvStore(pool, heads, dim, dtype=dt)
+    lengths = [0, 1, ps, ps + 1, 3 * ps - 1, 97, 0, 5 * ps]
+    for i, n in enumerate(lengths):
+        pool.reserve(("pad", i), ps * int(rng.integers(1, 4)))
+        pool.reserve(i, n)
+        k = torch.from_numpy(rng.standard_normal((n, heads, dim)).astype(np.float32)).to(dt)
+        v = torch.from_numpy(rng.standard_normal((n, heads, dim)).astype(np.float32)).to(dt)
+        store.assign(i, rng.permutation(n), k, v)
+        if i % 2:
+            pool.free(("pad", i))
+    ids = list(range(len(lengths)))
+    view = store.batch_view(ids)
+    gk, gv = store.gather_view(view)
+    rows = torch.from_numpy(store.view_row_indices(view)).cuda()
+    assert gk.shape == (sum(lengths), heads, dim)
+    assert torch.equal(gk, store.k_cache.index_select(0, rows))
+    assert torch.equal(gv, store.v_cache.index_select(0, rows))
+    for i, n in enumerate(lengths):
+        k1, v1 = store.gather(i, n)
+        r1 = torch.from_numpy(store.row_indices(i, n)).cuda()
+        assert torch.equal(k1, store.k_cache.index_select(0, r1)) and torch.equal(v1, store.v_cache.index_select(0, r1))
+    with pytest.raises(OutOfRange):
+        store.gather(2, ps + 1)
