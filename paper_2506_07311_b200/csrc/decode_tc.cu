@@ -45,6 +45,8 @@
 #include <algorithm>
 #include <cstdio>
 #include <cstdlib>
+#include <mutex>
+#include <unordered_map>
 #include <vector>
 
 #include "common.cuh"
@@ -285,9 +287,6 @@ __global__ void __launch_bounds__(kThreadsTc, 1) decode_tc_kernel(const __grid_c
   constexpr int KS = D / 16;             // k-steps of Q K^T
   constexpr int NT = D / 8;              // n-tiles of P V
   static_assert(CPR >= 8 && CPR <= 32, "D must be 64 or 128");
-
-  // dependents (the split combine) may launch now and wait for our completion
-  asm volatile("griddepcontrol.launch_dependents;");
 
   extern __shared__ __align__(1024) unsigned char smem[];
   __shared__ int s_flag[kWarpsTc];  // per head: this CTA's piece merges the split
@@ -722,6 +721,20 @@ int64_t decode_plan_ints(int64_t nq, int hq) {
          (kMaxGrid + 1) * (kCombInts + kWarpsTc);
 }
 
+// Raise (never lower) a kernel's dynamic shared-memory limit.  One record per
+// kernel: the occupancy query below and the launches share it, so a query
+// can no longer shrink the limit under a launch that configured more.
+cudaError_t ensure_smem(const void* fn, int smem) {
+  static std::mutex mu;
+  static std::unordered_map<const void*, int> limit;
+  std::lock_guard<std::mutex> g(mu);
+  int& cur = limit[fn];
+  if (cur >= smem) return cudaSuccess;
+  const cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  if (e == cudaSuccess) cur = smem;
+  return e;
+}
+
 // Co-resident clusters of `c` CTAs of the decode kernel (one CTA per SM):
 // queried from the device once (bf16, head_dim 128 instance, full smem),
 // else the measured B200 figures scaled to num_sms.
@@ -734,7 +747,7 @@ int cluster_capacity(int c, int num_sms) {
     if (cudaGetDeviceCount(&dev_count) == cudaSuccess && dev_count > 0) {
       auto fn = decode_tc_kernel<__nv_bfloat16, 128, false, false>;
       const int smem = 214016;
-      cudaFuncSetAttribute(reinterpret_cast<const void*>(fn), cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+      ensure_smem(reinterpret_cast<const void*>(fn), smem);
       cudaFuncSetAttribute(reinterpret_cast<const void*>(fn), cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
       cudaLaunchConfig_t cfg = {};
       cfg.gridDim = dim3(static_cast<unsigned>(c));
@@ -1057,14 +1070,11 @@ int launch_decode_tc(TcParams p, const int32_t* plan_host, int kv_dtype, int hea
   p.merge_offset = p.plan_in_smem ? static_cast<int>((plan_bytes + 127) / 128 * 128) : 0;
   p.ring_offset = (p.merge_offset + merge_bytes + 1023) / 1024 * 1024;
   const int smem = p.ring_offset + kWarpsTc * kStagesTc * 2 * kCh * head_dim * 2;
-  static int configured[16] = {0};
   const int key = (kv_dtype == PKV_BF16) * 8 + (head_dim == 128) * 4 + splitq * 2 + rows16;
-  if (configured[key] < smem) {
-    cudaError_t e = cudaFuncSetAttribute(reinterpret_cast<const void*>(fn),
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  {
+    const cudaError_t e = ensure_smem(reinterpret_cast<const void*>(fn), smem);
     if (e != cudaSuccess)
       return fail(PKV_CUDA_ERROR, "decode_tc smem attribute (%d B): %s", smem, cudaGetErrorString(e));
-    configured[key] = smem;
   }
   const int grid = plan_host[H_GRID];  // the planner's assignment is per CTA
   const int cluster = plan_host[H_CLUSTER];
@@ -1087,7 +1097,8 @@ int launch_decode_tc(TcParams p, const int32_t* plan_host, int kv_dtype, int hea
     attr[0].val.clusterDim.z = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    if (std::getenv("PKV_DEBUG_CLUSTER")) {
+    static const bool debug_cluster = std::getenv("PKV_DEBUG_CLUSTER") != nullptr;
+    if (debug_cluster) {
       int n = -1;
       cudaError_t oe = cudaOccupancyMaxActiveClusters(&n, fn, &cfg);
       std::fprintf(stderr, "pkv: cluster %d grid %d smem %d -> max active clusters %d (%s)\n", cluster, grid, smem,
@@ -1098,7 +1109,9 @@ int launch_decode_tc(TcParams p, const int32_t* plan_host, int kv_dtype, int hea
     fn<<<grid, kThreadsTc, smem, stream>>>(p);
     e = cudaGetLastError();
   }
-  if (e != cudaSuccess) return fail(PKV_CUDA_ERROR, "decode_tc launch: %s", cudaGetErrorString(e));
+  if (e != cudaSuccess)
+    return fail(PKV_CUDA_ERROR, "decode_tc launch: %s (grid %d cluster %d smem %d nq %d key %d)",
+                cudaGetErrorString(e), grid, cluster, smem, p.nq, key);
   return PKV_OK;
 }
 
