@@ -198,6 +198,47 @@ class L2Flush:
 # our implementation: the exact timed call, reusable by the parity tests
 # ---------------------------------------------------------------------------
 
+def build_cache(lengths, hq, hkv, d, ps, extra_tokens, device, seed=0, fragment=False, reserve_extra=0):
+    """A bf16 paged cache holding `lengths` tokens per sequence (randn K/V),
+    tables reserved for `reserve_extra` more tokens, pool room for
+    `extra_tokens` more.  Layout: the reference's scatter recipe
+    (verify.py:172-194: throw-away reservations interleaved with the real
+    ones, then freed), or with `fragment` every table over a random
+    permutation of the live pages (a long-running pool)."""
+    import torch
+
+    from paper_2506_07311_b200 import AttentionConfig, KvStore, PagePool
+
+    B = len(lengths)
+    need = sum(-(-(n + extra_tokens) // ps) for n in lengths)
+    pad = max(B, need // 8)
+    pool = PagePool(need + pad + B + 8, page_size=ps)
+    store = KvStore(pool, hkv, d, dtype=torch.bfloat16, device=device)
+    for b, n in enumerate(lengths):
+        pool.reserve(("pad", b), ps * (1 + (b * 7919) % max(1, pad // B)))
+        pool.reserve(b, n + reserve_extra)
+    for b in range(B):
+        pool.free(("pad", b))
+    if fragment:
+        live = [list(pool.table(b).entries) for b in range(B)]
+        flat = np.concatenate([np.asarray(e, dtype=np.int64) for e in live])
+        perm = np.random.default_rng(1000 + seed).permutation(flat)
+        off = 0
+        for b, e in enumerate(live):
+            pool.table(b).entries[:] = perm[off:off + len(e)].tolist()
+            off += len(e)
+    gen = torch.Generator(device=device).manual_seed(seed)
+    chunk = 1 << 15
+    for b, n in enumerate(lengths):
+        pool.table(b).logical_len = 0
+        for s0 in range(0, n, chunk):
+            m = min(chunk, n - s0)
+            k = torch.randn((m, hkv, d), generator=gen, device=device, dtype=torch.bfloat16)
+            v = torch.randn((m, hkv, d), generator=gen, device=device, dtype=torch.bfloat16)
+            store.assign(b, np.arange(s0, s0 + m), k, v)
+    return pool, store, AttentionConfig(head_count=hq, head_dim=d, page_size=ps, kv_head_count=hkv)
+
+
 class DecodeBench:
     """One rank's decode benchmark: a scattered (or fragmented) bf16 paged
     cache holding `lengths` tokens, per-step q / k_new / v_new resident in
@@ -208,43 +249,18 @@ class DecodeBench:
     def __init__(self, lengths, hq, hkv, d, ps, *, total_steps, device, seed=0, fragment=False, waves=0):
         import torch
 
-        from paper_2506_07311_b200 import AttentionConfig, KvStore, PagePool, _lib
+        from paper_2506_07311_b200 import AttentionConfig, _lib
         from paper_2506_07311_b200.attention import _Workspace
 
         self.lengths, self.hq, self.hkv, self.d, self.ps = list(lengths), hq, hkv, d, ps
         self.B = B = len(lengths)
         self.device, self.total_steps, self.fragment = device, total_steps, fragment
-        need = sum(-(-(n + total_steps + 1) // ps) for n in lengths)
-        pad = max(B, need // 8)
-        # room for the e2e phase's page grants after the device phase
-        e2e_room = sum(-(-(n + 2 * total_steps + 2) // ps) for n in lengths) - need + B
-        self.pool = pool = PagePool(need + pad + e2e_room + 8, page_size=ps)
-        self.store = store = KvStore(pool, hkv, d, dtype=torch.bfloat16, device=device)
-        # the reference's scatter recipe (verify.py:172-194): throw-away
-        # reservations interleaved with the real ones, then freed
-        for b, n in enumerate(lengths):
-            pool.reserve(("pad", b), ps * (1 + (b * 7919) % max(1, pad // B)))
-            pool.reserve(b, n + total_steps + 1)
-        for b in range(B):
-            pool.free(("pad", b))
-        if fragment:  # every table over a random permutation of the live pages
-            live = [list(pool.table(b).entries) for b in range(B)]
-            flat = np.concatenate([np.asarray(e, dtype=np.int64) for e in live])
-            perm = np.random.default_rng(1000 + seed).permutation(flat)
-            off = 0
-            for b, e in enumerate(live):
-                pool.table(b).entries[:] = perm[off:off + len(e)].tolist()
-                off += len(e)
-        for b, n in enumerate(lengths):
-            pool.table(b).logical_len = 0
-        gen = torch.Generator(device=device).manual_seed(seed)
-        chunk = 1 << 15
-        for b, n in enumerate(lengths):
-            for s0 in range(0, n, chunk):
-                m = min(chunk, n - s0)
-                k = torch.randn((m, hkv, d), generator=gen, device=device, dtype=torch.bfloat16)
-                v = torch.randn((m, hkv, d), generator=gen, device=device, dtype=torch.bfloat16)
-                store.assign(b, np.arange(s0, s0 + m), k, v)
+        # tables cover the device phase; the pool keeps room for the e2e
+        # phase's page grants
+        self.pool, self.store, _ = build_cache(lengths, hq, hkv, d, ps, extra_tokens=2 * total_steps + 2,
+                                               device=device, seed=seed, fragment=fragment,
+                                               reserve_extra=total_steps + 1)
+        pool, store = self.pool, self.store
         self.cfg = AttentionConfig(head_count=hq, head_dim=d, page_size=ps, kv_head_count=hkv)
         self.lib = lib = _lib.load()
         self.mirror = mirror = pool.device_table(device)

@@ -509,7 +509,7 @@ def attention_weights(queries, store: KvStore, meta: MaskMeta, config: Attention
     import torch
 
     _check_queries(queries, meta, config)
-    keys, _ = store.gather_view(meta.view)
+    keys, _ = KvStore.gather_view(store, meta.view)  # device tensors (also under the numpy facade)
     dev = keys.device
     q = torch.as_tensor(np.asarray(queries) if not isinstance(queries, torch.Tensor) else queries).to(dev, torch.float64)
     g = config.head_count // config.kv_head_count

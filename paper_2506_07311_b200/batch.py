@@ -32,6 +32,9 @@ import os as _os
 # PCIe while the step runs (measured on C2: 196 -> 186 us per e2e step).
 # PKV_ZERO_COPY_OUT=0 restores the copy.
 _ZERO_COPY_OUT = _os.environ.get("PKV_ZERO_COPY_OUT", "1") != "0"
+# Pinned host q / k_new / v_new read by the kernel through their mapped
+# pointers (no H2D copy ahead of the launch).  Experiment switch.
+_ZERO_COPY_IN = _os.environ.get("PKV_ZERO_COPY_IN", "0") == "1"
 
 
 class DecodeBatch:
@@ -214,6 +217,8 @@ class DecodeBatch:
         if type(x) is torch.Tensor and x.dtype is dtype and not x.is_cuda and x.shape == shape \
                 and x.is_contiguous():  # fast path: a host tensor ready to copy
             self._keep.append(x)
+            if _ZERO_COPY_IN and x.is_pinned():
+                return x, None, 0  # the kernel reads the mapped host rows itself
             return self._buffer(name, shape, dtype), x.data_ptr(), x.nbytes
         if not isinstance(x, torch.Tensor):
             x = torch.from_numpy(np.ascontiguousarray(x))

@@ -455,7 +455,7 @@ def test_gather_kernel_bit_exact(dtype, heads, dim, ps):
     """K-gather (pkv_kv_gather, store.py:152-161 / 187-190) against a host
     row-index gather of the same pages: bit-exact, any row size (16 / 4 /
     2-byte units), scattered and reused pages, zero-length members."""
-    dt = torch.bfloat16 if dtype == "bf16" else dtype
+    dt = {"bf16": torch.bfloat16, np.float16: torch.float16, np.float32: torch.float32}[dtype]
     rng = np.random.default_rng(3)
     pool = PagePool(512, page_size=ps)
     store = KvStore(pool, heads, dim, dtype=dt)
