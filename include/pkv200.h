@@ -391,6 +391,14 @@ int pkv_debug_trace(int32_t enable, uint64_t* out, int64_t n);
  * PKV_FAIL_STEP_LAUNCH = the attention launch of pkv_decode_step.  The step
  * returns PKV_CUDA_ERROR and the allocator is rolled back (tests of the
  * all-or-nothing contract, pool.py:143-148, 165-169). */
+/* Debug: host phase stamps (ns since entry) of this thread's last
+ * pkv_decode_step: [1] input copies issued, [2] staging slot free, [3]
+ * allocator + plan, [4] side blocks, [5] metadata upload issued, [6] aux
+ * kernel issued, [7] before / [8] after the decode launch, [9] output copy
+ * issued, [10] next plan speculated; [11] the entry time itself (steady clock,
+ * ns since its epoch: CLOCK_MONOTONIC on Linux). */
+int pkv_debug_step_times(int64_t* out, int32_t n);
+
 #define PKV_FAIL_STEP_UPLOAD 1
 #define PKV_FAIL_STEP_LAUNCH 2
 int pkv_debug_inject_failure(int32_t site);

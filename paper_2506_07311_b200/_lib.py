@@ -136,6 +136,7 @@ SIGNATURES = {
     "pkv_device_sm_count": (C.c_int, [_P(_i32)]),
     "pkv_debug_trace": (C.c_int, [_i32, _P(_u64), _i64]),
     "pkv_debug_inject_failure": (C.c_int, [_i32]),
+    "pkv_debug_step_times": (C.c_int, [_P(_i64), _i32]),
 }
 
 PKV_FAIL_STEP_UPLOAD, PKV_FAIL_STEP_LAUNCH = 1, 2

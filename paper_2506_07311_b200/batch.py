@@ -208,6 +208,39 @@ class DecodeBatch:
             view = self._bufs[key] = base[:shape[0]]
         return view
 
+    def _packed(self, q_shape, kv_shape, dtype):
+        """Adjacent device views q | k | v of one capacity-sized buffer, the
+        layout of a packed host input (one H2D copy)."""
+        import torch
+
+        key = ("packed", q_shape, kv_shape, dtype)
+        views = self._bufs.get(key)
+        if views is None:
+            qn, kvn = int(np.prod(q_shape)), int(np.prod(kv_shape))
+            base = self._bufs.get(("packed_base", dtype, self._cap))
+            per_row = (q_shape[1] + 2 * kv_shape[1]) * q_shape[2]
+            if base is None:
+                base = torch.empty(self._cap * per_row, dtype=dtype, device=self.device)
+                self._bufs[("packed_base", dtype, self._cap)] = base
+            views = (base[:qn].view(q_shape), base[qn:qn + kvn].view(kv_shape),
+                     base[qn + kvn:qn + 2 * kvn].view(kv_shape))
+            self._bufs[key] = views
+        return views
+
+    @staticmethod
+    def packed_host_inputs(n, hq, hkv, d, dtype, pin=True):
+        """Host buffers for step(): q [n,Hq,D], k_new / v_new [n,Hkv,D] as
+        adjacent views of one (pinned) allocation, so the step moves them
+        with a single host-to-device copy."""
+        import torch
+
+        base = torch.empty(n * (hq + 2 * hkv) * d, dtype=dtype)
+        if pin:
+            base = base.pin_memory()
+        qn, kvn = n * hq * d, n * hkv * d
+        return (base[:qn].view(n, hq, d), base[qn:qn + kvn].view(n, hkv, d),
+                base[qn + kvn:qn + 2 * kvn].view(n, hkv, d))
+
     def _input(self, x, dtype, shape, name):
         """-> (device tensor, host pointer or None, bytes).  CPU inputs are
         copied by the native step into a persistent device buffer (pin them
@@ -262,6 +295,11 @@ class DecodeBatch:
         kv_shape = (n, cfg.kv_head_count, cfg.head_dim)
         k, k_host, kv_bytes = self._input(k_new, store.torch_dtype, kv_shape, "k_new")
         v, v_host, _ = self._input(v_new, store.torch_dtype, kv_shape, "v_new")
+        if q_host and k_host == q_host + q_bytes and v_host == k_host + kv_bytes and q_t is store.torch_dtype:
+            # q | k | v adjacent in one host buffer (a fused QKV projection's
+            # output, planar): ONE host-to-device copy into a packed buffer
+            q, k, v = self._packed(q.shape, k.shape, q_t)
+            q_bytes, k_host, v_host = q_bytes + 2 * kv_bytes, None, None
         out_host = None
         if out is None:
             out_t, out_code = (torch.float32, _lib.PKV_F32) if out_dtype is None else torch_dtype(out_dtype)

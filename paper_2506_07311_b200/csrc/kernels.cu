@@ -27,6 +27,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <chrono>
 #include <vector>
 #include <cstdint>
 #include <cstring>
@@ -774,6 +775,22 @@ extern "C" int pkv_decode_step_prepare(pkv_pool* pool, const int64_t* seqs, int6
   return st;
 }
 
+// host-side phase stamps of the last pkv_decode_step on this thread
+// (pkv_debug_step_times): steady-clock ns since the call's entry
+namespace {
+thread_local int64_t t_stamp[12];
+thread_local std::chrono::steady_clock::time_point t_stamp0;
+inline void stamp(int i) {
+  t_stamp[i] = std::chrono::duration_cast<std::chrono::nanoseconds>(std::chrono::steady_clock::now() - t_stamp0).count();
+}
+}  // namespace
+
+extern "C" int pkv_debug_step_times(int64_t* out, int32_t n) {
+  t_stamp[11] = std::chrono::duration_cast<std::chrono::nanoseconds>(t_stamp0.time_since_epoch()).count();
+  for (int i = 0; i < n && i < 12; ++i) out[i] = t_stamp[i];
+  return PKV_OK;
+}
+
 // side blocks behind the plan: granted pages, copy triples, mirror pairs, the
 // zero list and the per-store cache pointer table (up to kMaxStageStores)
 constexpr int64_t kMaxStageStores = 256;
@@ -805,6 +822,7 @@ static int decode_step_stage(pkv_step_stage_args* a, cudaStream_t stream, pkv_ap
     cudaError_t e = cudaEventSynchronize(static_cast<cudaEvent_t>(a->slot_event));
     if (e != cudaSuccess) return pkv::fail(PKV_CUDA_ERROR, "slot event: %s", cudaGetErrorString(e));
   }
+  stamp(2);
   const int64_t n = a->n;
   const int64_t extra = stage_extra(n);
   if (a->n_stores > kMaxStageStores)
@@ -819,6 +837,7 @@ static int decode_step_stage(pkv_step_stage_args* a, cudaStream_t stream, pkv_ap
                                a->meta_cap - extra, &used, pages.data(), static_cast<int64_t>(pages.size()),
                                &n_pages, copies.data(), undo);
   if (st) return st;
+  stamp(3);
   // from here on a failure restores the allocator before returning
   auto fail_back = [&](int code) {
     pkv_pool_rollback_append(a->pool, *undo);
@@ -874,6 +893,7 @@ static int decode_step_stage(pkv_step_stage_args* a, cudaStream_t stream, pkv_ap
     }
   }
   // 3) one upload of everything, then ONE page / mirror kernel
+  stamp(4);
   const int64_t total = used + off;
   if (total > a->meta_cap) return fail_back(pkv::fail(PKV_VALUE_ERROR, "metadata slot too small"));
   if (page_work && (a->row_bytes & 1)) return fail_back(pkv::fail(PKV_CONFIG_ERROR, "row bytes must be even"));
@@ -884,6 +904,7 @@ static int decode_step_stage(pkv_step_stage_args* a, cudaStream_t stream, pkv_ap
   if (e != cudaSuccess)
     return fail_back(pkv::fail(PKV_CUDA_ERROR, "step metadata upload: %s", cudaGetErrorString(e)));
   if (a->slot_event) cudaEventRecord(static_cast<cudaEvent_t>(a->slot_event), stream);
+  stamp(5);
   if (page_work || n_pairs) {
     const int n_st = page_work ? a->n_stores : 0;
     const int64_t blocks = std::max<int64_t>(n_st * (n_zero + n_copies), (n_pairs + 255) / 256);
@@ -895,6 +916,7 @@ static int decode_step_stage(pkv_step_stage_args* a, cudaStream_t stream, pkv_ap
     if (le != cudaSuccess) return fail_back(pkv::fail(PKV_CUDA_ERROR, "step aux kernel: %s", cudaGetErrorString(le)));
     ++a->launches;
   }
+  stamp(6);
   a->meta_used = used;
   a->n_granted = n_pages;
   a->granted_off = pages_off;
@@ -1071,7 +1093,9 @@ static void plan_speculate(const int32_t* nk, const int32_t* row, int64_t n, int
 int pkv_decode_step(pkv_step_stage_args* stage, pkv_attention_args* attn, pkv_decode_io* io, void* stream_) {
   if (!stage || !attn) return pkv::fail(PKV_VALUE_ERROR, "null args");
   cudaStream_t stream = static_cast<cudaStream_t>(stream_);
+  t_stamp0 = std::chrono::steady_clock::now();
   pkv::DeviceGuard guard(stream);
+  stamp(0);
   if (io) io->launched = io->launches = 0;
   // the input copies go first so they overlap the host-side allocator / plan
   auto h2d = [&](const void* src, const void* dst, int64_t bytes, const char* what) -> int {
@@ -1087,6 +1111,7 @@ int pkv_decode_step(pkv_step_stage_args* stage, pkv_attention_args* attn, pkv_de
     if (!st) st = h2d(io->v_host, attn->v_new, io->kv_bytes, "v_new");
     if (st) return st;
   }
+  stamp(1);
   pkv_append_undo* undo = nullptr;
   int st = decode_step_stage(stage, stream, &undo);
   if (st) return st;
@@ -1116,8 +1141,10 @@ int pkv_decode_step(pkv_step_stage_args* stage, pkv_attention_args* attn, pkv_de
   }
   if (pkv_debug_should_fail(PKV_FAIL_STEP_LAUNCH))
     return fail_back(pkv::fail(PKV_CUDA_ERROR, "decode launch: injected failure"));
+  stamp(7);
   st = pkv_paged_attention(attn, stream_);
   if (st) return fail_back(st);
+  stamp(8);
   pkv_pool_release_undo(undo);
   const bool tensor = attn->mode == 2 || (attn->mode == 0 && attn->kv_dtype == PKV_BF16);
   if (io) {
@@ -1131,7 +1158,9 @@ int pkv_decode_step(pkv_step_stage_args* stage, pkv_attention_args* attn, pkv_de
     io->launched = 1;
   }
   // the next step's plan, computed while the GPU runs this one
+  stamp(9);
   if (tensor) plan_speculate(stage->meta_host + n, stage->meta_host + 2 * n, n, attn->page_size, attn->hq, attn->hkv);
+  stamp(10);
   return PKV_OK;
 }
 
