@@ -180,15 +180,17 @@ class ClockSampler:
 
 
 class L2Flush:
-    """Between timed steps: READ 2x L2 of unrelated data so the next step
+    """Between timed steps: READ 4x L2 of unrelated data so the next step
     starts with a cold, clean L2 (a write flush would leave dirty lines whose
-    write-back steals HBM bandwidth from the timed kernel)."""
+    write-back steals HBM bandwidth from the timed kernel).  4x (~80 us of
+    GPU time) also keeps the host's launch of the next step ahead of the GPU,
+    so short steps do not time the host's issue latency."""
 
     def __init__(self, device):
         import torch
 
         l2 = torch.cuda.get_device_properties(device).L2_cache_size
-        self.buf = torch.ones(max(2 * l2, 256 << 20) // 4, dtype=torch.float32, device=device)
+        self.buf = torch.ones(max(4 * l2, 512 << 20) // 4, dtype=torch.float32, device=device)
 
     def __call__(self):
         self.buf.sum()
@@ -672,7 +674,7 @@ def line_for(args, config, res, world, peak, peak_src, steps, warmup):
         "config": {"workload": res["name"], "global_batch": int(res["tokens_all"] / steps),
                    "kv_bytes_per_step": res["kv_all"] / steps, "page_size": res["shape"][3],
                    "parallelism": f"request-sharded x{world}" + (" (LPT, no data-path collective)" if world > 1 else ""),
-                   "l2": "flushed between steps (read of 2x L2 of unrelated data)",
+                   "l2": "flushed between steps (read of 4x L2 of unrelated data)",
                    "fragmented": bool(args.fragment)},
         "pct_of_8TBs": round(100 * value / world / NOMINAL_HBM_GBS, 2),
         "tokens_per_s": res["tokens_all"] / (res["total_ms_max"] / 1e3),
