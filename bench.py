@@ -317,10 +317,15 @@ class DecodeBench:
         self.last_step = t
 
     def run(self, W, K, flush, barrier=None):
-        """W untimed + K timed steps (L2 flushed before each); returns per-step
-        and per-launch CUDA-event times and the clock record."""
+        """W untimed + K timed steps (L2 flushed before each), then K more
+        steps whose decode launch alone is bracketed by events on the
+        launching stream (the roofline's per-launch time; kept out of the
+        timed steps, whose events would otherwise nest).  Needs
+        total_steps >= W + 2K.  Returns the step and launch times and the
+        clock record of the timed steps."""
         import torch
 
+        assert self.total_steps >= W + 2 * K, "DecodeBench needs total_steps >= W + 2K"
         prof = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(K)]
         for a, b in prof:  # materialise the cudaEvent_t handles
             a.record(self.stream)
@@ -338,20 +343,26 @@ class DecodeBench:
             for i in range(K):
                 flush()  # untimed
                 starts[i].record(self.stream)
-                self.step(W + i, prof[i])
+                self.step(W + i)
                 ends[i].record(self.stream)
             torch.cuda.synchronize(self.device)
         if barrier:
             barrier()
+        for i in range(K):  # launch-only timing pass (same per-step work)
+            flush()
+            self.step(W + K + i, prof[i])
+        torch.cuda.synchronize(self.device)
         step_ms = [s.elapsed_time(e) for s, e in zip(starts, ends)]
         kern_ms = [a.elapsed_time(b) for a, b in prof]
-        alg = kv = 0
+        alg = kv = kalg = 0
         for i in range(K):
             a_b, kv_b = algorithmic_bytes([n + W + i + 1 for n in self.lengths], self.hq, self.hkv, self.d, self.ps)
             alg += a_b
             kv += kv_b
+            kalg += algorithmic_bytes([n + W + K + i + 1 for n in self.lengths], self.hq, self.hkv, self.d,
+                                      self.ps)[0]
         return {"step_ms": step_ms, "kernel_ms": kern_ms, "alg_bytes": alg, "kv_bytes": kv,
-                "tokens": self.B * K, "clocks": clocks.summary(), "launches": K}
+                "kernel_alg_bytes": kalg, "tokens": self.B * K, "clocks": clocks.summary(), "launches": K}
 
     def verify(self, n_sample=32, seed=0):
         """Re-check the last executed step on `n_sample` sequences: every
@@ -637,7 +648,7 @@ def measure(args, config, rank, world, device, dist_ctx, *, steps, warmup, e2e=T
 
     name, lengths, hq, hkv, d, ps = workload(config, rank, world, batch=args.batch, context=args.context,
                                              heads=args.heads)
-    bench = DecodeBench(lengths, hq, hkv, d, ps, total_steps=warmup + steps, device=device, seed=rank,
+    bench = DecodeBench(lengths, hq, hkv, d, ps, total_steps=warmup + 2 * steps, device=device, seed=rank,
                         fragment=args.fragment, waves=args.waves)
     flush = L2Flush(device)
     r = bench.run(warmup, steps, flush, barrier=dist_ctx["barrier"])
@@ -645,7 +656,7 @@ def measure(args, config, rank, world, device, dist_ctx, *, steps, warmup, e2e=T
     sums = dist_ctx["sum"]([float(r["tokens"]), float(r["kv_bytes"]), float(r["alg_bytes"])])
     res = {"name": name, "B": bench.B, "total_ms_max": dist_ctx["max"](total_ms), "tokens_all": sums[0],
            "kv_all": sums[1], "alg_all": sums[2], "kernel_ms_mean": statistics.mean(r["kernel_ms"]),
-           "kernel_alg_bytes_mean": r["alg_bytes"] / steps, "step_ms_mean": total_ms / steps,
+           "kernel_alg_bytes_mean": r["kernel_alg_bytes"] / steps, "step_ms_mean": total_ms / steps,
            "clocks": r["clocks"], "launches": r["launches"], "shape": (hq, hkv, d, ps), "lengths": lengths}
     if check:
         v = bench.verify()

@@ -901,6 +901,14 @@ int plan_decode(const int32_t* nk, const int32_t* row, int64_t nq, int page_size
       }
     }
   }
+  static const int cluster_env = [] {  // experiment knob: force the cluster size (1 = segment schedule)
+    const char* e = std::getenv("PKV_DECODE_CLUSTER");
+    return e ? std::atoi(e) : 0;
+  }();
+  if (cluster_env == 1) cluster = 1;
+  if (cluster_env > 1 && hb == 1 && (cluster_env & (cluster_env - 1)) == 0 && cluster_env <= 16 &&
+      nq * head_items * cluster_env <= num_sms && nq * head_items <= cluster_capacity(cluster_env, num_sms))
+    cluster = cluster_env;
   int32_t* o = out;
   o[H_CLUSTER] = cluster;
   o[H_HB] = hb;
