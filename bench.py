@@ -248,7 +248,8 @@ class DecodeBench:
     call per step (pkv_paged_attention with the fused append).
     tests/test_gpu_bench_parity.py drives this same object."""
 
-    def __init__(self, lengths, hq, hkv, d, ps, *, total_steps, device, seed=0, fragment=False, waves=0):
+    def __init__(self, lengths, hq, hkv, d, ps, *, total_steps, device, seed=0, fragment=False, waves=0,
+                 e2e_steps=None):
         import torch
 
         from paper_2506_07311_b200 import AttentionConfig, _lib
@@ -259,7 +260,8 @@ class DecodeBench:
         self.device, self.total_steps, self.fragment = device, total_steps, fragment
         # tables cover the device phase; the pool keeps room for the e2e
         # phase's page grants
-        self.pool, self.store, _ = build_cache(lengths, hq, hkv, d, ps, extra_tokens=2 * total_steps + 2,
+        e2e_steps = total_steps if e2e_steps is None else e2e_steps
+        self.pool, self.store, _ = build_cache(lengths, hq, hkv, d, ps, extra_tokens=total_steps + e2e_steps + 2,
                                                device=device, seed=seed, fragment=fragment,
                                                reserve_extra=total_steps + 1)
         pool, store = self.pool, self.store

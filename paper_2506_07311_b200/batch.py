@@ -228,6 +228,13 @@ class DecodeBatch:
         return views
 
     @staticmethod
+    def _one_allocation(*tensors) -> bool:
+        """Adjacent host tensors are one copy only if they share a storage
+        (separately pinned buffers may sit back to back by chance)."""
+        base = tensors[0].untyped_storage().data_ptr()
+        return all(t.untyped_storage().data_ptr() == base for t in tensors[1:])
+
+    @staticmethod
     def packed_host_inputs(n, hq, hkv, d, dtype, pin=True):
         """Host buffers for step(): q [n,Hq,D], k_new / v_new [n,Hkv,D] as
         adjacent views of one (pinned) allocation, so the step moves them
@@ -295,7 +302,8 @@ class DecodeBatch:
         kv_shape = (n, cfg.kv_head_count, cfg.head_dim)
         k, k_host, kv_bytes = self._input(k_new, store.torch_dtype, kv_shape, "k_new")
         v, v_host, _ = self._input(v_new, store.torch_dtype, kv_shape, "v_new")
-        if q_host and k_host == q_host + q_bytes and v_host == k_host + kv_bytes and q_t is store.torch_dtype:
+        if q_host and k_host == q_host + q_bytes and v_host == k_host + kv_bytes and q_t is store.torch_dtype \
+                and self._one_allocation(queries, k_new, v_new):
             # q | k | v adjacent in one host buffer (a fused QKV projection's
             # output, planar): ONE host-to-device copy into a packed buffer
             q, k, v = self._packed(q.shape, k.shape, q_t)

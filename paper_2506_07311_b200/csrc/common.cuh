@@ -21,6 +21,13 @@ namespace pkv {
 
 inline int elem_bytes(int dt) { return dt == PKV_F32 ? 4 : 2; }
 
+// Message of a failed runtime call; also clears the (non-sticky) last error
+// so a later launch check does not report this failure again.
+inline const char* cuda_err_str(cudaError_t e) {
+  cudaGetLastError();
+  return cudaGetErrorString(e);
+}
+
 // Launch on the stream's device: entry points may be called while another
 // device is current (a store on cuda:1 driven from a thread whose current
 // device is cuda:0).  The legacy null stream has no device of its own and

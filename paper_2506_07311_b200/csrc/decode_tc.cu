@@ -214,6 +214,13 @@ __device__ __forceinline__ void st_dsmem(float* local, uint32_t rank, float v) {
   asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(a), "r"(rank));
   asm volatile("st.shared::cluster.f32 [%0], %1;" ::"r"(ra), "f"(v) : "memory");
 }
+__device__ __forceinline__ void st_dsmem4(float* local, uint32_t rank, float4 v) {
+  uint32_t a = static_cast<uint32_t>(__cvta_generic_to_shared(local)), ra;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(a), "r"(rank));
+  asm volatile("st.shared::cluster.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(ra), "f"(v.x), "f"(v.y), "f"(v.z),
+               "f"(v.w)
+               : "memory");
+}
 __device__ __forceinline__ uint32_t cluster_rank() {
   uint32_t r;
   asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
@@ -231,48 +238,66 @@ template <int D>
 __device__ __forceinline__ void finish_split_group(const TcParams& p, const int32_t* plan, int comb, int hslot,
                                                    int qi, int qh0, int rows, int tt, int grp, int bar_id,
                                                    int* flag) {
-  __threadfence();
+  // the group's partial stores happen-before the arrival: bar.sync orders
+  // them at CTA scope and thread 0's gpu-scope fence is cumulative
   named_bar(bar_id, grp);
   int* ctr = const_cast<int32_t*>(plan) + plan[H_CTR] + comb * kWarpsTc + hslot;
   const int32_t* c = plan + plan[H_COMB] + comb * kCombInts;
   const int s0 = __ldg(c + 2), ns = __ldg(c + 3);
-  if (tt == 0) *flag = atomicAdd(ctr, 1) == ns - 1;
+  if (tt == 0) {
+    __threadfence();
+    *flag = atomicAdd(ctr, 1) == ns - 1;
+    __threadfence();
+  }
   named_bar(bar_id, grp);
   if (!*flag) return;
-  __threadfence();
   const float2* ml = reinterpret_cast<const float2*>(p.ws_ml);
-  // one pass over the pieces with an online rescale; 16 pieces' (m, l) and
-  // O loads are issued together so the merge costs ~one L2 round trip
+  // one pass over the pieces with an online rescale, four consecutive
+  // elements per thread (16-byte loads); 16 pieces' (m, l) and O loads are
+  // issued together so a block of pieces costs one L2 round trip
+  constexpr int D4 = D / 4;
 #pragma unroll 1
-  for (int e = tt; e < rows * D; e += grp) {
-    const int r = e / D, d = e - r * D;
+  for (int e4 = tt; e4 < rows * D4; e4 += grp) {
+    const int r = e4 / D4, d = (e4 - r * D4) * 4;
     const int qh = qh0 + r;
-    float mx = -INFINITY, den = 0.f, acc = 0.f;
+    float mx = -INFINITY, den = 0.f;
+    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
     for (int sb = 0; sb < ns; sb += 16) {
       float2 mv[16];
-      float ov[16];
+      float4 ov[16];
 #pragma unroll
       for (int u = 0; u < 16; ++u) {
         const bool in = sb + u < ns;
         const int64_t slot = int64_t(s0 + sb + (in ? u : 0)) * p.hq + qh;
         mv[u] = in ? __ldcg(ml + slot) : make_float2(-INFINITY, 0.f);
-        ov[u] = in ? __ldcg(p.ws_o + slot * D + d) : 0.f;
+        ov[u] = in ? __ldcg(reinterpret_cast<const float4*>(p.ws_o + slot * D + d)) : make_float4(0.f, 0.f, 0.f, 0.f);
       }
       float bm = mx;
 #pragma unroll
       for (int u = 0; u < 16; ++u) bm = fmaxf(bm, mv[u].x);
-      const float cr = mx == -INFINITY ? 0.f : exp2f(mx - bm);
+      const float cr = mx == -INFINITY ? 0.f : ex2_ftz(mx - bm);
       den *= cr;
-      acc *= cr;
+      acc.x *= cr;
+      acc.y *= cr;
+      acc.z *= cr;
+      acc.w *= cr;
 #pragma unroll
       for (int u = 0; u < 16; ++u) {
-        const float w = mv[u].x == -INFINITY ? 0.f : exp2f(mv[u].x - bm);
+        const float w = mv[u].x == -INFINITY ? 0.f : ex2_ftz(mv[u].x - bm);
         den += w * mv[u].y;
-        acc += w * ov[u];
+        acc.x += w * ov[u].x;
+        acc.y += w * ov[u].y;
+        acc.z += w * ov[u].z;
+        acc.w += w * ov[u].w;
       }
       mx = bm;
     }
-    store_from_float(p.out, (int64_t(qi) * p.hq + qh) * D + d, p.out_dtype, acc / den);
+    const float inv = 1.f / den;
+    const int64_t o = (int64_t(qi) * p.hq + qh) * D + d;
+    store_from_float(p.out, o, p.out_dtype, acc.x * inv);
+    store_from_float(p.out, o + 1, p.out_dtype, acc.y * inv);
+    store_from_float(p.out, o + 2, p.out_dtype, acc.z * inv);
+    store_from_float(p.out, o + 3, p.out_dtype, acc.w * inv);
   }
   if (tt == 0) *ctr = 0;  // self-cleaning: the plan buffer can be replayed
 }
@@ -292,8 +317,12 @@ __global__ void __launch_bounds__(kThreadsTc, 1) decode_tc_kernel(const __grid_c
   __shared__ int s_flag[kWarpsTc];  // per head: this CTA's piece merges the split
   // cluster mode: the slices of the unit's pieces pushed here by every CTA of
   // the cluster (unnormalised O, then row max / row sum per piece)
-  __shared__ float r_o[kMergeRows * 128 + 16];
+  __shared__ __align__(16) float r_o[kMergeRows * 128 + 64];
   __shared__ float r_ml[16 * kMergeRows * 2];
+  __shared__ float s_wgt[kWarpsTc * kMergeRows];       // intra-CTA merge weights per (warp, row)
+  __shared__ float s_rml[kWarpsTc * kMergeRows * 2];   // per head group: row (max, sum)
+  __shared__ float s_cw[16 * kMergeRows];              // cluster merge weights per (rank, row)
+  __shared__ float s_cinv[kMergeRows];
   __shared__ int32_t s_cta_items[kCtaItemsSmem * kItemInts];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const bool trace_on = g_trace_on != 0;
@@ -427,8 +456,12 @@ __global__ void __launch_bounds__(kThreadsTc, 1) decode_tc_kernel(const __grid_c
   };
 
   start_item();
+  trace(24);  // prologue stamps (slots 24-26 are free when a warp runs <= 5 items)
+  issue_next();
+  trace(25);
 #pragma unroll
-  for (int i = 0; i < kStagesTc - 1; ++i) issue_next();
+  for (int i = 1; i < kStagesTc - 1; ++i) issue_next();
+  trace(26);
 
   // ======================= consumer ======================================
   long long gcons = 0;
@@ -638,34 +671,61 @@ __global__ void __launch_bounds__(kThreadsTc, 1) decode_tc_kernel(const __grid_c
     trace(5 + 4 * int(k));
     const int w0 = head_local * pv.wph;
     const int E = C.rows * D;
-    const int slice = cluster > 1 ? (E + cluster - 1) / cluster : E;
+    // slice of the rows x D block each cluster CTA merges (multiple of 4)
+    const int slice = cluster > 1 ? ((E + cluster - 1) / cluster + 3) & ~3 : E;
     const uint32_t my_rank = cluster > 1 ? cluster_rank() : 0u;
     if (cluster > 1) cluster_wait();  // every peer runs: its shared memory may be written
-#pragma unroll 1
-    for (int e = tt; e < E; e += grp) {
-      const int r = e / D, d = e - r * D;
+    // per (row, warp) weights and per-row (max, sum), once per row instead
+    // of once per element
+    if (tt < C.rows) {
+      const int r = tt;
       float mx = -INFINITY;
       for (int w = w0; w < w0 + pv.wph; ++w) mx = fmaxf(mx, s_ml[(w * kMergeRows + r) * 2]);
-      float den = 0.f, acc = 0.f;
+      float den = 0.f;
       for (int w = w0; w < w0 + pv.wph; ++w) {
         const float mw = s_ml[(w * kMergeRows + r) * 2];
-        const float wgt = mw == -INFINITY ? 0.f : exp2f(mw - mx);
+        const float wgt = mw == -INFINITY ? 0.f : ex2_ftz(mw - mx);
+        s_wgt[w * kMergeRows + r] = wgt;
         den += wgt * s_ml[(w * kMergeRows + r) * 2 + 1];
-        acc += wgt * s_mo[(w * kMergeRows + r) * D + d];
       }
-      if (cluster > 1) {  // push the element to the CTA that merges its slice
+      s_rml[(w0 * kMergeRows + r) * 2] = mx;
+      s_rml[(w0 * kMergeRows + r) * 2 + 1] = den;
+      if (cluster > 1)  // the row's max / sum to every peer
+        for (int c = 0; c < cluster; ++c) {
+          st_dsmem(&r_ml[(my_rank * kMergeRows + r) * 2], c, mx);
+          st_dsmem(&r_ml[(my_rank * kMergeRows + r) * 2 + 1], c, den);
+        }
+    }
+    named_bar(bar_id, grp);
+    trace(27);
+    constexpr int D4 = D / 4;
+#pragma unroll 1
+    for (int e4 = tt; e4 < C.rows * D4; e4 += grp) {
+      const int r = e4 / D4, d = (e4 - r * D4) * 4;
+      float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+      for (int w = w0; w < w0 + pv.wph; ++w) {
+        const float wgt = s_wgt[w * kMergeRows + r];
+        const float4 v = *reinterpret_cast<const float4*>(s_mo + (w * kMergeRows + r) * D + d);
+        acc.x += wgt * v.x;
+        acc.y += wgt * v.y;
+        acc.z += wgt * v.z;
+        acc.w += wgt * v.w;
+      }
+      const int e = r * D + d;
+      if (cluster > 1) {  // push the 4 elements to the CTA that merges their slice
         const int owner = e / slice;
-        st_dsmem(&r_o[my_rank * slice + (e - owner * slice)], owner, acc);
-        if (d == 0)  // and the row's max / sum to every peer
-          for (int c = 0; c < cluster; ++c) {
-            st_dsmem(&r_ml[(my_rank * kMergeRows + r) * 2], c, mx);
-            st_dsmem(&r_ml[(my_rank * kMergeRows + r) * 2 + 1], c, den);
-          }
+        st_dsmem4(&r_o[my_rank * slice + (e - owner * slice)], owner, acc);
       } else if (C.slot < 0) {
-        store_from_float(p.out, out_base + int64_t(r) * D + d, p.out_dtype, acc / den);
+        const float inv = 1.f / s_rml[(w0 * kMergeRows + r) * 2 + 1];
+        store_from_float(p.out, out_base + e, p.out_dtype, acc.x * inv);
+        store_from_float(p.out, out_base + e + 1, p.out_dtype, acc.y * inv);
+        store_from_float(p.out, out_base + e + 2, p.out_dtype, acc.z * inv);
+        store_from_float(p.out, out_base + e + 3, p.out_dtype, acc.w * inv);
       } else {
-        __stcg(p.ws_o + (pslot + r) * D + d, acc);
-        if (d == 0) __stcg(reinterpret_cast<float2*>(p.ws_ml) + pslot + r, make_float2(mx, den));
+        __stcg(reinterpret_cast<float4*>(p.ws_o + (pslot + r) * D + d), acc);
+        if (d == 0)
+          __stcg(reinterpret_cast<float2*>(p.ws_ml) + pslot + r,
+                 make_float2(s_rml[(w0 * kMergeRows + r) * 2], s_rml[(w0 * kMergeRows + r) * 2 + 1]));
       }
     }
     trace(28);
@@ -676,19 +736,37 @@ __global__ void __launch_bounds__(kThreadsTc, 1) decode_tc_kernel(const __grid_c
       // 1/cluster slice of the rows x D outputs from LOCAL shared memory, in
       // rank order.  No peer touches this CTA's memory after the barrier.
       asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;\n" ::: "memory");
-      const int e0 = static_cast<int>(my_rank) * slice, e1 = min(E, e0 + slice);
-      for (int e = e0 + static_cast<int>(threadIdx.x); e < e1; e += kThreadsTc) {
-        const int r = e / D;
+      if (threadIdx.x < C.rows) {  // per (rank, row) weights once
+        const int r = threadIdx.x;
         float mx = -INFINITY;
         for (int c = 0; c < cluster; ++c) mx = fmaxf(mx, r_ml[(c * kMergeRows + r) * 2]);
-        float den = 0.f, acc = 0.f;
+        float den = 0.f;
         for (int c = 0; c < cluster; ++c) {
           const float mw = r_ml[(c * kMergeRows + r) * 2];
-          const float w = mw == -INFINITY ? 0.f : exp2f(mw - mx);
+          const float w = mw == -INFINITY ? 0.f : ex2_ftz(mw - mx);
+          s_cw[c * kMergeRows + r] = w;
           den += w * r_ml[(c * kMergeRows + r) * 2 + 1];
-          acc += w * r_o[c * slice + (e - e0)];
         }
-        store_from_float(p.out, out_base + e, p.out_dtype, acc / den);
+        s_cinv[r] = 1.f / den;
+      }
+      __syncthreads();
+      const int e0 = static_cast<int>(my_rank) * slice, e1 = min(E, e0 + slice);
+      for (int e = e0 + 4 * static_cast<int>(threadIdx.x); e < e1; e += 4 * kThreadsTc) {
+        const int r = e / D;
+        float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+        for (int c = 0; c < cluster; ++c) {
+          const float w = s_cw[c * kMergeRows + r];
+          const float4 v = *reinterpret_cast<const float4*>(&r_o[c * slice + (e - e0)]);
+          acc.x += w * v.x;
+          acc.y += w * v.y;
+          acc.z += w * v.z;
+          acc.w += w * v.w;
+        }
+        const float inv = s_cinv[r];
+        store_from_float(p.out, out_base + e, p.out_dtype, acc.x * inv);
+        store_from_float(p.out, out_base + e + 1, p.out_dtype, acc.y * inv);
+        store_from_float(p.out, out_base + e + 2, p.out_dtype, acc.z * inv);
+        store_from_float(p.out, out_base + e + 3, p.out_dtype, acc.w * inv);
       }
       break;  // one item per CTA in cluster mode
     }
@@ -1082,7 +1160,7 @@ int launch_decode_tc(TcParams p, const int32_t* plan_host, int kv_dtype, int hea
   {
     const cudaError_t e = ensure_smem(reinterpret_cast<const void*>(fn), smem);
     if (e != cudaSuccess)
-      return fail(PKV_CUDA_ERROR, "decode_tc smem attribute (%d B): %s", smem, cudaGetErrorString(e));
+      return fail(PKV_CUDA_ERROR, "decode_tc smem attribute (%d B): %s", smem, pkv::cuda_err_str(e));
   }
   const int grid = plan_host[H_GRID];  // the planner's assignment is per CTA
   const int cluster = plan_host[H_CLUSTER];
@@ -1119,7 +1197,7 @@ int launch_decode_tc(TcParams p, const int32_t* plan_host, int kv_dtype, int hea
   }
   if (e != cudaSuccess)
     return fail(PKV_CUDA_ERROR, "decode_tc launch: %s (grid %d cluster %d smem %d nq %d key %d)",
-                cudaGetErrorString(e), grid, cluster, smem, p.nq, key);
+                pkv::cuda_err_str(e), grid, cluster, smem, p.nq, key);
   return PKV_OK;
 }
 
@@ -1137,7 +1215,7 @@ int debug_trace(int enable, uint64_t* out, int64_t n) {
     cudaMemcpyFromSymbol(out, g_trace, m * sizeof(unsigned long long));
   }
   cudaError_t e = cudaGetLastError();
-  return e == cudaSuccess ? PKV_OK : fail(PKV_CUDA_ERROR, "debug trace: %s", cudaGetErrorString(e));
+  return e == cudaSuccess ? PKV_OK : fail(PKV_CUDA_ERROR, "debug trace: %s", pkv::cuda_err_str(e));
 }
 
 }  // namespace pkv

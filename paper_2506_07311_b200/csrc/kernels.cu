@@ -820,7 +820,7 @@ static int decode_step_stage(pkv_step_stage_args* a, cudaStream_t stream, pkv_ap
   a->launches = 0;
   if (a->slot_event) {  // the slot's previous upload has landed
     cudaError_t e = cudaEventSynchronize(static_cast<cudaEvent_t>(a->slot_event));
-    if (e != cudaSuccess) return pkv::fail(PKV_CUDA_ERROR, "slot event: %s", cudaGetErrorString(e));
+    if (e != cudaSuccess) return pkv::fail(PKV_CUDA_ERROR, "slot event: %s", pkv::cuda_err_str(e));
   }
   stamp(2);
   const int64_t n = a->n;
@@ -902,7 +902,7 @@ static int decode_step_stage(pkv_step_stage_args* a, cudaStream_t stream, pkv_ap
   cudaError_t e = cudaMemcpyAsync(a->meta_dev, a->meta_host, static_cast<size_t>(total) * 4,
                                   cudaMemcpyHostToDevice, stream);
   if (e != cudaSuccess)
-    return fail_back(pkv::fail(PKV_CUDA_ERROR, "step metadata upload: %s", cudaGetErrorString(e)));
+    return fail_back(pkv::fail(PKV_CUDA_ERROR, "step metadata upload: %s", pkv::cuda_err_str(e)));
   if (a->slot_event) cudaEventRecord(static_cast<cudaEvent_t>(a->slot_event), stream);
   stamp(5);
   if (page_work || n_pairs) {
@@ -913,7 +913,7 @@ static int decode_step_stage(pkv_step_stage_args* a, cudaStream_t stream, pkv_ap
                                 a->meta_dev + zero_off, n_zero, a->meta_dev + trip_off, n_copies,
                                 a->mirror_dev, a->meta_dev + pairs_off, n_pairs, a->row_bytes, a->page_size);
     const cudaError_t le = cudaGetLastError();
-    if (le != cudaSuccess) return fail_back(pkv::fail(PKV_CUDA_ERROR, "step aux kernel: %s", cudaGetErrorString(le)));
+    if (le != cudaSuccess) return fail_back(pkv::fail(PKV_CUDA_ERROR, "step aux kernel: %s", pkv::cuda_err_str(le)));
     ++a->launches;
   }
   stamp(6);
@@ -935,7 +935,7 @@ int pkv_paged_attention(const pkv_attention_args* a, void* stream_) {
     if (!a->meta_dev) return pkv::fail(PKV_VALUE_ERROR, "meta_host without meta_dev");
     cudaError_t e = cudaMemcpyAsync(a->meta_dev, a->meta_host, static_cast<size_t>(a->meta_bytes),
                                     cudaMemcpyHostToDevice, stream);
-    if (e != cudaSuccess) return pkv::fail(PKV_CUDA_ERROR, "metadata upload: %s", cudaGetErrorString(e));
+    if (e != cudaSuccess) return pkv::fail(PKV_CUDA_ERROR, "metadata upload: %s", pkv::cuda_err_str(e));
   }
   if (a->n_queries <= 0) return PKV_OK;
   if (a->hq <= 0 || a->hkv <= 0 || a->hq % a->hkv)
@@ -1103,7 +1103,7 @@ int pkv_decode_step(pkv_step_stage_args* stage, pkv_attention_args* attn, pkv_de
     if (!dst || bytes <= 0) return pkv::fail(PKV_VALUE_ERROR, "%s: host source without device buffer", what);
     cudaError_t e = cudaMemcpyAsync(const_cast<void*>(dst), src, static_cast<size_t>(bytes),
                                     cudaMemcpyHostToDevice, stream);
-    return e == cudaSuccess ? PKV_OK : pkv::fail(PKV_CUDA_ERROR, "%s upload: %s", what, cudaGetErrorString(e));
+    return e == cudaSuccess ? PKV_OK : pkv::fail(PKV_CUDA_ERROR, "%s upload: %s", what, pkv::cuda_err_str(e));
   };
   if (io) {
     int st = h2d(io->q_host, attn->q, io->q_bytes, "q");
@@ -1153,7 +1153,7 @@ int pkv_decode_step(pkv_step_stage_args* stage, pkv_attention_args* attn, pkv_de
       if (io->out_bytes <= 0) return pkv::fail(PKV_VALUE_ERROR, "out_host without out_bytes");
       cudaError_t e = cudaMemcpyAsync(io->out_host, attn->out, static_cast<size_t>(io->out_bytes),
                                       cudaMemcpyDeviceToHost, stream);
-      if (e != cudaSuccess) return pkv::fail(PKV_CUDA_ERROR, "output download: %s", cudaGetErrorString(e));
+      if (e != cudaSuccess) return pkv::fail(PKV_CUDA_ERROR, "output download: %s", pkv::cuda_err_str(e));
     }
     io->launched = 1;
   }

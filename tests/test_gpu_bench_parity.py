@@ -30,10 +30,11 @@ pytestmark = pytest.mark.gpu
 BF16_TOL = 2e-2
 
 
-def _bench(config, steps, fragment=False):
+def _bench(config, steps, fragment=False, e2e_steps=None):
     _, lengths, hq, hkv, d, ps = bench.workload(config, 0, 1)
     dev = torch.device("cuda", 0)
-    b = bench.DecodeBench(lengths, hq, hkv, d, ps, total_steps=steps, device=dev, seed=0, fragment=fragment)
+    b = bench.DecodeBench(lengths, hq, hkv, d, ps, total_steps=steps, device=dev, seed=0, fragment=fragment,
+                          e2e_steps=e2e_steps)
     for t in range(steps):
         b.step(t)
     torch.cuda.synchronize()
@@ -113,7 +114,7 @@ def test_bench_e2e_path_grants_pages_and_stays_correct():
     from paper_2506_07311_b200.batch import DecodeBatch
 
     steps = 2
-    b = _bench("c2", steps)
+    b = _bench("c2", steps, e2e_steps=24)
     e = b.run_e2e(1, 20, lambda: None)
     assert e["pages_granted"] > 0
     for s in range(b.B):

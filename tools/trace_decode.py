@@ -33,6 +33,19 @@ flush = torch.ones(64 << 20, device=dev)
 if not os.environ.get("WARM"):
     flush.sum()
 torch.cuda.synchronize()
+# event time of the same launch (cold L2), for comparison with the in-kernel span
+ev = []
+for _ in range(10):
+    flush.sum()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    paged_attention(q, store, meta, cfg)
+    e1.record()
+    torch.cuda.synchronize()
+    ev.append(e0.elapsed_time(e1) * 1e3)
+print("event-timed paged_attention (us): median %.1f min %.1f" % (np.median(ev), np.min(ev)))
+flush.sum()
+torch.cuda.synchronize()
 lib.pkv_debug_trace(1, None, 0)
 paged_attention(q, store, meta, cfg)
 torch.cuda.synchronize()
@@ -44,6 +57,8 @@ t = np.array(buf, dtype=np.float64).reshape(256, 8, 32)[:148]
 t0 = t[:, :, 0][t[:, :, 0] > 0].min()
 rel = np.where(t > 0, (t - t0) / 1000.0, np.nan)
 print("kernel span (us): %.1f   plan done median %.2f" % (np.nanmax(rel[:, :, 31]), np.nanmedian(rel[:, :, 1])))
+print("prologue medians: start_item %.2f  first issue %.2f  prologue issued %.2f  | merge: stored %.2f  "
+      "cluster_wait %.2f  pushed %.2f  end %.2f" % tuple(np.nanmedian(rel[:, :, s]) for s in (24, 25, 26, 5, 27, 28, 31)))
 gaps = {"start->first data": [], "first data->chunks done": [], "chunks done->stored": [],
         "stored->next start": []}
 for c in range(148):
