@@ -37,6 +37,35 @@ _ZERO_COPY_OUT = _os.environ.get("PKV_ZERO_COPY_OUT", "1") != "0"
 _ZERO_COPY_IN = _os.environ.get("PKV_ZERO_COPY_IN", "0") == "1"
 
 
+class _FastStep:
+    """A repeatable step() call: the caller's buffers (held here, so their ids
+    stay theirs) and private copies of the argument blocks the first call
+    filled.  Valid while the same objects keep the same storage and the
+    batch's membership, attached stores and staging buffers are unchanged."""
+
+    __slots__ = ("tensors", "ptrs", "args", "args_p", "io", "io_p", "result", "out_host", "out_dev", "tensor",
+                 "mirror", "fixed", "nstores", "bufs")
+
+    def __init__(self, batch, tensors, result, out_host, out_dev, tensor):
+        self.tensors = tensors
+        self.ptrs = tuple(t.data_ptr() for t in tensors)
+        self.args = _lib.AttentionArgs.from_buffer_copy(batch._args)
+        self.args_p = C.byref(self.args)
+        self.io = _lib.DecodeIO.from_buffer_copy(batch._io)
+        self.io_p = C.byref(self.io)
+        self.result, self.out_host, self.out_dev, self.tensor = result, out_host, out_dev, tensor
+        self.mirror = batch._stage_mirror
+        self.fixed = batch._stage_fixed
+        self.nstores = len(batch.pool._stores)
+        self.bufs = batch._bufs
+
+    def valid(self, batch, q, k, v, out) -> bool:
+        t = self.tensors
+        return (q is t[0] and k is t[1] and v is t[2] and out is t[3] and self.bufs is batch._bufs
+                and self.fixed == batch._stage_fixed and self.nstores == len(batch.pool._stores)
+                and (q.data_ptr(), k.data_ptr(), v.data_ptr(), out.data_ptr()) == self.ptrs)
+
+
 class DecodeBatch:
     """Decode B sequences of one pool together.
 
@@ -78,6 +107,8 @@ class DecodeBatch:
         self._bufs = {}
         self._keep = []
         self._store_ptrs = {}
+        self._fast = {}
+        self._dev_index = self.device.index if self.device.index is not None else torch.cuda.current_device()
         self.set_sequences(seq_ids, capacity)
 
     def set_sequences(self, seq_ids, capacity: int | None = None) -> None:
@@ -114,6 +145,7 @@ class DecodeBatch:
             self._bufs = {}
         self._ring_ptrs = [(h.data_ptr(), d.data_ptr(), e.cuda_event) for h, d, e in self._ring]
         self._members = object()  # invalidates the cached stage fields
+        self._fast = {}
         self._slot = 0
         self._cur = None
         self._args.n_queries = self.n
@@ -251,15 +283,19 @@ class DecodeBatch:
     def _input(self, x, dtype, shape, name):
         """-> (device tensor, host pointer or None, bytes).  CPU inputs are
         copied by the native step into a persistent device buffer (pin them
-        for an asynchronous copy); device inputs are used in place."""
+        for an asynchronous copy); device inputs are used in place.  Records
+        in self._direct whether the caller's own buffer is used (no
+        conversion copy), which makes the call repeatable by _step_fast."""
         import torch
 
         if type(x) is torch.Tensor and x.dtype is dtype and not x.is_cuda and x.shape == shape \
                 and x.is_contiguous():  # fast path: a host tensor ready to copy
             self._keep.append(x)
+            self._direct.append(True)
             if _ZERO_COPY_IN and x.is_pinned():
                 return x, None, 0  # the kernel reads the mapped host rows itself
             return self._buffer(name, shape, dtype), x.data_ptr(), x.nbytes
+        self._direct.append(False)
         if not isinstance(x, torch.Tensor):
             x = torch.from_numpy(np.ascontiguousarray(x))
         if tuple(x.shape) != shape:
@@ -271,11 +307,94 @@ class DecodeBatch:
             return self._buffer(name, shape, dtype), x.data_ptr(), x.numel() * x.element_size()
         if x.device != self.device or x.dtype != dtype or not x.is_contiguous():
             x = x.to(device=self.device, dtype=dtype, non_blocking=True).contiguous()
+            return x, None, 0
+        self._direct[-1] = True
         return x, None, 0
 
-    @on_device(_self_device)
     def step(self, queries, k_new, v_new, *, out=None, out_dtype=None, layer: int = 0, advance: bool = True,
              precision: str = "auto"):
+        """Append one token per sequence into `stores[layer]` and attend.
+
+        queries [B, Hq, D]; k_new / v_new [B, Hkv, D] (numpy or torch, any
+        device).  With `advance` (the default) the whole step — copies of CPU
+        inputs, allocator + plan + metadata upload, page work, the fused
+        append + decode launch and the copy into a CPU `out` — is ONE native
+        call (pkv_decode_step).  `out` (optional) is a [B, Hq, D] tensor the
+        result is written to: on the device, or on the host (pinned: the
+        copy is asynchronous on the current stream, synchronise before
+        reading it, as with a non_blocking torch copy).
+
+        A serving loop calls this with the same input / output buffers every
+        token; such a repeated call (same tensor objects, same storage) skips
+        the argument checks and marshalling and re-uses the argument blocks
+        prepared by the first call (`_FastStep`)."""
+        if out is not None and advance:
+            e = self._fast.get((id(queries), id(k_new), id(v_new), id(out), layer, precision))
+            if e is not None and e.valid(self, queries, k_new, v_new, out):
+                return self._step_fast(e)
+        return self._step_full(queries, k_new, v_new, out=out, out_dtype=out_dtype, layer=layer,
+                               advance=advance, precision=precision)
+
+    def _step_fast(self, e):
+        import torch
+
+        if torch.cuda.current_device() != self._dev_index:
+            with torch.cuda.device(self.device):
+                return self._step_fast(e)
+        sp = torch._C._cuda_getCurrentRawStream(self._dev_index)
+        slot = self._slot
+        self._slot = (slot + 1) % len(self._ring)
+        st_args = self._stage
+        st_args.meta_host, st_args.meta_dev, st_args.slot_event = self._ring_ptrs[slot]
+        mirror = self.pool._mirror
+        if mirror is not self._stage_mirror:  # re-exported mirror: refresh the table fields
+            self._stage_setup_mirror()
+        if e.mirror is not self._stage_mirror:
+            e.args.block_table, e.args.bt_stride = st_args.mirror_dev, st_args.mirror_cols
+            e.mirror = self._stage_mirror
+        st = self._lib.pkv_decode_step(self._stage_p, e.args_p, e.io_p, C.c_void_p(sp))
+        if st:
+            _lib.check(st, "pkv_decode_step")
+        self._cur = slot
+        self._used.value = st_args.meta_used
+        if st_args.needs_resync or not e.io.launched:  # block-table shape change: the general path
+            self._stage_finish_resync(e, sp)
+        else:
+            self.last_launches = e.io.launches
+        return e.result
+
+    def _stage_setup_mirror(self):
+        a = self._stage
+        mirror = self.pool._mirror
+        if mirror is None or mirror.device != self.device:
+            mirror = self.pool.device_table(self.device)
+        if mirror is not self._stage_mirror:
+            a.mirror_dev, a.mirror_rows, a.mirror_cols = mirror.data_ptr(), mirror.shape[0], mirror.shape[1]
+            self._stage_mirror = mirror
+
+    def _stage_finish_resync(self, e, sp):
+        """Fast-path tail after a block-table shape change: full mirror
+        re-export, then the attention launch on it (as in _step_full)."""
+        if self._stage.needs_resync:
+            self.pool.device_table(self.device)
+        launches = self._stage.launches
+        if not e.io.launched:
+            mirror = self.pool.device_table(self.device)
+            e.args.block_table, e.args.bt_stride = mirror.data_ptr(), mirror.shape[1]
+            e.mirror = None
+            st = self._lib.pkv_paged_attention(e.args_p, C.c_void_p(sp))
+            if st:
+                _lib.check(st, "pkv_paged_attention")
+            if e.out_host is not None:
+                e.out_host.copy_(e.out_dev, non_blocking=True)
+            launches += 1 if e.tensor else 4
+        else:
+            launches = e.io.launches
+        self.last_launches = launches
+
+    @on_device(_self_device)
+    def _step_full(self, queries, k_new, v_new, *, out=None, out_dtype=None, layer: int = 0, advance: bool = True,
+                   precision: str = "auto"):
         """Append one token per sequence into `stores[layer]` and attend.
 
         queries [B, Hq, D]; k_new / v_new [B, Hkv, D] (numpy or torch, any
@@ -292,10 +411,12 @@ class DecodeBatch:
         if not advance or not self._native_pages():
             return self._step_split(queries, k_new, v_new, out=out, out_dtype=out_dtype, layer=layer,
                                     advance=advance, precision=precision, sp=sp)
+        fast_key = (id(queries), id(k_new), id(v_new), id(out), layer, precision) if out is not None else None
         store: KvStore = self.stores[layer]
         cfg = self.config
         n = self.n
         self._keep = []
+        self._direct = []
         qd = queries.dtype if isinstance(queries, torch.Tensor) else None
         q_t = qd if qd in self._qcodes else torch.float32
         q, q_host, q_bytes = self._input(queries, q_t, (n, cfg.head_count, cfg.head_dim), "queries")
@@ -363,6 +484,16 @@ class DecodeBatch:
         else:
             launches = io.launches
         self.last_launches = launches
+        if fast_key is not None and all(type(x) is torch.Tensor for x in (queries, k_new, v_new)):
+            # every buffer used in place (host pointer or device tensor of the
+            # caller's own objects): later calls with these objects skip to
+            # _step_fast with a private copy of the argument blocks
+            if all(self._direct) and (o is out or out_host is out):
+                tensor = (store.dtype_code == _lib.PKV_BF16 and precision != "exact") or precision == "tensor"
+                if len(self._fast) >= 16:
+                    self._fast.clear()
+                self._fast[fast_key] = _FastStep(self, (queries, k_new, v_new, out), result, out_host, o,
+                                                 tensor)
         return result
 
     def _step_split(self, queries, k_new, v_new, *, out, out_dtype, layer, advance, precision, sp):

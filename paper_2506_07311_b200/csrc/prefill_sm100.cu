@@ -268,6 +268,12 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int nt[2] = {it[7], it[8]};
   const int n_tiles = max(nt[0], nt[1]);
 
+  if (p.dbg && threadIdx.x == 0) {  // per-CTA record: start, first S, end, SM
+    p.dbg[512 + 4 * blockIdx.x] = gtime();
+    uint32_t smid;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+    p.dbg[512 + 4 * blockIdx.x + 3] = smid;
+  }
   if (threadIdx.x == 0) {
     mbar_init(bar(B_Q), 1);
     for (int s = 0; s < 2; ++s) {
@@ -396,6 +402,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_wait(bar(B_SF + t), j & 1);
       tc_fence_after();
       if (r == 0 && j < 64) PDBG(t * 64 + j);
+      if (p.dbg && r == 0 && t == 0 && j == 0) p.dbg[512 + 4 * blockIdx.x + 1] = gtime();
       const int kbase = j * kN;
       // diagonal / tail tiles take the masked code path (warp-uniform branch)
       const bool masked = __any_sync(0xffffffffu, kbase + kN > nk);
@@ -501,6 +508,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
   tc_fence_before();
   __syncthreads();
+  if (p.dbg && threadIdx.x == 0) p.dbg[512 + 4 * blockIdx.x + 2] = gtime();
   if (warp == 2) {
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "r"(kTmemCols)

@@ -366,6 +366,61 @@ def test_host_buffer_step_single_native_call(dtype, precision):
         assert torch.equal(kk, ctx[i][0]) and torch.equal(vv, ctx[i][1])
 
 
+@pytest.mark.parametrize("packed", [False, True])
+def test_repeated_buffers_take_the_fast_path(packed):
+    """A serving loop re-using the same pinned host q/k/v and `out` every
+    token: after the first call step() replays the prepared argument blocks
+    (_FastStep).  Results stay exact across page grants, the block-table
+    shape change (mirror re-export) and buffer contents rewritten in place;
+    new buffer objects or a membership change drop back to the full path."""
+    hq, hkv, d, ps = 16, 4, 128, 8
+    dtype = torch.bfloat16
+    pool = PagePool(512, ps)
+    store = KvStore(pool, hkv, d, dtype=dtype)
+    cfg = AttentionConfig(head_count=hq, head_dim=d, page_size=ps, kv_head_count=hkv)
+    gen = torch.Generator(device="cuda").manual_seed(5)
+    lengths = [6, 15, 40]
+    ctx = []
+    for s, n in enumerate(lengths):
+        pool.reserve(s, n)
+        k = torch.randn((n, hkv, d), generator=gen, device="cuda").to(dtype)
+        v = torch.randn((n, hkv, d), generator=gen, device="cuda").to(dtype)
+        store.assign(s, np.arange(n), k, v)
+        ctx.append([k, v])
+    B = 3
+    batch = DecodeBatch(store, list(range(B)), cfg)
+    if packed:
+        qh, kh, vh = DecodeBatch.packed_host_inputs(B, hq, hkv, d, dtype)
+    else:
+        qh, kh, vh = (torch.empty(s, dtype=dtype).pin_memory() for s in ((B, hq, d), (B, hkv, d), (B, hkv, d)))
+    out_h = torch.empty((B, hq, d), dtype=torch.float32).pin_memory()
+    for step in range(40):
+        q = torch.randn((B, hq, d), generator=gen, device="cuda").to(dtype)
+        kn = torch.randn((B, hkv, d), generator=gen, device="cuda").to(dtype)
+        vn = torch.randn((B, hkv, d), generator=gen, device="cuda").to(dtype)
+        qh.copy_(q)
+        kh.copy_(kn)
+        vh.copy_(vn)
+        assert batch.step(qh, kh, vh, out=out_h) is out_h
+        torch.cuda.current_stream().synchronize()
+        if step >= 1:
+            assert len(batch._fast) == 1
+        for i in range(B):
+            ctx[i][0] = torch.cat([ctx[i][0], kn[i:i + 1]])
+            ctx[i][1] = torch.cat([ctx[i][1], vn[i:i + 1]])
+            k = ctx[i][0].double().repeat_interleave(hq // hkv, 1)
+            v = ctx[i][1].double().repeat_interleave(hq // hkv, 1)
+            p = torch.softmax(torch.einsum("hd,lhd->hl", q[i].double(), k) * cfg.scale, -1)
+            ref = torch.einsum("hl,lhd->hd", p, v)
+            assert relative_error(out_h[i].numpy(), ref.cpu().numpy()) <= 6e-3, (step, i)
+    for i in range(B):
+        kk, vv = store.gather(i, ctx[i][0].shape[0])
+        assert torch.equal(kk, ctx[i][0]) and torch.equal(vv, ctx[i][1])
+    # a membership change invalidates the prepared calls
+    batch.set_sequences([0, 1])
+    assert not batch._fast
+
+
 def test_step_mixed_row_sizes_uses_split_path():
     """Stores of different row sizes on one pool: step() falls back to the
     two-call form (page work through the stores) and stays correct."""

@@ -60,12 +60,33 @@ def main():
                              plan=dplan.data_ptr(), n_items=plan.shape[0])
         sp = _stream(dev)
         if os.environ.get("PF_DEBUG"):
-            dbg = torch.zeros(512, dtype=torch.int64, device=dev)
+            dbg = torch.zeros(512 + 4 * plan.shape[0], dtype=torch.int64, device=dev)
             a.debug = dbg.data_ptr()
             _lib.check(lib.pkv_paged_prefill(C.byref(a), sp))
             torch.cuda.synchronize()
-            t = dbg.cpu().numpy().astype(np.float64)
-            t0 = t[t > 0].min()
+            full = dbg.cpu().numpy()
+            cta = full[512:].reshape(-1, 4).astype(np.float64)
+            t = full[:512].astype(np.float64)
+            t0 = min(t[t > 0].min(), cta[:, 0].min())
+            span = (cta[:, 2].max() - cta[:, 0].min()) / 1e3
+            dur = (cta[:, 2] - cta[:, 0]) / 1e3
+            first = (cta[:, 1] - cta[:, 0]) / 1e3
+            ntiles = np.maximum(plan[:, 7], plan[:, 8]).astype(np.float64)
+            A = np.stack([np.ones_like(ntiles), ntiles], 1)
+            coef = np.linalg.lstsq(A, dur, rcond=None)[0]
+            nsm = len(np.unique(cta[:, 3]))
+            busy = dur.sum() / (span * nsm)
+            # idle gap between consecutive CTAs on the same SM
+            gaps = []
+            for sm in np.unique(cta[:, 3]):
+                rr = cta[cta[:, 3] == sm]
+                rr = rr[np.argsort(rr[:, 0])]
+                gaps += list((rr[1:, 0] - rr[:-1, 2]) / 1e3)
+            print(json.dumps({"span_us": round(span, 1), "sms": int(nsm), "busy_frac": round(float(busy), 3),
+                              "per_item_us": round(float(coef[0]), 2), "per_tile_us": round(float(coef[1]), 3),
+                              "first_S_us_median": round(float(np.median(first)), 2),
+                              "gap_us_median": round(float(np.median(gaps)), 2) if gaps else None,
+                              "tail_us": round(float((cta[:, 2].max() - np.percentile(cta[:, 2], 50)) / 1e3), 1)}))
             rel = np.where(t > 0, (t - t0) / 1e3, np.nan)
             print("item 0:", plan[0].tolist())
             for name, off in (("S_A ready", 0), ("S_B ready", 64), ("P_A done", 128), ("P_B done", 192),
