@@ -72,16 +72,38 @@ __device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
 __device__ __forceinline__ void mbar_arrive(uint32_t bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(bar) : "memory");
 }
+__device__ __forceinline__ unsigned long long gtime();
+// Debug builds (-DPKV_K3_WATCHDOG): a wait that has not completed after ~4 s
+// is a scheduling bug: report the barrier and trap instead of hanging the
+// device.  Off by default: the extra registers in every inlined wait cost
+// ~14% of K3 throughput (measured).
+__device__ __noinline__ void mbar_hang(uint32_t bar, uint32_t parity) {
+  printf("pkv K3: mbarrier wait timed out (smem 0x%x parity %u) block %d thread %d\n", bar, parity,
+         static_cast<int>(blockIdx.x), static_cast<int>(threadIdx.x));
+  asm volatile("trap;");
+}
 __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
   uint32_t done = 0;
-  do {
+#ifdef PKV_K3_WATCHDOG
+  uint32_t spins = 0;
+  unsigned long long t0 = 0;
+#endif
+  for (;;) {
     asm volatile(
         "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
         " selp.u32 %0, 1, 0, p;\n}\n"
         : "=r"(done)
         : "r"(bar), "r"(parity)
         : "memory");
-  } while (!done);
+    if (done) return;
+#ifdef PKV_K3_WATCHDOG
+    if ((++spins & 0xfff) == 0) {
+      const unsigned long long now = gtime();
+      if (t0 == 0) t0 = now;
+      else if (now - t0 > 4000000000ull) mbar_hang(bar, parity);
+    }
+#endif
+  }
 }
 __device__ __forceinline__ void tma_load_3d(uint32_t dst, const CUtensorMap* map, uint32_t bar, int c0,
                                             int c1, int c2) {

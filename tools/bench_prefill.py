@@ -27,6 +27,8 @@ def main():
     ap.add_argument("--hkv", type=int, default=8)
     ap.add_argument("--d", type=int, default=128)
     ap.add_argument("--batch", type=int, default=1)
+    ap.add_argument("--gathered", action="store_true",
+                    help="experiment: contiguous K/V rows without the block table (one TMA box per 128 keys)")
     args = ap.parse_args()
     dev = torch.device("cuda:0")
     hq, hkv, d, ps = args.hq, args.hkv, args.d, 16
@@ -48,14 +50,19 @@ def main():
         out = torch.empty((B * n, hq, d), device=dev, dtype=torch.float32)
         runs = suffix_runs(meta)
         rows = np.asarray([pool.table(b).mirror_row for b in range(B)], dtype=np.int32)
+        if args.gathered:
+            ent = [np.asarray(pool.table(b).entries) for b in range(B)]
+            assert all((np.diff(e) == 1).all() for e in ent), "pages not contiguous"
+            rows = np.asarray([e[0] * ps for e in ent], dtype=np.int32)
         plan = _lib.prefill_plan(runs[0], runs[1], meta.view.lengths, rows, hq, hkv, True)
         dplan = torch.from_numpy(plan).to(dev)
         mirror = pool.device_table(dev)
         lib = _lib.load()
         a = _lib.PrefillArgs(q=q.data_ptr(), total_q=B * n, k_cache=store.keys.data_ptr(),
                              v_cache=store.values.data_ptr(), kv_dtype=_lib.PKV_BF16,
-                             cache_rows=store.keys.shape[0], block_table=mirror.data_ptr(),
-                             bt_stride=mirror.shape[1], page_size=ps, hq=hq, hkv=hkv, head_dim=d,
+                             cache_rows=store.keys.shape[0],
+                             block_table=None if args.gathered else mirror.data_ptr(),
+                             bt_stride=0 if args.gathered else mirror.shape[1], page_size=ps, hq=hq, hkv=hkv, head_dim=d,
                              scale=cfg.scale, causal=1, out=out.data_ptr(), out_dtype=_lib.PKV_F32,
                              plan=dplan.data_ptr(), n_items=plan.shape[0])
         sp = _stream(dev)
