@@ -277,7 +277,7 @@ class DecodeBench:
         self.vs = torch.randn((T, B, hkv, d), generator=gen2, device=device, dtype=torch.bfloat16)
         # per-step metadata [q_seq | key counts | mirror rows | host work plan];
         # key counts grow by one per step (the appended token is attended)
-        self.plans = [_lib.attention_plan(base + t + 1, rows, ps, hq, hkv, waves) for t in range(T)]
+        self.plans = [_lib.attention_plan(base + t + 1, rows, ps, hq, hkv, waves, head_dim=d) for t in range(T)]
         width = 3 * B + max(pl.size for pl in self.plans)
         meta_np = np.zeros((T, width), dtype=np.int32)
         for t in range(T):

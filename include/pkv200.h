@@ -242,6 +242,11 @@ int64_t pkv_attention_plan_ints(int64_t n_queries, int32_t hq);
 int pkv_attention_plan(const int32_t* q_nkeys, const int32_t* q_row, int64_t n_queries,
                        int32_t page_size, int32_t hq, int32_t hkv, int32_t num_sms,
                        int32_t target_waves, int32_t* plan_out, int64_t cap, int64_t* n_out);
+/* the same with the head dim the planner's byte costs use (pkv_attention_plan
+ * assumes 128; the batched decode step derives it from the store rows) */
+int pkv_attention_plan_d(const int32_t* q_nkeys, const int32_t* q_row, int64_t n_queries,
+                         int32_t page_size, int32_t hq, int32_t hkv, int32_t head_dim, int32_t num_sms,
+                         int32_t target_waves, int32_t* plan_out, int64_t cap, int64_t* n_out);
 
 /* One decode step's host work for n sequences of a pool — the batched form of
  * DecodeSession.step (decoder.py:263-284): pkv_pool_prepare_append (grow,

@@ -127,6 +127,7 @@ SIGNATURES = {
     "pkv_attention_plan_ints": (_i64, [_i64, _i32]),
     "pkv_plan_memo_reset": (None, []),
     "pkv_attention_plan": (C.c_int, [_vp, _vp, _i64, _i32, _i32, _i32, _i32, _i32, _vp, _i64, _P(_i64)]),
+    "pkv_attention_plan_d": (C.c_int, [_vp, _vp, _i64, _i32, _i32, _i32, _i32, _i32, _i32, _vp, _i64, _P(_i64)]),
     "pkv_paged_attention": (C.c_int, [_P(AttentionArgs), _vp]),
     "pkv_decode_step": (C.c_int, [_P(StepStageArgs), _P(AttentionArgs), _P(DecodeIO), _vp]),
     "pkv_prefill_supported": (C.c_int, [_i32, _i32, _i32, _i32, _i32]),
@@ -174,8 +175,9 @@ def call(name: str, *args) -> None:
     check(getattr(load(), name)(*args), name)
 
 
-def attention_plan(q_nkeys, q_row, page_size: int, hq: int, hkv: int, target_waves: int = 0):
-    """Host plan of the tensor-core decode (pkv_attention_plan) as int32 numpy."""
+def attention_plan(q_nkeys, q_row, page_size: int, hq: int, hkv: int, target_waves: int = 0,
+                   head_dim: int = 128):
+    """Host plan of the tensor-core decode (pkv_attention_plan_d) as int32 numpy."""
     import numpy as np
 
     nk = np.ascontiguousarray(q_nkeys, dtype=np.int32)
@@ -184,9 +186,9 @@ def attention_plan(q_nkeys, q_row, page_size: int, hq: int, hkv: int, target_wav
     lib = load()
     out = np.empty(lib.pkv_attention_plan_ints(n, hq), dtype=np.int32)
     got = C.c_int64()
-    check(lib.pkv_attention_plan(nk.ctypes.data, rows.ctypes.data, n, page_size, hq, hkv, 0,
-                                 target_waves, out.ctypes.data, out.size, C.byref(got)),
-          "pkv_attention_plan")
+    check(lib.pkv_attention_plan_d(nk.ctypes.data, rows.ctypes.data, n, page_size, hq, hkv, head_dim, 0,
+                                   target_waves, out.ctypes.data, out.size, C.byref(got)),
+          "pkv_attention_plan_d")
     return out[: got.value].copy()
 
 

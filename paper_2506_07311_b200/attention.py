@@ -262,7 +262,7 @@ def _launch_attention(q, qcode, meta, config, nkeys, *, k, v, kv_code, bt, bt_st
     if q_row.size and (q_row.max() >= 2 ** 31):
         raise OutOfRange("K/V rows beyond 2^31 are not addressable")
     plan = _lib.attention_plan(nkeys, q_row, config.page_size, config.head_count,
-                               config.kv_head_count)
+                               config.kv_head_count, head_dim=config.head_dim)
     seq_part = (np.asarray(seq_row, dtype=np.int32) if bt is not None
                 else np.asarray(seq_start, dtype=np.int64).view(np.int32))
     nseq = seq_part.size

@@ -858,7 +858,7 @@ int cluster_capacity(int c, int num_sms) {
 // items.  A cut inside a unit splits its pages between neighbouring CTAs (the
 // pieces get partial slots and a combine record); cuts that would leave a
 // piece shorter than the per-item overhead snap to the unit boundary.
-int plan_decode(const int32_t* nk, const int32_t* row, int64_t nq, int page_size, int hq, int hkv,
+int plan_decode(const int32_t* nk, const int32_t* row, int64_t nq, int page_size, int hq, int hkv, int head_dim,
                 int num_sms, int waves, int32_t* out, int64_t cap, int64_t* n_out) {
   if (cap < decode_plan_ints(nq, hq)) return fail(PKV_VALUE_ERROR, "plan buffer too small");
   static const int max_grid_env = [] {  // experiment knob: cap the segment grid
@@ -894,7 +894,8 @@ int plan_decode(const int32_t* nk, const int32_t* row, int64_t nq, int page_size
   const int head_items = (hkv / hb) * qgroups;
   // costs in pages of one unit; the per-item overhead (pipeline refill,
   // query load, partial store) is ~4 us ~ `ovh` pages of a CTA's stream
-  const int64_t page_bytes = int64_t(hb) * ps * 128 * 2 * 2;  // K+V of the block (D ~ 128)
+  const int D = head_dim > 0 ? head_dim : 128;
+  const int64_t page_bytes = int64_t(hb) * ps * D * 2 * 2;  // K+V of the block
   static const int64_t ovh_kb = [] {  // per-item overhead in KB of stream (tuning knob)
     const char* e = std::getenv("PKV_DECODE_ITEM_KB");
     return e ? std::max<int64_t>(1, std::atoll(e)) : int64_t(400);  // measured optimum (C2, C3, C5)
@@ -960,7 +961,7 @@ int plan_decode(const int32_t* nk, const int32_t* row, int64_t nq, int page_size
     // time model (us): streaming at ~45 GB/s per CTA plus the merge — a
     // DSMEM cluster merge ~1 us, the global last-arriver merge ~2 us + 0.4 us
     // per piece of a unit (measured)
-    const double bytes_per_head_page = double(ps) * 128 * 2 * 2;
+    const double bytes_per_head_page = double(ps) * D * 2 * 2;
     const double stream_us = double(total_pages) * head_items * bytes_per_head_page / 45e3;
     const int64_t reg_grid = std::min<int64_t>(num_sms, std::max<int64_t>(1, total_pages * head_items / 16));
     const double reg_us = stream_us / double(reg_grid) + 2.0 + 0.4 * double((reg_grid + units_c - 1) / units_c);

@@ -734,7 +734,7 @@ int64_t pkv_attention_workspace_bytes(int64_t n_queries, int32_t hq, int32_t hea
 // holds the allocator's undo record (the caller commits or rolls it back),
 // on failure the allocator is unchanged.
 static int decode_step_prepare(pkv_pool* pool, const int64_t* seqs, int64_t n, int32_t page_size,
-                               int32_t hq, int32_t hkv, int32_t* meta, int64_t meta_cap,
+                               int32_t hq, int32_t hkv, int32_t head_dim, int32_t* meta, int64_t meta_cap,
                                int64_t* meta_used, uint32_t* pages_out, int64_t pages_cap,
                                int64_t* n_pages_out, int64_t* copies_out, pkv_append_undo** undo) {
   *undo = nullptr;
@@ -753,7 +753,7 @@ static int decode_step_prepare(pkv_pool* pool, const int64_t* seqs, int64_t n, i
     nkeys[i] += 1;
   }
   int64_t used = 0;
-  st = pkv_attention_plan(nkeys, rows, n, page_size, hq, hkv, 0, 0, meta + 3 * n,
+  st = pkv_attention_plan_d(nkeys, rows, n, page_size, hq, hkv, head_dim, 0, 0, meta + 3 * n,
                           meta_cap - 3 * n, &used);
   if (st) {
     pkv_pool_rollback_append(pool, *undo);
@@ -769,7 +769,7 @@ extern "C" int pkv_decode_step_prepare(pkv_pool* pool, const int64_t* seqs, int6
                                        int64_t* meta_used, uint32_t* pages_out, int64_t pages_cap,
                                        int64_t* n_pages_out, int64_t* copies_out) {
   pkv_append_undo* undo = nullptr;
-  const int st = decode_step_prepare(pool, seqs, n, page_size, hq, hkv, meta, meta_cap, meta_used, pages_out,
+  const int st = decode_step_prepare(pool, seqs, n, page_size, hq, hkv, 128, meta, meta_cap, meta_used, pages_out,
                                      pages_cap, n_pages_out, copies_out, &undo);
   pkv_pool_release_undo(undo);
   return st;
@@ -833,7 +833,10 @@ static int decode_step_stage(pkv_step_stage_args* a, cudaStream_t stream, pkv_ap
   std::vector<uint32_t> pages(2 * n + 1);
   std::vector<int64_t> copies(2 * n);
   int64_t n_pages = 0, used = 0;
-  int st = decode_step_prepare(a->pool, a->seqs, n, a->page_size, a->hq, a->hkv, a->meta_host,
+  // head dim for the planner's byte costs: 16-bit rows of hkv heads (the
+  // tensor-core path the plan feeds), 128 when no store is attached
+  const int32_t head_dim = a->row_bytes > 0 ? static_cast<int32_t>(a->row_bytes / (2 * a->hkv)) : 128;
+  int st = decode_step_prepare(a->pool, a->seqs, n, a->page_size, a->hq, a->hkv, head_dim, a->meta_host,
                                a->meta_cap - extra, &used, pages.data(), static_cast<int64_t>(pages.size()),
                                &n_pages, copies.data(), undo);
   if (st) return st;
@@ -1088,7 +1091,8 @@ int pkv_paged_attention(const pkv_attention_args* a, void* stream_) {
   return PKV_OK;
 }
 
-static void plan_speculate(const int32_t* nk, const int32_t* row, int64_t n, int32_t ps, int32_t hq, int32_t hkv);
+static void plan_speculate(const int32_t* nk, const int32_t* row, int64_t n, int32_t ps, int32_t hq, int32_t hkv,
+                           int32_t head_dim);
 
 int pkv_decode_step(pkv_step_stage_args* stage, pkv_attention_args* attn, pkv_decode_io* io, void* stream_) {
   if (!stage || !attn) return pkv::fail(PKV_VALUE_ERROR, "null args");
@@ -1159,7 +1163,9 @@ int pkv_decode_step(pkv_step_stage_args* stage, pkv_attention_args* attn, pkv_de
   }
   // the next step's plan, computed while the GPU runs this one
   stamp(9);
-  if (tensor) plan_speculate(stage->meta_host + n, stage->meta_host + 2 * n, n, attn->page_size, attn->hq, attn->hkv);
+  if (tensor)
+    plan_speculate(stage->meta_host + n, stage->meta_host + 2 * n, n, attn->page_size, attn->hq, attn->hkv,
+                   attn->head_dim);
   stamp(10);
   return PKV_OK;
 }
@@ -1183,17 +1189,18 @@ thread_local PlanMemo t_memo;
 thread_local std::vector<int32_t> t_key;
 
 void plan_key(std::vector<int32_t>& k, const int32_t* nk, const int32_t* row, int64_t n, int32_t ps,
-              int32_t hq, int32_t hkv, int32_t sms, int32_t waves, int32_t bump) {
-  k.resize(static_cast<size_t>(2 * n + 6));
+              int32_t hq, int32_t hkv, int32_t d, int32_t sms, int32_t waves, int32_t bump) {
+  k.resize(static_cast<size_t>(2 * n + 7));
   k[0] = static_cast<int32_t>(n);
   k[1] = ps;
   k[2] = hq;
   k[3] = hkv;
   k[4] = sms;
   k[5] = waves;
+  k[6] = d;
   for (int64_t i = 0; i < n; ++i) {
-    k[6 + i] = nk[i] + bump;
-    k[6 + n + i] = row[i];
+    k[7 + i] = nk[i] + bump;
+    k[7 + n + i] = row[i];
   }
 }
 }  // namespace
@@ -1210,14 +1217,14 @@ static int resolve_sms(int32_t num_sms) {
 
 // compute and memoise the plan of the next decode step (every key count + 1)
 static void plan_speculate(const int32_t* nk, const int32_t* row, int64_t n, int32_t ps, int32_t hq,
-                           int32_t hkv) {
+                           int32_t hkv, int32_t head_dim) {
   const int sms = resolve_sms(0);
   PlanMemo& m = t_memo;
-  plan_key(m.key, nk, row, n, ps, hq, hkv, sms, 0, 1);
+  plan_key(m.key, nk, row, n, ps, hq, hkv, head_dim, sms, 0, 1);
   m.plan.resize(static_cast<size_t>(pkv::decode_plan_ints(n, hq)));
-  std::vector<int32_t> nk1(m.key.begin() + 6, m.key.begin() + 6 + n);
+  std::vector<int32_t> nk1(m.key.begin() + 7, m.key.begin() + 7 + n);
   int64_t used = 0;
-  if (pkv::plan_decode(nk1.data(), row, n, ps, hq, hkv, sms, 0, m.plan.data(),
+  if (pkv::plan_decode(nk1.data(), row, n, ps, hq, hkv, head_dim, sms, 0, m.plan.data(),
                        static_cast<int64_t>(m.plan.size()), &used) != PKV_OK) {
     m.key.clear();
     return;
@@ -1230,11 +1237,12 @@ extern "C" void pkv_plan_memo_reset(void) {
   t_memo.plan.clear();
 }
 
-extern "C" int pkv_attention_plan(const int32_t* q_nkeys, const int32_t* q_row, int64_t n_queries,
-                                  int32_t page_size, int32_t hq, int32_t hkv, int32_t num_sms,
-                                  int32_t target_waves, int32_t* plan_out, int64_t cap, int64_t* n_out) {
+extern "C" int pkv_attention_plan_d(const int32_t* q_nkeys, const int32_t* q_row, int64_t n_queries,
+                                    int32_t page_size, int32_t hq, int32_t hkv, int32_t head_dim, int32_t num_sms,
+                                    int32_t target_waves, int32_t* plan_out, int64_t cap, int64_t* n_out) {
   if (n_queries > 0 && hq > 0 && hkv > 0 && !t_memo.key.empty()) {
-    plan_key(t_key, q_nkeys, q_row, n_queries, page_size, hq, hkv, resolve_sms(num_sms), target_waves, 0);
+    plan_key(t_key, q_nkeys, q_row, n_queries, page_size, hq, hkv, head_dim, resolve_sms(num_sms), target_waves,
+             0);
     if (t_key == t_memo.key && cap >= static_cast<int64_t>(t_memo.plan.size())) {
       std::copy(t_memo.plan.begin(), t_memo.plan.end(), plan_out);
       if (n_out) *n_out = static_cast<int64_t>(t_memo.plan.size());
@@ -1253,8 +1261,15 @@ extern "C" int pkv_attention_plan(const int32_t* q_nkeys, const int32_t* q_row, 
     }
     num_sms = g_num_sms;
   }
-  return pkv::plan_decode(q_nkeys, q_row, n_queries, page_size, hq, hkv, num_sms,
+  return pkv::plan_decode(q_nkeys, q_row, n_queries, page_size, hq, hkv, head_dim, num_sms,
                           target_waves, plan_out, cap, n_out);
+}
+
+extern "C" int pkv_attention_plan(const int32_t* q_nkeys, const int32_t* q_row, int64_t n_queries,
+                                  int32_t page_size, int32_t hq, int32_t hkv, int32_t num_sms,
+                                  int32_t target_waves, int32_t* plan_out, int64_t cap, int64_t* n_out) {
+  return pkv_attention_plan_d(q_nkeys, q_row, n_queries, page_size, hq, hkv, 128, num_sms, target_waves,
+                              plan_out, cap, n_out);
 }
 
 extern "C" int pkv_debug_trace(int32_t enable, uint64_t* out, int64_t n) {

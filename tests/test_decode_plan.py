@@ -55,9 +55,20 @@ def test_planner_fuzz_terminates_and_covers():
         check_plan(lengths, hq, hkv, ps)
 
 
-def check_plan(lengths, hq, hkv, ps, balance=False):
+@pytest.mark.parametrize("name,lengths,hq,hkv", CASES, ids=[c[0] for c in CASES])
+def test_head_dim_64_plans_cover_and_use_the_smaller_page_cost(name, lengths, hq, hkv):
+    """The planner's byte costs follow the head dim: a D = 64 page streams
+    half the bytes, so the fixed per-item cost is twice as many pages and a
+    D = 64 plan cuts units no more often than the D = 128 plan."""
+    p64 = check_plan(lengths, hq, hkv, 16, head_dim=64)
+    p128 = parse(_lib.attention_plan(np.asarray(lengths, np.int32), np.arange(len(lengths), dtype=np.int32), 16,
+                                     hq, hkv, head_dim=128))
+    assert len(p64["comb"]) <= len(p128["comb"])
+
+
+def check_plan(lengths, hq, hkv, ps, balance=False, head_dim=128):
     nk = np.asarray(lengths, dtype=np.int32)
-    plan = _lib.attention_plan(nk, np.arange(nk.size, dtype=np.int32), ps, hq, hkv)
+    plan = _lib.attention_plan(nk, np.arange(nk.size, dtype=np.int32), ps, hq, hkv, head_dim=head_dim)
     P = parse(plan)
     assert P["nq"] == nk.size and np.array_equal(P["nk"], nk)
     items, comb = P["items"], P["comb"]
@@ -95,6 +106,7 @@ def check_plan(lengths, hq, hkv, ps, balance=False):
         assert P["grid"] == len(items) <= 148 and P["grid"] % P["cluster"] == 0
     # few items per CTA
     assert len(items) <= nk.size * P["head_items"] + 2 * P["grid"]
+    return P
 
 
 @pytest.mark.parametrize("L,B", [(2048, 64), (4096, 32), (16384, 16), (8192, 64)])
