@@ -876,7 +876,7 @@ def sweep():
                 continue
             cmd = [sys.executable, os.path.abspath(__file__), "--config", "c3", "--context", str(ctx),
                    "--batch", str(b), "--steps", "10", "--warmup", "3", "--no-cpu-baseline", "--no-e2e",
-                   "--no-prefill"]
+                   "--no-prefill", "--no-c5"]
             out = subprocess.run(cmd, capture_output=True, text=True)
             line = out.stdout.strip().splitlines()[-1] if out.stdout.strip() else json.dumps(
                 {"error": out.stderr[-500:]})

@@ -30,3 +30,16 @@ for _ in range(20):
 pr.disable()
 torch.cuda.synchronize()
 pstats.Stats(pr).sort_stats("tottime").print_stats(18)
+
+# KvStore.assign of the whole prompt (K1): host side
+pos = np.arange(n)
+for _ in range(3):
+    store.assign(0, pos, k, k)
+torch.cuda.synchronize()
+pr = cProfile.Profile()
+pr.enable()
+for _ in range(20):
+    store.assign(0, pos, k, k)
+pr.disable()
+torch.cuda.synchronize()
+pstats.Stats(pr).sort_stats("tottime").print_stats(14)
