@@ -846,6 +846,16 @@ def prefill_c4(device, n=8192):
         app.append(e0.elapsed_time(e1))
         times.append(e1.elapsed_time(e2))
         kern.append(ev[0].elapsed_time(ev[1]))
+    # the same call issued back to back (a model's layers): host planning of
+    # call i+1 overlaps kernel i
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize(device)
+    e0.record()
+    for _ in range(10):
+        paged_attention(q, store, meta, cfg, precision="prefill")
+    e1.record()
+    torch.cuda.synchronize(device)
+    pipelined_ms = e0.elapsed_time(e1) / 10
     ms = sorted(times)[len(times) // 2]
     kms = sorted(kern)[len(kern) // 2]
     flops = 4 * hq * d * n * (n + 1) // 2
@@ -860,11 +870,13 @@ def prefill_c4(device, n=8192):
     return {"workload": f"C4 causal prefill, 1 x {n} tokens, GQA 32q/8kv x128 bf16, page 16",
             "kernel": "prefill_tc_kernel (K3, tcgen05/TMEM)", "kernel_ms": kms, "tflops": round(tf, 1),
             "frac_of_burst_bf16": round(tf / burst, 3), "frac_of_sustained_bf16": round(tf / sustained, 3),
-            "api_ms": ms, "api_tflops": round(flops / (ms * 1e-3) / 1e12, 1), "append_ms": min(app),
+            "api_ms": ms, "api_tflops": round(flops / (ms * 1e-3) / 1e12, 1),
+            "api_pipelined_ms": pipelined_ms, "append_ms": min(app),
             "append_gbs": round(append_bytes / (min(app) * 1e-3) / 1e9, 1),
-            "note": "kernel_ms: CUDA events around the K3 launch; api_ms: the whole paged_attention() call "
-                    "(host planning + metadata upload + launch); append: KvStore.assign of the prompt "
-                    "(host validation included); FLOPs per the reference convention"}
+            "note": "kernel_ms: CUDA events around the K3 launch; api_ms: one paged_attention() call on an idle "
+                    "GPU (host planning + metadata upload + launch + kernel); api_pipelined_ms: the call issued "
+                    "10x back to back (host work of a call hidden behind the previous kernel); append: "
+                    "KvStore.assign of the prompt (host validation included); FLOPs per the reference convention"}
 
 
 def sweep():

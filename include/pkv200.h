@@ -128,6 +128,10 @@ int pkv_pool_prepare_append(pkv_pool* pool, const int64_t* seqs, int64_t n, int3
  * on the device with pkv_mirror_apply (or re-uploads the whole matrix after a
  * shape change, signalled by *full_resync). */
 int pkv_pool_mirror_row(pkv_pool* pool, int64_t seq, int32_t* row_out);
+/* batched table query for n sequence handles: page count and mirror row of
+ * each (either output may be NULL); one call instead of two per sequence */
+int pkv_pool_tables_info(pkv_pool* pool, const int64_t* seqs, int64_t n, int64_t* n_pages_out,
+                         int32_t* mirror_row_out);
 int pkv_pool_mirror_shape(pkv_pool* pool, int64_t* rows_out, int64_t* cols_out);
 /* pairs_out holds (flat_index, value) int32 pairs; at most cap pairs */
 int pkv_pool_mirror_drain(pkv_pool* pool, int32_t* pairs_out, int64_t cap, int64_t* n_out,
@@ -162,6 +166,13 @@ int pkv_kv_append(const void* k_new, const void* v_new, int64_t n_tok, const int
                   int32_t tok_row_stride, const int32_t* tok_pos, const int32_t* block_table,
                   int64_t bt_stride, int32_t page_size, void* k_cache, void* v_cache,
                   int64_t row_bytes, void* stream);
+/* K1 for a contiguous run (the prompt of a prefill, one decode token):
+ * token t goes to position pos0 + t of the sequence at mirror row seq_row; no
+ * per-token metadata is uploaded (store.py:146-150 for positions
+ * pos0 .. pos0 + n_tok - 1) */
+int pkv_kv_append_range(const void* k_new, const void* v_new, int64_t n_tok, int32_t seq_row, int32_t pos0,
+                        const int32_t* block_table, int64_t bt_stride, int32_t page_size, void* k_cache,
+                        void* v_cache, int64_t row_bytes, void* stream);
 
 /* K-gather: contiguous copies of paged rows — KvStore.gather / gather_view
  * (store.py:152-161, 187-190).  For view sequence s (s < n_seq) with block

@@ -109,6 +109,7 @@ SIGNATURES = {
     "pkv_pool_refcount": (C.c_int, [_vp, _u64, _P(_i64)]),
     "pkv_pool_census": (C.c_int, [_vp, _P(_i64)]),
     "pkv_pool_free_stack": (C.c_int, [_vp, _P(_u32), _i64, _P(_i64)]),
+    "pkv_pool_tables_info": (C.c_int, [_vp, _vp, _i64, _vp, _vp]),
     "pkv_pool_mirror_row": (C.c_int, [_vp, _i64, _P(_i32)]),
     "pkv_pool_mirror_shape": (C.c_int, [_vp, _P(_i64), _P(_i64)]),
     "pkv_pool_mirror_drain": (C.c_int, [_vp, _P(_i32), _i64, _P(_i64), _P(_i32)]),
@@ -117,6 +118,7 @@ SIGNATURES = {
     "pkv_mirror_apply": (C.c_int, [_vp, _vp, _i64, _vp]),
     "pkv_page_zero": (C.c_int, [_vp, _vp, _vp, _i64, _i64, _vp]),
     "pkv_page_copy": (C.c_int, [_vp, _vp, _vp, _i64, _i64, _i32, _vp]),
+    "pkv_kv_append_range": (C.c_int, [_vp, _vp, _i64, _i32, _i32, _vp, _i64, _i32, _vp, _vp, _i64, _vp]),
     "pkv_kv_append": (C.c_int, [_vp, _vp, _i64, _vp, _i32, _vp, _vp, _i64, _i32, _vp, _vp, _i64, _vp]),
     "pkv_kv_gather": (C.c_int, [_vp, _vp, _vp, _i64, _vp, _vp, _i64, _i64, _i32, _i64, _vp, _vp, _vp]),
     "pkv_attention_workspace_bytes": (_i64, [_i64, _i32, _i32]),

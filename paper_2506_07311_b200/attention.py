@@ -388,10 +388,12 @@ def paged_attention(queries, store: KvStore, meta: MaskMeta, config: AttentionCo
     if config.page_size != store.page_size:
         raise ShapeMismatch("attention page_size does not match the pool")
     view = meta.view
-    tables = [store.pool.table(s) for s in view.ids]
-    for t, n in zip(tables, view.lengths):
-        if n < 0 or n > len(t.entries) * store.page_size:
-            raise OutOfRange(f"length {int(n)} exceeds reserved capacity of sequence {t.seq_id!r}")
+    n_pages, seq_row = store.pool.tables_info(view.ids)  # one native call for every table
+    lengths = np.asarray(view.lengths, dtype=np.int64)
+    bad = np.nonzero((lengths < 0) | (lengths > n_pages * store.page_size))[0]
+    if bad.size:
+        i = int(bad[0])
+        raise OutOfRange(f"length {int(lengths[i])} exceeds reserved capacity of sequence {view.ids[i]!r}")
     nkeys = allowed_key_counts(meta, config.causal)
     if meta.query_count and (nkeys <= 0).any():
         bad = np.nonzero(nkeys <= 0)[0].tolist()
@@ -400,7 +402,6 @@ def paged_attention(queries, store: KvStore, meta: MaskMeta, config: AttentionCo
         _fill_stats(stats, meta, config, nkeys, block_mask)
     device = store.device
     q, qcode = _q_tensor(queries, device)
-    seq_row = np.asarray([t.mirror_row for t in tables], dtype=np.int32)
     runs = _prefill_route(meta, config, store.dtype_code, precision)
     mirror = store.pool.device_table(device)
     if runs is not None:

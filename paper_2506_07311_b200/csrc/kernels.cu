@@ -112,15 +112,18 @@ __global__ void step_aux_kernel(const uint64_t* __restrict__ caches, int n_store
 
 // one CTA per token (grid-stride); the slot is resolved in-kernel from the
 // block-table mirror (shift/mask: the page size is a power of two)
+// tok_pos == NULL: a contiguous run, token t at position pos0 + t of mirror
+// row row0 (no per-token metadata at all)
 __global__ void kv_append_kernel(const char* __restrict__ kn, const char* __restrict__ vn,
                                  int64_t n_tok, const int32_t* __restrict__ tok_row,
                                  int row_stride, const int32_t* __restrict__ tok_pos,
                                  const int32_t* __restrict__ bt, int64_t bt_stride, int log2ps,
-                                 char* __restrict__ kc, char* __restrict__ vc, int64_t row_bytes) {
+                                 char* __restrict__ kc, char* __restrict__ vc, int64_t row_bytes,
+                                 int32_t pos0, int32_t row0) {
   const int ps = 1 << log2ps;
   for (int64_t t = blockIdx.x; t < n_tok; t += gridDim.x) {
-    const int32_t pos = tok_pos[t];
-    const int64_t r = tok_row[t * row_stride];
+    const int32_t pos = tok_pos ? tok_pos[t] : pos0 + static_cast<int32_t>(t);
+    const int64_t r = tok_pos ? tok_row[t * row_stride] : row0;
     const int64_t page = bt[r * bt_stride + (pos >> log2ps)];
     const int64_t dst = (page * ps + (pos & (ps - 1))) * row_bytes;
     copy_bytes(kc + dst, kn + t * row_bytes, row_bytes, threadIdx.x, blockDim.x);
@@ -695,7 +698,28 @@ int pkv_kv_append(const void* k_new, const void* v_new, int64_t n_tok, const int
   kv_append_kernel<<<static_cast<unsigned>(blocks), threads, 0, static_cast<cudaStream_t>(stream)>>>(
       static_cast<const char*>(k_new), static_cast<const char*>(v_new), n_tok, tok_row,
       tok_row_stride, tok_pos, block_table, bt_stride, __builtin_ctz(page_size),
-      static_cast<char*>(k_cache), static_cast<char*>(v_cache), row_bytes);
+      static_cast<char*>(k_cache), static_cast<char*>(v_cache), row_bytes, 0, 0);
+  PKV_CHECK_LAUNCH();
+  return PKV_OK;
+}
+
+int pkv_kv_append_range(const void* k_new, const void* v_new, int64_t n_tok, int32_t seq_row, int32_t pos0,
+                        const int32_t* block_table, int64_t bt_stride, int32_t page_size, void* k_cache,
+                        void* v_cache, int64_t row_bytes, void* stream) {
+  if (n_tok <= 0) return PKV_OK;
+  if (pos0 < 0 || int64_t(pos0) + n_tok > (int64_t(1) << 31) || seq_row < 0)
+    return pkv::fail(PKV_OUT_OF_RANGE, "append range outside int32 positions");
+  pkv::DeviceGuard guard(static_cast<cudaStream_t>(stream));
+  if (page_size <= 0 || (page_size & (page_size - 1)))
+    return pkv::fail(PKV_VALUE_ERROR, "page_size must be a power of two");
+  if (row_bytes & 1) return pkv::fail(PKV_CONFIG_ERROR, "row bytes must be even");
+  int threads = static_cast<int>(row_bytes / 16);
+  threads = threads < 32 ? 32 : (threads > 256 ? 256 : ((threads + 31) / 32) * 32);
+  const int64_t blocks = n_tok < 65535 * 4 ? n_tok : 65535 * 4;
+  kv_append_kernel<<<static_cast<unsigned>(blocks), threads, 0, static_cast<cudaStream_t>(stream)>>>(
+      static_cast<const char*>(k_new), static_cast<const char*>(v_new), n_tok, nullptr, 0, nullptr, block_table,
+      bt_stride, __builtin_ctz(page_size), static_cast<char*>(k_cache), static_cast<char*>(v_cache), row_bytes,
+      pos0, seq_row);
   PKV_CHECK_LAUNCH();
   return PKV_OK;
 }

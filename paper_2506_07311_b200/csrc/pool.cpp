@@ -640,6 +640,18 @@ int pkv_pool_mirror_row(pkv_pool* pool, int64_t seq, int32_t* row_out) {
   return PKV_OK;
 }
 
+int pkv_pool_tables_info(pkv_pool* pool, const int64_t* seqs, int64_t n, int64_t* n_pages_out,
+                         int32_t* mirror_row_out) {
+  if (n < 0 || (n > 0 && !seqs)) return pkv::fail(PKV_VALUE_ERROR, "bad sequence list");
+  LOCK(pool);
+  for (int64_t i = 0; i < n; ++i) {
+    TABLE_OR_FAIL(t, pool, seqs[i]);
+    if (n_pages_out) n_pages_out[i] = static_cast<int64_t>(t->entries.size());
+    if (mirror_row_out) mirror_row_out[i] = t->mirror_row;
+  }
+  return PKV_OK;
+}
+
 int pkv_pool_mirror_shape(pkv_pool* pool, int64_t* rows_out, int64_t* cols_out) {
   LOCK(pool);
   pool->ensure_shape(1, 1);

@@ -43,6 +43,7 @@
 
 #include <algorithm>
 #include <cstring>
+#include <mutex>
 #include <numeric>
 #include <type_traits>
 #include <vector>
@@ -556,8 +557,8 @@ EncodeTiledFn encode_fn() {
 }
 
 // 3-D map over [dim2][dim1][dim0] 16-bit elements, box (64, box1, box2), 128-B swizzle
-int make_map(CUtensorMap* map, const void* base, int dtype, uint64_t dim0, uint64_t dim1, uint64_t dim2,
-             uint32_t box1, uint32_t box2) {
+int encode_map(CUtensorMap* map, const void* base, int dtype, uint64_t dim0, uint64_t dim1, uint64_t dim2,
+               uint32_t box1, uint32_t box2) {
   EncodeTiledFn fn = encode_fn();
   if (!fn) return fail(PKV_CUDA_ERROR, "cuTensorMapEncodeTiled unavailable");
   const cuuint64_t dims[3] = {dim0, dim1, dim2};
@@ -569,6 +570,41 @@ int make_map(CUtensorMap* map, const void* base, int dtype, uint64_t dim0, uint6
                         CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                         CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) return fail(PKV_CUDA_ERROR, "cuTensorMapEncodeTiled failed (%d)", static_cast<int>(r));
+  return PKV_OK;
+}
+
+// The encoded maps are cached (a cache's K / V maps are the same on every
+// call; a caller that reuses its query buffer hits too): a small per-process
+// table keyed by every encode argument, most recent first.
+int make_map(CUtensorMap* map, const void* base, int dtype, uint64_t dim0, uint64_t dim1, uint64_t dim2,
+             uint32_t box1, uint32_t box2) {
+  struct Entry {
+    const void* base;
+    uint64_t d0, d1, d2;
+    uint32_t b1, b2;
+    int dtype;
+    CUtensorMap map;
+  };
+  static std::mutex mu;
+  static std::vector<Entry> cache;
+  constexpr size_t kMaxEntries = 16;
+  {
+    std::lock_guard<std::mutex> g(mu);
+    for (size_t i = 0; i < cache.size(); ++i) {
+      const Entry& e = cache[i];
+      if (e.base == base && e.d0 == dim0 && e.d1 == dim1 && e.d2 == dim2 && e.b1 == box1 && e.b2 == box2 &&
+          e.dtype == dtype) {
+        *map = e.map;
+        if (i > 0) std::rotate(cache.begin(), cache.begin() + i, cache.begin() + i + 1);
+        return PKV_OK;
+      }
+    }
+  }
+  const int st = encode_map(map, base, dtype, dim0, dim1, dim2, box1, box2);
+  if (st) return st;
+  std::lock_guard<std::mutex> g(mu);
+  cache.insert(cache.begin(), Entry{base, dim0, dim1, dim2, box1, box2, dtype, *map});
+  if (cache.size() > kMaxEntries) cache.pop_back();
   return PKV_OK;
 }
 
@@ -631,9 +667,62 @@ extern "C" int64_t pkv_prefill_plan_ints(const int32_t* q_len, int64_t n_seqs, i
 // Work items: one kv head x two consecutive query tiles (A, B) of 128/G
 // positions each; per tile the key range is the causal prefix of its last
 // valid query (n_tiles of 128 keys).  Longest first.
+namespace pkv {
+int prefill_plan_build(const int64_t* q_start, const int32_t* q_len, const int32_t* seq_len,
+                       const int32_t* seq_row, int64_t n_seqs, int32_t hq, int32_t hkv, int32_t causal,
+                       int32_t* plan_out, int64_t cap, int64_t* n_items_out);
+}
+namespace {
+// Memo of the last plan per host thread: every layer of a model runs the
+// same prefill metadata, so the planner (item build + longest-first sort)
+// runs once per forward instead of once per layer.
+struct PrefillMemo {
+  std::vector<int64_t> key;
+  std::vector<int32_t> plan;
+  int64_t n_items = -1;
+};
+thread_local PrefillMemo t_prefill_memo;
+}  // namespace
+
 extern "C" int pkv_prefill_plan(const int64_t* q_start, const int32_t* q_len, const int32_t* seq_len,
                                 const int32_t* seq_row, int64_t n_seqs, int32_t hq, int32_t hkv,
                                 int32_t causal, int32_t* plan_out, int64_t cap, int64_t* n_items_out) {
+  if (n_seqs < 0 || (n_seqs > 0 && (!q_start || !q_len || !seq_len || !seq_row)))
+    return fail(PKV_VALUE_ERROR, "bad prefill plan inputs");
+  std::vector<int64_t> key;
+  key.reserve(static_cast<size_t>(4 * n_seqs + 4));
+  key.push_back(n_seqs);
+  key.push_back(hq);
+  key.push_back(hkv);
+  key.push_back(causal);
+  for (int64_t s = 0; s < n_seqs; ++s) {
+    key.push_back(q_start[s]);
+    key.push_back(q_len[s]);
+    key.push_back(seq_len[s]);
+    key.push_back(seq_row[s]);
+  }
+  PrefillMemo& m = t_prefill_memo;
+  if (m.n_items >= 0 && key == m.key) {
+    const int64_t need = m.n_items * kItemInts;
+    if (need > cap) return fail(PKV_VALUE_ERROR, "plan buffer too small (%lld < %lld)", static_cast<long long>(cap),
+                                static_cast<long long>(need));
+    if (need) std::memcpy(plan_out, m.plan.data(), need * sizeof(int32_t));
+    *n_items_out = m.n_items;
+    return PKV_OK;
+  }
+  const int st = pkv::prefill_plan_build(q_start, q_len, seq_len, seq_row, n_seqs, hq, hkv, causal, plan_out, cap,
+                                         n_items_out);
+  if (st) return st;
+  m.key.swap(key);
+  m.n_items = *n_items_out;
+  m.plan.assign(plan_out, plan_out + m.n_items * kItemInts);
+  return PKV_OK;
+}
+
+namespace pkv {
+int prefill_plan_build(const int64_t* q_start, const int32_t* q_len, const int32_t* seq_len,
+                       const int32_t* seq_row, int64_t n_seqs, int32_t hq, int32_t hkv, int32_t causal,
+                       int32_t* plan_out, int64_t cap, int64_t* n_items_out) {
   if (hq <= 0 || hkv <= 0 || hq % hkv) return fail(PKV_SHAPE_MISMATCH, "hq must be a multiple of hkv");
   const int G = hq / hkv;
   if (G > kM || kM % G) return fail(PKV_CONFIG_ERROR, "group size %d does not divide %d", G, kM);
@@ -683,6 +772,8 @@ extern "C" int pkv_prefill_plan(const int64_t* q_start, const int32_t* q_len, co
   *n_items_out = static_cast<int64_t>(items.size());
   return PKV_OK;
 }
+
+}  // namespace pkv
 
 extern "C" int pkv_paged_prefill(const pkv_prefill_args* a, void* stream_) {
   if (!a) return fail(PKV_VALUE_ERROR, "null args");

@@ -310,6 +310,20 @@ class PagePool:
             raise UnknownSequence(f"no block table for sequence {seq_id!r}")
         return BlockTable(self, seq_id, h)
 
+    def tables_info(self, seq_ids):
+        """(pages held int64[n], mirror row int32[n]) of the given sequences in
+        one native call (pkv_pool_tables_info) — the per-call table lookups
+        of the attention entry points, batched."""
+        n = len(seq_ids)
+        try:
+            handles = np.fromiter((self._ids[s] for s in seq_ids), dtype=np.int64, count=n)
+        except KeyError as e:
+            raise UnknownSequence(f"no block table for sequence {e.args[0]!r}") from None
+        pages = np.empty(n, dtype=np.int64)
+        rows = np.empty(n, dtype=np.int32)
+        _lib.call("pkv_pool_tables_info", self._h, handles.ctypes.data, n, pages.ctypes.data, rows.ctypes.data)
+        return pages, rows
+
     def has_sequence(self, seq_id) -> bool:
         return seq_id in self._ids
 
