@@ -773,6 +773,9 @@ def main():
         if world > 1:
             line["config"]["backend"] = backend
             line["config"]["devices"] = ndev
+            if ndev < world:  # plumbing check only: ranks time-share one device
+                line["note"] = (f"{world} ranks on {ndev} device(s): the ranks time-share a GPU, so the "
+                                "max-over-ranks time is not a throughput number")
         if c5 is not None:
             line["c5"] = line_for(args, "c5", c5, world, peak, peak_src, min(args.steps, 10),
                                   max(3, min(args.warmup, 5)))
