@@ -130,6 +130,37 @@ __device__ __forceinline__ void store_from_float(void* base, int64_t idx, int dt
     static_cast<__half*>(base)[idx] = __float2half_rn(v);
 }
 
+// four consecutive outputs (idx a multiple of 4) with one vector store: one
+// dtype switch instead of four (the merge tails run once per launch from a
+// cold instruction cache, so their code size is their latency)
+__device__ __forceinline__ void store4_from_float(void* base, int64_t idx, int dtype, float4 v) {
+  if (dtype == PKV_F32) {
+    *reinterpret_cast<float4*>(static_cast<float*>(base) + idx) = v;
+  } else if (dtype == PKV_BF16) {
+    __nv_bfloat162 a = __floats2bfloat162_rn(v.x, v.y), b = __floats2bfloat162_rn(v.z, v.w);
+    uint2 w;
+    w.x = *reinterpret_cast<uint32_t*>(&a);
+    w.y = *reinterpret_cast<uint32_t*>(&b);
+    *reinterpret_cast<uint2*>(static_cast<__nv_bfloat16*>(base) + idx) = w;
+  } else {
+    __half2 a = __floats2half2_rn(v.x, v.y), b = __floats2half2_rn(v.z, v.w);
+    uint2 w;
+    w.x = *reinterpret_cast<uint32_t*>(&a);
+    w.y = *reinterpret_cast<uint32_t*>(&b);
+    *reinterpret_cast<uint2*>(static_cast<__half*>(base) + idx) = w;
+  }
+}
+// two consecutive outputs (idx even)
+__device__ __forceinline__ void store2_from_float(void* base, int64_t idx, int dtype, float a, float b) {
+  if (dtype == PKV_F32) {
+    *reinterpret_cast<float2*>(static_cast<float*>(base) + idx) = make_float2(a, b);
+  } else if (dtype == PKV_BF16) {
+    *reinterpret_cast<__nv_bfloat162*>(static_cast<__nv_bfloat16*>(base) + idx) = __floats2bfloat162_rn(a, b);
+  } else {
+    *reinterpret_cast<__half2*>(static_cast<__half*>(base) + idx) = __floats2half2_rn(a, b);
+  }
+}
+
 // byte copy with the widest vector the alignment allows
 __device__ __forceinline__ void copy_bytes(char* dst, const char* src, int64_t n, int64_t tid,
                                            int64_t nthreads) {

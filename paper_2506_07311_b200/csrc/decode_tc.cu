@@ -294,10 +294,8 @@ __device__ __forceinline__ void finish_split_group(const TcParams& p, const int3
     }
     const float inv = 1.f / den;
     const int64_t o = (int64_t(qi) * p.hq + qh) * D + d;
-    store_from_float(p.out, o, p.out_dtype, acc.x * inv);
-    store_from_float(p.out, o + 1, p.out_dtype, acc.y * inv);
-    store_from_float(p.out, o + 2, p.out_dtype, acc.z * inv);
-    store_from_float(p.out, o + 3, p.out_dtype, acc.w * inv);
+    store4_from_float(p.out, o, p.out_dtype,
+                      make_float4(acc.x * inv, acc.y * inv, acc.z * inv, acc.w * inv));
   }
   if (tt == 0) *ctr = 0;  // self-cleaning: the plan buffer can be replayed
 }
@@ -630,12 +628,10 @@ __global__ void __launch_bounds__(kThreadsTc, 1) decode_tc_kernel(const __grid_c
         const int d = n * 8 + 2 * t4;
         if (C.slot < 0) {
           if (g < C.rows) {
-            store_from_float(p.out, out_base + int64_t(g) * D + d, p.out_dtype, o[n][0] / l0);
-            store_from_float(p.out, out_base + int64_t(g) * D + d + 1, p.out_dtype, o[n][1] / l0);
+            store2_from_float(p.out, out_base + int64_t(g) * D + d, p.out_dtype, o[n][0] / l0, o[n][1] / l0);
           }
           if (ROWS16 && g + 8 < C.rows) {
-            store_from_float(p.out, out_base + int64_t(g + 8) * D + d, p.out_dtype, o[n][2] / l1);
-            store_from_float(p.out, out_base + int64_t(g + 8) * D + d + 1, p.out_dtype, o[n][3] / l1);
+            store2_from_float(p.out, out_base + int64_t(g + 8) * D + d, p.out_dtype, o[n][2] / l1, o[n][3] / l1);
           }
         } else {
           if (g < C.rows) __stcg(reinterpret_cast<float2*>(p.ws_o + (pslot + g) * D + d), make_float2(o[n][0], o[n][1]));
@@ -717,10 +713,8 @@ __global__ void __launch_bounds__(kThreadsTc, 1) decode_tc_kernel(const __grid_c
         st_dsmem4(&r_o[my_rank * slice + (e - owner * slice)], owner, acc);
       } else if (C.slot < 0) {
         const float inv = 1.f / s_rml[(w0 * kMergeRows + r) * 2 + 1];
-        store_from_float(p.out, out_base + e, p.out_dtype, acc.x * inv);
-        store_from_float(p.out, out_base + e + 1, p.out_dtype, acc.y * inv);
-        store_from_float(p.out, out_base + e + 2, p.out_dtype, acc.z * inv);
-        store_from_float(p.out, out_base + e + 3, p.out_dtype, acc.w * inv);
+        store4_from_float(p.out, out_base + e, p.out_dtype,
+                          make_float4(acc.x * inv, acc.y * inv, acc.z * inv, acc.w * inv));
       } else {
         __stcg(reinterpret_cast<float4*>(p.ws_o + (pslot + r) * D + d), acc);
         if (d == 0)
@@ -763,10 +757,8 @@ __global__ void __launch_bounds__(kThreadsTc, 1) decode_tc_kernel(const __grid_c
           acc.w += w * v.w;
         }
         const float inv = s_cinv[r];
-        store_from_float(p.out, out_base + e, p.out_dtype, acc.x * inv);
-        store_from_float(p.out, out_base + e + 1, p.out_dtype, acc.y * inv);
-        store_from_float(p.out, out_base + e + 2, p.out_dtype, acc.z * inv);
-        store_from_float(p.out, out_base + e + 3, p.out_dtype, acc.w * inv);
+        store4_from_float(p.out, out_base + e, p.out_dtype,
+                          make_float4(acc.x * inv, acc.y * inv, acc.z * inv, acc.w * inv));
       }
       break;  // one item per CTA in cluster mode
     }

@@ -1012,6 +1012,8 @@ int pkv_paged_attention(const pkv_attention_args* a, void* stream_) {
     if (a->plan_host[7] != a->n_queries)
       return pkv::fail(PKV_VALUE_ERROR, "plan was built for %d queries, call has %lld", a->plan_host[7],
                        static_cast<long long>(a->n_queries));
+    if (reinterpret_cast<uintptr_t>(a->out) % 16)
+      return pkv::fail(PKV_VALUE_ERROR, "attention output must be 16-byte aligned (vector stores)");
     TcParams t;
     t.q = a->q;
     t.q_dtype = a->q_dtype;
