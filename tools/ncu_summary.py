@@ -79,7 +79,8 @@ def main():
             if alg:
                 a = float(alg)
                 entry["algorithmic"] = a
-                alg_s = f"{a / 1e6:.1f} MB" if a < 1e10 else f"{a / 1e9:.1f} GFLOP"
+                # prefill (tensor-bound) captures carry FLOPs, decode ones bytes
+                alg_s = f"{a / 1e9:.1f} GFLOP" if name.startswith("c4") else f"{a / 1e6:.1f} MB"
             summary[name] = entry
             md.append(f"| {name} | `{d['kernel'][:60]}` | {t * 1e6:.1f} | {rd / 1e6:.1f} | {wr / 1e6:.1f} | "
                       f"{alg_s} | {entry['dram_pct_peak'] or 0:.1f} | {entry['sm_pct'] or 0:.1f} | "
