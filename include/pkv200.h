@@ -352,6 +352,20 @@ typedef struct pkv_decode_io {
 } pkv_decode_io;
 int pkv_decode_step(pkv_step_stage_args* stage, pkv_attention_args* attn, pkv_decode_io* io, void* stream);
 
+/* CUDA-graph mode of the same step: identical host work and semantics, but
+ * the step's device work (input copies, metadata copy, page / mirror aux
+ * kernel, fused append + decode) is recorded and replayed as ONE
+ * cudaGraphLaunch from a cache of executable graphs (one per topology; only
+ * the changed parameters are updated between launches).  Steps with a host
+ * `out_host` copy or on the fp32 path run as pkv_decode_step.  Replaces the
+ * per-token launch sequence of DecodeSession.step (decoder.py:263-284). */
+typedef struct pkv_step_graph pkv_step_graph;
+int pkv_step_graph_create(pkv_step_graph** out);
+void pkv_step_graph_destroy(pkv_step_graph* graphs);
+int pkv_step_graph_stats(pkv_step_graph* graphs, int64_t* launches, int64_t* builds);
+int pkv_decode_step_graph(pkv_step_graph* graphs, pkv_step_stage_args* stage, pkv_attention_args* attn,
+                          pkv_decode_io* io, void* stream);
+
 /* K3   causal / suffix prefill on tcgen05 tensor cores (16-bit caches).
  * Replaces _streaming_attention (attention.py:259-329) under the
  * self-attention and suffix metas (attention.py:81-84, 98-110): the queries

@@ -131,6 +131,10 @@ SIGNATURES = {
     "pkv_attention_plan": (C.c_int, [_vp, _vp, _i64, _i32, _i32, _i32, _i32, _i32, _vp, _i64, _P(_i64)]),
     "pkv_attention_plan_d": (C.c_int, [_vp, _vp, _i64, _i32, _i32, _i32, _i32, _i32, _i32, _vp, _i64, _P(_i64)]),
     "pkv_paged_attention": (C.c_int, [_P(AttentionArgs), _vp]),
+    "pkv_step_graph_create": (C.c_int, [_P(_vp)]),
+    "pkv_step_graph_destroy": (None, [_vp]),
+    "pkv_step_graph_stats": (C.c_int, [_vp, _P(_i64), _P(_i64)]),
+    "pkv_decode_step_graph": (C.c_int, [_vp, _vp, _vp, _vp, _vp]),
     "pkv_decode_step": (C.c_int, [_P(StepStageArgs), _P(AttentionArgs), _P(DecodeIO), _vp]),
     "pkv_prefill_supported": (C.c_int, [_i32, _i32, _i32, _i32, _i32]),
     "pkv_prefill_plan_ints": (_i64, [_vp, _i64, _i32, _i32]),

@@ -35,6 +35,13 @@ _ZERO_COPY_OUT = _os.environ.get("PKV_ZERO_COPY_OUT", "1") != "0"
 # Pinned host q / k_new / v_new read by the kernel through their mapped
 # pointers (no H2D copy ahead of the launch).  Experiment switch.
 _ZERO_COPY_IN = _os.environ.get("PKV_ZERO_COPY_IN", "0") == "1"
+# CUDA-graph mode of the repeated step (pkv_decode_step_graph): its kernels
+# replayed as one cached graph.  Off by default (PKV_STEP_GRAPH=1 or
+# DecodeBatch.use_graph turns it on): measured on C2 it saves ~4 us of host
+# launch time but the graph executes ~10 us later on the GPU (host inputs:
+# 165-172 vs 164 us per step; device inputs: 146-154 vs 137 us,
+# tools/e2e_graph_ab.py), so the launch-by-launch step is faster.
+_STEP_GRAPH = _os.environ.get("PKV_STEP_GRAPH", "0") == "1"
 
 
 class _FastStep:
@@ -44,7 +51,7 @@ class _FastStep:
     batch's membership, attached stores and staging buffers are unchanged."""
 
     __slots__ = ("tensors", "ptrs", "args", "args_p", "io", "io_p", "result", "out_host", "out_dev", "tensor",
-                 "mirror", "fixed", "nstores", "bufs")
+                 "mirror", "fixed", "nstores", "bufs", "graph_ok")
 
     def __init__(self, batch, tensors, result, out_host, out_dev, tensor):
         self.tensors = tensors
@@ -58,6 +65,9 @@ class _FastStep:
         self.fixed = batch._stage_fixed
         self.nstores = len(batch.pool._stores)
         self.bufs = batch._bufs
+        # graph memcpy nodes need pinned (or device) sources and no host out copy
+        self.graph_ok = out_host is None and all(
+            t.is_cuda or t.is_pinned() for t in tensors[:3])
 
     def valid(self, batch, q, k, v, out) -> bool:
         t = self.tensors
@@ -108,8 +118,29 @@ class DecodeBatch:
         self._keep = []
         self._store_ptrs = {}
         self._fast = {}
+        self._graphs = None  # pkv_step_graph cache of the repeated step, created on first use
+        self.use_graph = _STEP_GRAPH
         self._dev_index = self.device.index if self.device.index is not None else torch.cuda.current_device()
         self.set_sequences(seq_ids, capacity)
+
+    def __del__(self):
+        g = getattr(self, "_graphs", None)
+        if g is not None and _lib is not None:
+            try:
+                torch_sync = __import__("torch").cuda.synchronize
+                torch_sync(self.device)  # executable graphs may still run
+                self._lib.pkv_step_graph_destroy(g)
+            except Exception:
+                pass
+            self._graphs = None
+
+    def graph_stats(self):
+        """(graph launches, graph builds) of the repeated-step CUDA graphs."""
+        if self._graphs is None:
+            return 0, 0
+        n, b = C.c_int64(), C.c_int64()
+        _lib.check(self._lib.pkv_step_graph_stats(self._graphs, C.byref(n), C.byref(b)), "pkv_step_graph_stats")
+        return n.value, b.value
 
     def set_sequences(self, seq_ids, capacity: int | None = None) -> None:
         """Change the batch membership (continuous batching): later steps
@@ -352,7 +383,14 @@ class DecodeBatch:
         if e.mirror is not self._stage_mirror:
             e.args.block_table, e.args.bt_stride = st_args.mirror_dev, st_args.mirror_cols
             e.mirror = self._stage_mirror
-        st = self._lib.pkv_decode_step(self._stage_p, e.args_p, e.io_p, C.c_void_p(sp))
+        if e.graph_ok and self.use_graph:
+            if self._graphs is None:
+                h = C.c_void_p()
+                _lib.check(self._lib.pkv_step_graph_create(C.byref(h)), "pkv_step_graph_create")
+                self._graphs = h
+            st = self._lib.pkv_decode_step_graph(self._graphs, self._stage_p, e.args_p, e.io_p, C.c_void_p(sp))
+        else:
+            st = self._lib.pkv_decode_step(self._stage_p, e.args_p, e.io_p, C.c_void_p(sp))
         if st:
             _lib.check(st, "pkv_decode_step")
         self._cur = slot

@@ -26,7 +26,7 @@ NVCC_FLAGS = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "--expt-r
               "-Xptxas", "-v"] + ARCH
 CXX_FLAGS = ["-O3", "-std=c++17", "-fPIC", "-Wall"]
 
-CU_SOURCES = ["kernels.cu", "decode_tc.cu", "prefill_sm100.cu"]
+CU_SOURCES = ["kernels.cu", "decode_tc.cu", "prefill_sm100.cu", "step_graph.cu"]
 CXX_SOURCES = ["pool.cpp", "status.cpp"]
 
 

@@ -51,6 +51,7 @@
 
 #include "common.cuh"
 #include "decode_tc.h"
+#include "step_graph.h"
 
 namespace pkv {
 
@@ -1164,6 +1165,13 @@ int launch_decode_tc(TcParams p, const int32_t* plan_host, int kv_dtype, int hea
       cudaFuncSetAttribute(reinterpret_cast<const void*>(fn), cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
       nonportable[key] = true;
     }
+  }
+  if (launch_recorder()) {  // CUDA-graph mode of the batched step
+    record_kernel(fn, dim3(static_cast<unsigned>(grid)), dim3(kThreadsTc), static_cast<unsigned>(smem),
+                  static_cast<unsigned>(cluster), p);
+    return PKV_OK;
+  }
+  if (cluster > 1) {
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(static_cast<unsigned>(grid));
     cfg.blockDim = dim3(kThreadsTc);

@@ -35,6 +35,7 @@
 #include "common.cuh"
 #include "pool_internal.h"
 #include "decode_tc.h"
+#include "step_graph.h"
 #include "pkv200.h"
 #include "status.h"
 
@@ -926,19 +927,33 @@ static int decode_step_stage(pkv_step_stage_args* a, cudaStream_t stream, pkv_ap
   if (page_work && (a->row_bytes & 1)) return fail_back(pkv::fail(PKV_CONFIG_ERROR, "row bytes must be even"));
   if (pkv_debug_should_fail(PKV_FAIL_STEP_UPLOAD))
     return fail_back(pkv::fail(PKV_CUDA_ERROR, "step metadata upload: injected failure"));
-  cudaError_t e = cudaMemcpyAsync(a->meta_dev, a->meta_host, static_cast<size_t>(total) * 4,
-                                  cudaMemcpyHostToDevice, stream);
-  if (e != cudaSuccess)
-    return fail_back(pkv::fail(PKV_CUDA_ERROR, "step metadata upload: %s", pkv::cuda_err_str(e)));
-  if (a->slot_event) cudaEventRecord(static_cast<cudaEvent_t>(a->slot_event), stream);
+  const bool recording = pkv::launch_recorder() != nullptr;  // CUDA-graph mode: record, do not issue
+  if (recording && pkv::graph_copies()) {
+    pkv::record_copy(a->meta_dev, a->meta_host, static_cast<size_t>(total) * 4);
+    if (a->slot_event) pkv::record_event(static_cast<cudaEvent_t>(a->slot_event));
+  } else {
+    cudaError_t e = cudaMemcpyAsync(a->meta_dev, a->meta_host, static_cast<size_t>(total) * 4,
+                                    cudaMemcpyHostToDevice, stream);
+    if (e != cudaSuccess)
+      return fail_back(pkv::fail(PKV_CUDA_ERROR, "step metadata upload: %s", pkv::cuda_err_str(e)));
+    if (a->slot_event) cudaEventRecord(static_cast<cudaEvent_t>(a->slot_event), stream);
+  }
   stamp(5);
   if (page_work || n_pairs) {
     const int n_st = page_work ? a->n_stores : 0;
     const int64_t blocks = std::max<int64_t>(n_st * (n_zero + n_copies), (n_pairs + 255) / 256);
-    step_aux_kernel<<<static_cast<unsigned>(std::min<int64_t>(std::max<int64_t>(blocks, 1), 65535)), 256, 0,
-                      stream>>>(reinterpret_cast<const uint64_t*>(a->meta_dev + ptr_off), n_st,
-                                a->meta_dev + zero_off, n_zero, a->meta_dev + trip_off, n_copies,
-                                a->mirror_dev, a->meta_dev + pairs_off, n_pairs, a->row_bytes, a->page_size);
+    const unsigned grid = static_cast<unsigned>(std::min<int64_t>(std::max<int64_t>(blocks, 1), 65535));
+    const uint64_t* caches = reinterpret_cast<const uint64_t*>(a->meta_dev + ptr_off);
+    const int32_t* zero_p = a->meta_dev + zero_off;
+    const int32_t* trip_p = a->meta_dev + trip_off;
+    const int32_t* pairs_p = a->meta_dev + pairs_off;
+    const int ps = a->page_size;
+    if (recording)
+      pkv::record_kernel(step_aux_kernel, dim3(grid), dim3(256), 0u, 1u, caches, n_st, zero_p, n_zero, trip_p,
+                         n_copies, a->mirror_dev, pairs_p, n_pairs, a->row_bytes, ps);
+    else
+      step_aux_kernel<<<grid, 256, 0, stream>>>(caches, n_st, zero_p, n_zero, trip_p, n_copies, a->mirror_dev,
+                                                pairs_p, n_pairs, a->row_bytes, ps);
     const cudaError_t le = cudaGetLastError();
     if (le != cudaSuccess) return fail_back(pkv::fail(PKV_CUDA_ERROR, "step aux kernel: %s", pkv::cuda_err_str(le)));
     ++a->launches;
@@ -1131,6 +1146,10 @@ int pkv_decode_step(pkv_step_stage_args* stage, pkv_attention_args* attn, pkv_de
   auto h2d = [&](const void* src, const void* dst, int64_t bytes, const char* what) -> int {
     if (!src) return PKV_OK;
     if (!dst || bytes <= 0) return pkv::fail(PKV_VALUE_ERROR, "%s: host source without device buffer", what);
+    if (pkv::launch_recorder() && pkv::graph_copies()) {
+      pkv::record_copy(const_cast<void*>(dst), src, static_cast<size_t>(bytes));
+      return PKV_OK;
+    }
     cudaError_t e = cudaMemcpyAsync(const_cast<void*>(dst), src, static_cast<size_t>(bytes),
                                     cudaMemcpyHostToDevice, stream);
     return e == cudaSuccess ? PKV_OK : pkv::fail(PKV_CUDA_ERROR, "%s upload: %s", what, pkv::cuda_err_str(e));

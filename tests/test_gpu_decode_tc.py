@@ -389,6 +389,7 @@ def test_repeated_buffers_take_the_fast_path(packed):
         ctx.append([k, v])
     B = 3
     batch = DecodeBatch(store, list(range(B)), cfg)
+    batch.use_graph = True  # the CUDA-graph mode of the repeated step
     if packed:
         qh, kh, vh = DecodeBatch.packed_host_inputs(B, hq, hkv, d, dtype)
     else:
@@ -416,6 +417,11 @@ def test_repeated_buffers_take_the_fast_path(packed):
     for i in range(B):
         kk, vv = store.gather(i, ctx[i][0].shape[0])
         assert torch.equal(kk, ctx[i][0]) and torch.equal(vv, ctx[i][1])
+    # the repeated step ran as cached CUDA graphs (pinned inputs, zero-copy
+    # out): a few topologies (ring slots x aux kernel or not), many launches;
+    # the graph-free step is covered by test_host_buffer_step_single_native_call
+    launches, builds = batch.graph_stats()
+    assert launches >= 30 and 1 <= builds <= 16, (launches, builds)
     # a membership change invalidates the prepared calls
     batch.set_sequences([0, 1])
     assert not batch._fast
