@@ -35,6 +35,13 @@ _ZERO_COPY_OUT = _os.environ.get("PKV_ZERO_COPY_OUT", "1") != "0"
 # Pinned host q / k_new / v_new read by the kernel through their mapped
 # pointers (no H2D copy ahead of the launch).  Experiment switch.
 _ZERO_COPY_IN = _os.environ.get("PKV_ZERO_COPY_IN", "0") == "1"
+# Pinned host k_new / v_new only (the default): read by the kernel through
+# their mapped pointers (the fused append and the new token's key row, 256-B
+# coalesced reads spread over the launch), while the queries still go by DMA
+# — the decode launch waits for the third of the inputs it needs first
+# instead of all of them (C2 e2e 174-181 -> 160-161 us per step on a 20 GB/s
+# PCIe box).  PKV_ZERO_COPY_KV=0 copies all three.
+_ZERO_COPY_KV = _os.environ.get("PKV_ZERO_COPY_KV", "1") != "0"
 # CUDA-graph mode of the repeated step (pkv_decode_step_graph): its kernels
 # replayed as one cached graph.  Off by default (PKV_STEP_GRAPH=1 or
 # DecodeBatch.use_graph turns it on): measured on C2 it saves ~4 us of host
@@ -311,7 +318,7 @@ class DecodeBatch:
         return (base[:qn].view(n, hq, d), base[qn:qn + kvn].view(n, hkv, d),
                 base[qn + kvn:qn + 2 * kvn].view(n, hkv, d))
 
-    def _input(self, x, dtype, shape, name):
+    def _input(self, x, dtype, shape, name, zero_copy=False):
         """-> (device tensor, host pointer or None, bytes).  CPU inputs are
         copied by the native step into a persistent device buffer (pin them
         for an asynchronous copy); device inputs are used in place.  Records
@@ -323,7 +330,7 @@ class DecodeBatch:
                 and x.is_contiguous():  # fast path: a host tensor ready to copy
             self._keep.append(x)
             self._direct.append(True)
-            if _ZERO_COPY_IN and x.is_pinned():
+            if (_ZERO_COPY_IN or zero_copy) and x.is_pinned():
                 return x, None, 0  # the kernel reads the mapped host rows itself
             return self._buffer(name, shape, dtype), x.data_ptr(), x.nbytes
         self._direct.append(False)
@@ -459,8 +466,8 @@ class DecodeBatch:
         q_t = qd if qd in self._qcodes else torch.float32
         q, q_host, q_bytes = self._input(queries, q_t, (n, cfg.head_count, cfg.head_dim), "queries")
         kv_shape = (n, cfg.kv_head_count, cfg.head_dim)
-        k, k_host, kv_bytes = self._input(k_new, store.torch_dtype, kv_shape, "k_new")
-        v, v_host, _ = self._input(v_new, store.torch_dtype, kv_shape, "v_new")
+        k, k_host, kv_bytes = self._input(k_new, store.torch_dtype, kv_shape, "k_new", _ZERO_COPY_KV)
+        v, v_host, _ = self._input(v_new, store.torch_dtype, kv_shape, "v_new", _ZERO_COPY_KV)
         if q_host and k_host == q_host + q_bytes and v_host == k_host + kv_bytes and q_t is store.torch_dtype \
                 and self._one_allocation(queries, k_new, v_new):
             # q | k | v adjacent in one host buffer (a fused QKV projection's
