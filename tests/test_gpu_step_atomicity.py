@@ -47,27 +47,51 @@ def _refcounts(pool):
     return [pool.page_refcount(p) for p in range(pool.capacity_pages)]
 
 
+class _Repeated:
+    """A serving loop's step: the same pinned host buffers and device `out`
+    every token (DecodeBatch's prepared fast path, optionally as CUDA graphs)."""
+
+    def __init__(self, batch, n, graph):
+        self.batch = batch
+        batch.use_graph = graph
+        self.q = torch.empty((n, 8, 128), dtype=torch.bfloat16).pin_memory()
+        self.k = torch.empty((n, 2, 128), dtype=torch.bfloat16).pin_memory()
+        self.v = torch.empty((n, 2, 128), dtype=torch.bfloat16).pin_memory()
+        self.out = torch.empty((n, 8, 128), dtype=torch.float32, device="cuda")
+
+    def step(self, q, k, v):
+        torch.cuda.synchronize()  # the previous step has read the buffers
+        self.q.copy_(q)
+        self.k.copy_(k)
+        self.v.copy_(v)
+        return self.batch.step(self.q, self.k, self.v, out=self.out).clone()
+
+
+@pytest.mark.parametrize("mode", ["call", "repeated", "graph"])
 @pytest.mark.parametrize("site", [_lib.PKV_FAIL_STEP_UPLOAD, _lib.PKV_FAIL_STEP_LAUNCH])
-def test_failed_step_rolls_back_and_retry_matches_twin(site):
+def test_failed_step_rolls_back_and_retry_matches_twin(site, mode):
     pool_a, store_a, batch_a, ids = _setup(0)
     pool_b, store_b, batch_b, _ = _setup(0)
+    step_a = batch_a.step if mode == "call" else _Repeated(batch_a, len(ids), mode == "graph").step
     for i in range(3):  # a few normal steps first (mirror and ring in use)
         q, k, v = _inputs(len(ids), i)
-        batch_a.step(q, k, v)
+        step_a(q, k, v)
         batch_b.step(q, k, v)
     torch.cuda.synchronize()
     before = (pool_a.dump(), _refcounts(pool_a))
     q, k, v = _inputs(len(ids), 99)
     _lib.load().pkv_debug_inject_failure(site)
     with pytest.raises(DeviceError, match="injected"):
-        batch_a.step(q, k, v)
+        step_a(q, k, v)
     torch.cuda.synchronize()
     assert (pool_a.dump(), _refcounts(pool_a)) == before
-    out_a = batch_a.step(q, k, v)
+    out_a = step_a(q, k, v)
     out_b = batch_b.step(q, k, v)
     torch.cuda.synchronize()
     assert pool_a.dump() == pool_b.dump()
     assert torch.equal(out_a, out_b)
+    if mode == "graph":
+        assert batch_a.graph_stats()[0] >= 3  # every prepared call after the first
     for s in ids:  # the retried step wrote the same K/V into the same pages
         ka, va = store_a.gather(s, pool_a.table(s).logical_len)
         kb, vb = store_b.gather(s, pool_b.table(s).logical_len)
