@@ -898,8 +898,11 @@ int plan_decode(const int32_t* nk, const int32_t* row, int64_t nq, int page_size
   // leave; both tunable for experiments
   static const int64_t cost_kb = [] {
     const char* e = std::getenv("PKV_DECODE_COST_KB");
-    // 600 KB: C2 5.53 -> 5.58 TB/s over 3 reps, C3 / C5 within noise
-    return e ? std::max<int64_t>(0, std::atoll(e)) : int64_t(600);
+    // 400 KB (round 2, current kernel): C2 5.87 -> 5.99 TB/s over 3 reps
+    // (350 / 450 / 500 / 600: 5.95 / 5.93 / 5.95 / 5.87); C3, C5 within noise.
+    // A per-CTA timeline fit (tools/trace_decode.py, CORR=1) gives ~4.5 us
+    // per item vs ~1.1 us per 64 KB page on C2.
+    return e ? std::max<int64_t>(0, std::atoll(e)) : int64_t(400);
   }();
   const int64_t ovh = ((cost_kb << 10) / page_bytes) * (waves > 0 ? waves : 1);
   bool whole = false;
