@@ -843,8 +843,9 @@ static int decode_step_stage(pkv_step_stage_args* a, cudaStream_t stream, pkv_ap
   a->meta_used = 0;
   a->needs_resync = 0;
   a->launches = 0;
-  if (a->slot_event) {  // the slot's previous upload has landed
-    cudaError_t e = cudaEventSynchronize(static_cast<cudaEvent_t>(a->slot_event));
+  if (a->slot_event) {  // the slot's previous upload has landed (a query first: it almost always has)
+    cudaError_t e = cudaEventQuery(static_cast<cudaEvent_t>(a->slot_event));
+    if (e == cudaErrorNotReady) e = cudaEventSynchronize(static_cast<cudaEvent_t>(a->slot_event));
     if (e != cudaSuccess) return pkv::fail(PKV_CUDA_ERROR, "slot event: %s", pkv::cuda_err_str(e));
   }
   stamp(2);
