@@ -157,6 +157,9 @@ int pkv_page_zero(void* k_cache, void* v_cache, const int32_t* pages, int64_t n,
  * rest of dst */
 int pkv_page_copy(void* k_cache, void* v_cache, const int32_t* triples, int64_t n,
                   int64_t row_bytes, int32_t page_size, void* stream);
+/* one copy (a fork's partial trailing page) without a metadata upload */
+int pkv_page_copy1(void* k_cache, void* v_cache, int64_t src_page, int64_t dst_page, int64_t rows,
+                   int64_t row_bytes, int32_t page_size, void* stream);
 
 /* K1   KvStore.assign scatter   store.py:146-150 (reshape-and-cache):
  * cache[row(tok_row[i*row_stride], tok_pos[i])] = new[i] for K and V, where

@@ -63,10 +63,13 @@ __global__ void page_zero_kernel(char* k, char* v, const int32_t* pages, int64_t
   }
 }
 
+// triples == NULL: one copy given by (src0, dst0, rows0) (a fork's partial
+// page: no metadata upload)
 __global__ void page_copy_kernel(char* k, char* v, const int32_t* triples, int64_t n,
-                                 int64_t row_bytes, int page_size) {
+                                 int64_t row_bytes, int page_size, int64_t src0, int64_t dst0, int64_t rows0) {
   for (int64_t i = blockIdx.x; i < n; i += gridDim.x) {
-    const int64_t src = triples[3 * i], dst = triples[3 * i + 1], rows = triples[3 * i + 2];
+    const int64_t src = triples ? triples[3 * i] : src0, dst = triples ? triples[3 * i + 1] : dst0;
+    const int64_t rows = triples ? triples[3 * i + 2] : rows0;
     const int64_t pb = row_bytes * page_size;
     const int64_t keep = rows * row_bytes;
     // src == dst would alias; the allocator never reports that
@@ -679,7 +682,21 @@ int pkv_page_copy(void* k_cache, void* v_cache, const int32_t* triples, int64_t 
   page_copy_kernel<<<static_cast<unsigned>(n < 65535 ? n : 65535), 256, 0,
                      static_cast<cudaStream_t>(stream)>>>(static_cast<char*>(k_cache),
                                                           static_cast<char*>(v_cache), triples, n,
-                                                          row_bytes, page_size);
+                                                          row_bytes, page_size, 0, 0, 0);
+  PKV_CHECK_LAUNCH();
+  return PKV_OK;
+}
+
+int pkv_page_copy1(void* k_cache, void* v_cache, int64_t src_page, int64_t dst_page, int64_t rows,
+                   int64_t row_bytes, int32_t page_size, void* stream) {
+  pkv::DeviceGuard guard(static_cast<cudaStream_t>(stream));
+  if (row_bytes & 1) return pkv::fail(PKV_CONFIG_ERROR, "row bytes must be even");
+  if (src_page < 0 || dst_page < 0 || src_page == dst_page || rows < 0 || rows > page_size)
+    return pkv::fail(PKV_VALUE_ERROR, "bad page copy (%lld -> %lld, %lld rows)", static_cast<long long>(src_page),
+                     static_cast<long long>(dst_page), static_cast<long long>(rows));
+  page_copy_kernel<<<1, 256, 0, static_cast<cudaStream_t>(stream)>>>(
+      static_cast<char*>(k_cache), static_cast<char*>(v_cache), nullptr, 1, row_bytes, page_size, src_page, dst_page,
+      rows);
   PKV_CHECK_LAUNCH();
   return PKV_OK;
 }
