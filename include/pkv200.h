@@ -157,6 +157,11 @@ int pkv_page_zero(void* k_cache, void* v_cache, const int32_t* pages, int64_t n,
  * rest of dst */
 int pkv_page_copy(void* k_cache, void* v_cache, const int32_t* triples, int64_t n,
                   int64_t row_bytes, int32_t page_size, void* stream);
+/* host -> device copy of a pinned staging buffer on `stream`, then (optional)
+ * cudaEventRecord(event); and a wait for such an event (query first) — the
+ * metadata staging ring of the Python shim in two calls */
+int pkv_copy_h2d_record(void* dst, const void* src, int64_t bytes, void* event, void* stream);
+int pkv_event_wait(void* event);
 /* one copy (a fork's partial trailing page) without a metadata upload */
 int pkv_page_copy1(void* k_cache, void* v_cache, int64_t src_page, int64_t dst_page, int64_t rows,
                    int64_t row_bytes, int32_t page_size, void* stream);

@@ -117,6 +117,8 @@ SIGNATURES = {
     "pkv_pool_mirror_export": (C.c_int, [_vp, _P(_i32), _i64, _i64]),
     "pkv_mirror_apply": (C.c_int, [_vp, _vp, _i64, _vp]),
     "pkv_page_zero": (C.c_int, [_vp, _vp, _vp, _i64, _i64, _vp]),
+    "pkv_copy_h2d_record": (C.c_int, [_vp, _vp, _i64, _vp, _vp]),
+    "pkv_event_wait": (C.c_int, [_vp]),
     "pkv_page_copy1": (C.c_int, [_vp, _vp, _i64, _i64, _i64, _i64, _i32, _vp]),
     "pkv_page_copy": (C.c_int, [_vp, _vp, _vp, _i64, _i64, _i32, _vp]),
     "pkv_kv_append_range": (C.c_int, [_vp, _vp, _i64, _i32, _i32, _vp, _i64, _i32, _vp, _vp, _i64, _vp]),

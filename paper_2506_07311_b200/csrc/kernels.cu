@@ -687,6 +687,27 @@ int pkv_page_copy(void* k_cache, void* v_cache, const int32_t* triples, int64_t 
   return PKV_OK;
 }
 
+int pkv_copy_h2d_record(void* dst, const void* src, int64_t bytes, void* event, void* stream) {
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  pkv::DeviceGuard guard(st);
+  if (bytes > 0) {
+    const cudaError_t e = cudaMemcpyAsync(dst, src, static_cast<size_t>(bytes), cudaMemcpyHostToDevice, st);
+    if (e != cudaSuccess) return pkv::fail(PKV_CUDA_ERROR, "metadata upload: %s", pkv::cuda_err_str(e));
+  }
+  if (event) {
+    const cudaError_t e = cudaEventRecord(static_cast<cudaEvent_t>(event), st);
+    if (e != cudaSuccess) return pkv::fail(PKV_CUDA_ERROR, "metadata upload event: %s", pkv::cuda_err_str(e));
+  }
+  return PKV_OK;
+}
+
+int pkv_event_wait(void* event) {
+  if (!event) return PKV_OK;
+  cudaError_t e = cudaEventQuery(static_cast<cudaEvent_t>(event));
+  if (e == cudaErrorNotReady) e = cudaEventSynchronize(static_cast<cudaEvent_t>(event));
+  return e == cudaSuccess ? PKV_OK : pkv::fail(PKV_CUDA_ERROR, "event wait: %s", pkv::cuda_err_str(e));
+}
+
 int pkv_page_copy1(void* k_cache, void* v_cache, int64_t src_page, int64_t dst_page, int64_t rows,
                    int64_t row_bytes, int32_t page_size, void* stream) {
   pkv::DeviceGuard guard(static_cast<cudaStream_t>(stream));

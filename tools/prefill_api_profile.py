@@ -1,0 +1,78 @@
+"""Host time of one isolated paged_attention (prefill meta, 8192 tokens):
+perf_counter around the call (no sync), with a cProfile of the same."""
+import cProfile
+import os
+import pstats
+import sys
+import time
+
+import numpy as np
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+from paper_2506_07311_b200 import AttentionConfig, KvStore, MaskMeta, PagePool, paged_attention  # noqa: E402
+
+dev = torch.device("cuda:0")
+n, hq, hkv, d, ps = 8192, 32, 8, 128, 16
+pool = PagePool(n // ps + 8, page_size=ps)
+store = KvStore(pool, hkv, d, dtype=torch.bfloat16, device=dev)
+pool.reserve(0, n)
+k = torch.randn((n, hkv, d), device=dev).bfloat16()
+store.assign(0, np.arange(n), k, k)
+cfg = AttentionConfig(head_count=hq, head_dim=d, page_size=ps, kv_head_count=hkv)
+meta = MaskMeta.self_attention(store.batch_view([0]))
+q = torch.randn((n, hq, d), device=dev).bfloat16()
+for _ in range(3):
+    paged_attention(q, store, meta, cfg)
+torch.cuda.synchronize()
+ts = []
+for _ in range(20):
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    paged_attention(q, store, meta, cfg)
+    ts.append((time.perf_counter() - t0) * 1e6)
+print("isolated paged_attention host us: p50 %.1f min %.1f" % (np.median(ts), np.min(ts)))
+pr = cProfile.Profile()
+for _ in range(20):
+    torch.cuda.synchronize()
+    pr.enable()
+    paged_attention(q, store, meta, cfg)
+    pr.disable()
+pstats.Stats(pr).sort_stats("tottime").print_stats(15)
+
+# piecewise host timing of one isolated call's steps
+from paper_2506_07311_b200 import attention as A  # noqa: E402
+from paper_2506_07311_b200 import _lib  # noqa: E402
+from paper_2506_07311_b200.store import stage_upload  # noqa: E402
+
+
+def t(fn, reps=20):
+    out = []
+    for _ in range(reps):
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        fn()
+        out.append((time.perf_counter() - t0) * 1e6)
+    return round(float(np.median(out)), 1)
+
+
+view = meta.view
+runs = A.suffix_runs(meta)
+rows = np.asarray([pool.table(0).mirror_row], dtype=np.int32)
+plan = _lib.prefill_plan(runs[0], runs[1], view.lengths, rows, hq, hkv, True)
+print({
+    "check_queries": t(lambda: A._check_queries(q, meta, cfg)),
+    "tables_info": t(lambda: pool.tables_info(view.ids)),
+    "allowed_key_counts": t(lambda: A.allowed_key_counts(meta, cfg.causal)),
+    "q_tensor": t(lambda: A._q_tensor(q, dev)),
+    "prefill_route": t(lambda: A._prefill_route(meta, cfg, store.dtype_code, "auto")),
+    "device_table": t(lambda: pool.device_table(dev)),
+    "out_empty": t(lambda: torch.empty((n, hq, d), dtype=torch.float32, device=dev)),
+    "q_to": t(lambda: q.to(store.k_cache.dtype).contiguous()),
+    "prefill_plan": t(lambda: _lib.prefill_plan(runs[0], runs[1], view.lengths, rows, hq, hkv, True)),
+    "stage_upload": t(lambda: stage_upload(dev, plan.reshape(-1))),
+    "launch_prefill_total": t(lambda: A._launch_prefill(q, meta, cfg, runs, k=store.k_cache, v=store.v_cache,
+                                                        kv_code=store.dtype_code, bt=pool.device_table(dev),
+                                                        rows=rows, out_dtype=torch.float32, device=dev)),
+    "paged_attention_total": t(lambda: paged_attention(q, store, meta, cfg)),
+})
