@@ -44,9 +44,13 @@ def _stale(obj: str, deps: list[str]) -> bool:
     return any(os.path.getmtime(d) > t for d in deps)
 
 
-def build(verbose: bool = False, force: bool = False) -> str:
+def build(verbose: bool = False, force: bool = False, defines=(), out: str = OUT, build_dir: str = BUILD) -> str:
+    """Compile and link the library.  `defines` / `out` / `build_dir` build
+    an experiment variant (e.g. -DPKV_K3_PHASES) next to the product one;
+    load it with PKV200_LIB."""
     nvcc = _nvcc()
-    os.makedirs(BUILD, exist_ok=True)
+    os.makedirs(build_dir, exist_ok=True)
+    dflags = [f"-D{d}" for d in defines]
     headers = [os.path.join(CSRC, f) for f in os.listdir(CSRC) if f.endswith((".h", ".cuh"))]
     headers.append(os.path.join(INCLUDE, "pkv200.h"))
     objs = []
@@ -55,32 +59,32 @@ def build(verbose: bool = False, force: bool = False) -> str:
         path = os.path.join(CSRC, src)
         if not os.path.exists(path):
             continue
-        obj = os.path.join(BUILD, src + ".o")
+        obj = os.path.join(build_dir, src + ".o")
         objs.append(obj)
         if force or _stale(obj, [path] + headers):
-            cmd = [nvcc, *NVCC_FLAGS, "-I", INCLUDE, "-I", CSRC, "-c", path, "-o", obj]
+            cmd = [nvcc, *NVCC_FLAGS, *dflags, "-I", INCLUDE, "-I", CSRC, "-c", path, "-o", obj]
             r = subprocess.run(cmd, capture_output=True, text=True)
             logs.append(r.stderr)
             if r.returncode:
                 raise RuntimeError(f"nvcc failed for {src}:\n{r.stderr[-8000:]}")
     for src in CXX_SOURCES:
         path = os.path.join(CSRC, src)
-        obj = os.path.join(BUILD, src + ".o")
+        obj = os.path.join(build_dir, src + ".o")
         objs.append(obj)
         if force or _stale(obj, [path] + headers):
             cmd = ["g++", *CXX_FLAGS, "-I", INCLUDE, "-I", CSRC, "-c", path, "-o", obj]
             r = subprocess.run(cmd, capture_output=True, text=True)
             if r.returncode:
                 raise RuntimeError(f"g++ failed for {src}:\n{r.stderr[-8000:]}")
-    if force or _stale(OUT, objs):
-        cmd = [nvcc, *ARCH, "-shared", "-cudart", "static", "-o", OUT, *objs, "-lpthread"]
+    if force or _stale(out, objs):
+        cmd = [nvcc, *ARCH, "-shared", "-cudart", "static", "-o", out, *objs, "-lpthread"]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode:
             raise RuntimeError(f"link failed:\n{r.stderr[-8000:]}")
     if verbose:
         for log in logs:
             sys.stderr.write(log)
-    return OUT
+    return out
 
 
 if __name__ == "__main__":

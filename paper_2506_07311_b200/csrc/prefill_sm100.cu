@@ -421,9 +421,26 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int nk = p.causal ? min(qpos + 1, kv_len) : kv_len;  // allowed key prefix of this row
     float m_used = -INFINITY, l = 0.f;
     const float2 qs2 = make_float2(p.qscale, p.qscale);
+#ifdef PKV_K3_PHASES
+    // -DPKV_K3_PHASES: clock64 per softmax phase (wait S, TMEM load, max,
+    // exp + store, publish) summed over the tiles of row 0 of each query tile
+    // of CTA 0, into dbg[448 + 8t + k] (tools/bench_prefill.py prints them)
+    long long ph[5] = {0, 0, 0, 0, 0}, pc = clock64();
+#define PHASE(k)                      \
+  do {                                \
+    const long long now_ = clock64(); \
+    ph[k] += now_ - pc;               \
+    pc = now_;                        \
+  } while (0)
+#else
+#define PHASE(k) \
+  do {           \
+  } while (0)
+#endif
     for (int j = 0; j < nt[t]; ++j) {
       mbar_wait(bar(B_SF + t), j & 1);
       tc_fence_after();
+      PHASE(0);
       if (r == 0 && j < 64) PDBG(t * 64 + j);
       if (p.dbg && r == 0 && t == 0 && j == 0) p.dbg[512 + 4 * blockIdx.x + 1] = gtime();
       const int kbase = j * kN;
@@ -436,6 +453,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
       for (int c = 0; c < kN / 32; ++c) tmem_ld32(tS + c * 32, v + 32 * c);
       tmem_wait_ld();
+      PHASE(1);
       if (masked) {
         const int lim = nk - kbase;  // element e is allowed iff e < lim
 #pragma unroll
@@ -466,6 +484,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           tmem_st32(tO + c * 32, o);
         }
       }
+      PHASE(2);
       // P = 2^(s*qscale - m) rounded to 16 bits, written over S
       const float2 negm2 = make_float2(-m_used, -m_used);
       float2 l2[4] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
@@ -486,11 +505,18 @@ __global__ void __launch_bounds__(kThreads, 1)
         const float2 a = fadd2(fadd2(l2[0], l2[1]), fadd2(l2[2], l2[3]));
         l += a.x + a.y;
       }
+      PHASE(3);
       tmem_wait_st();
       tc_fence_before();
       mbar_arrive(bar(B_PF + t));
+      PHASE(4);
       if (r == 0 && j < 64) PDBG(128 + t * 64 + j);
     }
+#ifdef PKV_K3_PHASES
+    if (p.dbg && blockIdx.x == 0 && r == 0)
+      for (int k = 0; k < 5; ++k) p.dbg[448 + 8 * t + k] = static_cast<unsigned long long>(ph[k]);
+#endif
+#undef PHASE
     // epilogue: O / l for the valid rows
     if (nt[t] > 0) {
       mbar_wait(bar(B_OD + t), 0);

@@ -94,6 +94,11 @@ def main():
                               "first_S_us_median": round(float(np.median(first)), 2),
                               "gap_us_median": round(float(np.median(gaps)), 2) if gaps else None,
                               "tail_us": round(float((cta[:, 2].max() - np.percentile(cta[:, 2], 50)) / 1e3), 1)}))
+            if full[448:464].any():  # -DPKV_K3_PHASES build: clocks per softmax phase, CTA 0 row 0
+                ph = full[448:464].reshape(2, 8)[:, :5]
+                nt0 = int(max(plan[0, 7], plan[0, 8]))
+                print("softmax phase clk/tile (wait S, tmem ld, max, exp+st, publish):",
+                      [[round(x / max(nt0, 1)) for x in row] for row in ph.tolist()])
             rel = np.where(t > 0, (t - t0) / 1e3, np.nan)
             print("item 0:", plan[0].tolist())
             for name, off in (("S_A ready", 0), ("S_B ready", 64), ("P_A done", 128), ("P_B done", 192),
