@@ -629,6 +629,18 @@ def load_traffic(config_name, fragment=False):
         return None
 
 
+def read_probe_gbs():
+    """Best read-only HBM bandwidth of tools/probes/read_bw.cu on this pool
+    (committed JSON lines): context for the read-dominated decode kernel,
+    whose roofline denominator stays the driver's read+write copy."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "r02", "read_bw.jsonl")) as f:
+            vals = [json.loads(x)["read_gbs"] for x in f if x.startswith("{")]
+        return max(vals) if vals else None
+    except Exception:
+        return None
+
+
 def _free_port() -> int:
     with socket.socket() as s:
         s.bind(("127.0.0.1", 0))
@@ -694,6 +706,8 @@ def line_for(args, config, res, world, peak, peak_src, steps, warmup):
         "roofline": {"bound": "hbm", "kernel": "decode_tc_kernel (K2-TC, K1 append fused)",
                      "achieved": round(k_ach, 1), "peak": peak, "unit": "GB/s", "frac": round(k_ach / peak, 4),
                      "traffic": load_traffic(config, args.fragment), "peak_source": peak_src,
+                     "read_probe_gbs": read_probe_gbs(),
+                     "frac_of_read_probe": (round(k_ach / read_probe_gbs(), 4) if read_probe_gbs() else None),
                      "kernel_ms_mean": res["kernel_ms_mean"],
                      "kernel_share_of_step": res["kernel_ms_mean"] / res["step_ms_mean"],
                      "algorithmic_bytes_per_launch": res["kernel_alg_bytes_mean"],

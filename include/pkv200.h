@@ -128,6 +128,20 @@ int pkv_pool_prepare_append(pkv_pool* pool, const int64_t* seqs, int64_t n, int3
  * on the device with pkv_mirror_apply (or re-uploads the whole matrix after a
  * shape change, signalled by *full_resync). */
 int pkv_pool_mirror_row(pkv_pool* pool, int64_t seq, int32_t* row_out);
+/* One native pass of KvStore.assign's host side (store.py:117-150): scan the
+ * positions (min, max, strictly increasing, contiguous run), check them
+ * against the table's reserved capacity and, for strictly increasing
+ * positions inside it, copy-on-write every touched block in ascending order
+ * (pool.py:238-254; copies_out receives (old, fresh) page pairs for the
+ * caller's page copies).  info_out[5] = {min, max, flags, pages held, mirror
+ * row}; flags: PKV_ASSIGN_*.  Out-of-range or non-increasing positions
+ * privatize nothing (the caller raises / dedupes first). */
+#define PKV_ASSIGN_INCREASING 1
+#define PKV_ASSIGN_CONTIGUOUS 2
+#define PKV_ASSIGN_OUT_OF_RANGE 4
+int pkv_pool_assign_prepare(pkv_pool* pool, int64_t seq, const int64_t* positions, int64_t n,
+                            int64_t* info_out, int64_t* copies_out, int64_t copies_cap, int64_t* n_copies_out);
+
 /* batched table query for n sequence handles: page count and mirror row of
  * each (either output may be NULL); one call instead of two per sequence */
 int pkv_pool_tables_info(pkv_pool* pool, const int64_t* seqs, int64_t n, int64_t* n_pages_out,

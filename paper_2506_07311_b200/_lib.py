@@ -18,6 +18,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("PKV200_LIB") or os.path.join(_HERE, "libpkv200.so")
 
 PKV_F32, PKV_F16, PKV_BF16 = 0, 1, 2
+PKV_ASSIGN_INCREASING, PKV_ASSIGN_CONTIGUOUS, PKV_ASSIGN_OUT_OF_RANGE = 1, 2, 4
 PREFILL_ITEM_INTS = 10  # {q_row0, cnt_a, cnt_b, qpos0, kv_len, row, kv_head, tiles_a, tiles_b, 0}
 
 _STATUS = {
@@ -110,6 +111,7 @@ SIGNATURES = {
     "pkv_pool_census": (C.c_int, [_vp, _P(_i64)]),
     "pkv_pool_free_stack": (C.c_int, [_vp, _P(_u32), _i64, _P(_i64)]),
     "pkv_pool_tables_info": (C.c_int, [_vp, _vp, _i64, _vp, _vp]),
+    "pkv_pool_assign_prepare": (C.c_int, [_vp, _i64, _vp, _i64, _vp, _vp, _i64, _vp]),
     "pkv_pool_mirror_row": (C.c_int, [_vp, _i64, _P(_i32)]),
     "pkv_pool_mirror_shape": (C.c_int, [_vp, _P(_i64), _P(_i64)]),
     "pkv_pool_mirror_drain": (C.c_int, [_vp, _P(_i32), _i64, _P(_i64), _P(_i32)]),

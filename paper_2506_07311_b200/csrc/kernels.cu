@@ -114,25 +114,65 @@ __global__ void step_aux_kernel(const uint64_t* __restrict__ caches, int n_store
     mirror[pairs[2 * i]] = pairs[2 * i + 1];
 }
 
-// one CTA per token (grid-stride); the slot is resolved in-kernel from the
-// block-table mirror (shift/mask: the page size is a power of two)
+// One warp per token (grid-stride over tokens); the slot is resolved
+// in-kernel from the block-table mirror (shift/mask: the page size is a power
+// of two).  kVec (16-byte rows and pointers): every lane keeps four 16-byte
+// K and four V loads in flight before its stores, so a 2 KB row pair moves in
+// one round trip per warp.
 // tok_pos == NULL: a contiguous run, token t at position pos0 + t of mirror
 // row row0 (no per-token metadata at all)
-__global__ void kv_append_kernel(const char* __restrict__ kn, const char* __restrict__ vn,
+template <bool kVec>
+__global__ void __launch_bounds__(256) kv_append_kernel(const char* __restrict__ kn, const char* __restrict__ vn,
                                  int64_t n_tok, const int32_t* __restrict__ tok_row,
                                  int row_stride, const int32_t* __restrict__ tok_pos,
                                  const int32_t* __restrict__ bt, int64_t bt_stride, int log2ps,
                                  char* __restrict__ kc, char* __restrict__ vc, int64_t row_bytes,
                                  int32_t pos0, int32_t row0) {
   const int ps = 1 << log2ps;
-  for (int64_t t = blockIdx.x; t < n_tok; t += gridDim.x) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warps = int64_t(gridDim.x) * (blockDim.x >> 5);
+  for (int64_t t = blockIdx.x * int64_t(blockDim.x >> 5) + (threadIdx.x >> 5); t < n_tok; t += warps) {
     const int32_t pos = tok_pos ? tok_pos[t] : pos0 + static_cast<int32_t>(t);
     const int64_t r = tok_pos ? tok_row[t * row_stride] : row0;
     const int64_t page = bt[r * bt_stride + (pos >> log2ps)];
     const int64_t dst = (page * ps + (pos & (ps - 1))) * row_bytes;
-    copy_bytes(kc + dst, kn + t * row_bytes, row_bytes, threadIdx.x, blockDim.x);
-    copy_bytes(vc + dst, vn + t * row_bytes, row_bytes, threadIdx.x, blockDim.x);
+    if (kVec) {
+      const uint4* ks = reinterpret_cast<const uint4*>(kn + t * row_bytes);
+      const uint4* vs = reinterpret_cast<const uint4*>(vn + t * row_bytes);
+      uint4* kd = reinterpret_cast<uint4*>(kc + dst);
+      uint4* vd = reinterpret_cast<uint4*>(vc + dst);
+      const int64_t n16 = row_bytes >> 4;
+      for (int64_t b = lane; b < n16; b += 128) {
+        uint4 a[4], c[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+          if (b + 32 * u < n16) {
+            a[u] = __ldg(ks + b + 32 * u);
+            c[u] = __ldg(vs + b + 32 * u);
+          }
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+          if (b + 32 * u < n16) {
+            kd[b + 32 * u] = a[u];
+            vd[b + 32 * u] = c[u];
+          }
+      }
+    } else {
+      copy_bytes(kc + dst, kn + t * row_bytes, row_bytes, lane, 32);
+      copy_bytes(vc + dst, vn + t * row_bytes, row_bytes, lane, 32);
+    }
   }
+}
+
+// grid of the append: one warp per token, at most 16 CTAs of 8 warps per SM
+inline unsigned append_blocks(int64_t n_tok) {
+  const int64_t want = (n_tok + 7) / 8;
+  return static_cast<unsigned>(want < 148 * 16 ? want : 148 * 16);
+}
+inline bool append_vec(const void* a, const void* b, const void* c, const void* d, int64_t row_bytes) {
+  const uintptr_t m = reinterpret_cast<uintptr_t>(a) | reinterpret_cast<uintptr_t>(b) |
+                      reinterpret_cast<uintptr_t>(c) | reinterpret_cast<uintptr_t>(d);
+  return (row_bytes & 15) == 0 && (m & 15) == 0;
 }
 
 // K-gather (store.py:152-161, 187-190): out[t] = cache[slot(t)] for the
@@ -731,10 +771,9 @@ int pkv_kv_append(const void* k_new, const void* v_new, int64_t n_tok, const int
   if (page_size <= 0 || (page_size & (page_size - 1)))
     return pkv::fail(PKV_VALUE_ERROR, "page_size must be a power of two");
   if (row_bytes & 1) return pkv::fail(PKV_CONFIG_ERROR, "row bytes must be even");
-  int threads = static_cast<int>(row_bytes / 16);
-  threads = threads < 32 ? 32 : (threads > 256 ? 256 : ((threads + 31) / 32) * 32);
-  const int64_t blocks = n_tok < 65535 * 4 ? n_tok : 65535 * 4;
-  kv_append_kernel<<<static_cast<unsigned>(blocks), threads, 0, static_cast<cudaStream_t>(stream)>>>(
+  auto kern = append_vec(k_new, v_new, k_cache, v_cache, row_bytes) ? kv_append_kernel<true>
+                                                                      : kv_append_kernel<false>;
+  kern<<<append_blocks(n_tok), 256, 0, static_cast<cudaStream_t>(stream)>>>(
       static_cast<const char*>(k_new), static_cast<const char*>(v_new), n_tok, tok_row,
       tok_row_stride, tok_pos, block_table, bt_stride, __builtin_ctz(page_size),
       static_cast<char*>(k_cache), static_cast<char*>(v_cache), row_bytes, 0, 0);
@@ -752,10 +791,9 @@ int pkv_kv_append_range(const void* k_new, const void* v_new, int64_t n_tok, int
   if (page_size <= 0 || (page_size & (page_size - 1)))
     return pkv::fail(PKV_VALUE_ERROR, "page_size must be a power of two");
   if (row_bytes & 1) return pkv::fail(PKV_CONFIG_ERROR, "row bytes must be even");
-  int threads = static_cast<int>(row_bytes / 16);
-  threads = threads < 32 ? 32 : (threads > 256 ? 256 : ((threads + 31) / 32) * 32);
-  const int64_t blocks = n_tok < 65535 * 4 ? n_tok : 65535 * 4;
-  kv_append_kernel<<<static_cast<unsigned>(blocks), threads, 0, static_cast<cudaStream_t>(stream)>>>(
+  auto kern = append_vec(k_new, v_new, k_cache, v_cache, row_bytes) ? kv_append_kernel<true>
+                                                                      : kv_append_kernel<false>;
+  kern<<<append_blocks(n_tok), 256, 0, static_cast<cudaStream_t>(stream)>>>(
       static_cast<const char*>(k_new), static_cast<const char*>(v_new), n_tok, nullptr, 0, nullptr, block_table,
       bt_stride, __builtin_ctz(page_size), static_cast<char*>(k_cache), static_cast<char*>(v_cache), row_bytes,
       pos0, seq_row);

@@ -50,6 +50,7 @@ struct pkv_pool {
   uint64_t bump_raw = 0;             // itertools.count value (may overshoot)
   std::vector<int64_t> refcount;     // grown on demand, logically [capacity]
   int64_t nonzero = 0;               // count_nonzero(refcount)
+  int64_t shared = 0;                // pages with refcount > 1 (0: no copy-on-write anywhere)
   std::unordered_map<int64_t, Table> tables;
   uint64_t next_order = 0;
 
@@ -70,6 +71,7 @@ struct pkv_pool {
     int64_t old = refcount[page];
     refcount[page] = v;
     nonzero += (v != 0) - (old != 0);
+    shared += (v > 1) - (old > 1);
   }
 
   // pool.py:130-136
@@ -196,6 +198,30 @@ void copy_out(const std::vector<uint32_t>& v, uint32_t* out, int64_t* n) {
                            static_cast<long long>(seq))
 
 }  // namespace
+
+// copy-on-write of one block of a table (pool.py:238-254), pool lock held
+static int privatize_locked(pkv_pool* pool, Table* t, int64_t block_idx, int64_t* old_page, int64_t* new_page) {
+  const int64_t n = static_cast<int64_t>(t->entries.size());
+  int64_t idx = block_idx < 0 ? block_idx + n : block_idx;
+  if (idx < 0 || idx >= n) return pkv::fail(PKV_INDEX_ERROR, "array index out of range");
+  uint32_t old = t->entries[idx];
+  if (old >= pool->capacity)
+    return pkv::fail(PKV_INDEX_ERROR, "index %u is out of bounds for refcounts", old);
+  if (old_page) *old_page = old;
+  if (pool->ref(old) <= 1) return PKV_OK;
+  std::vector<uint32_t> got;
+  if (!pool->take(1, &got))
+    return pkv::fail(PKV_CAPACITY_EXHAUSTED, "pool cannot supply 1 pages (%zu free, bump at %llu/%llu)",
+                     pool->free_stack.size(), static_cast<unsigned long long>(pool->bump_cursor()),
+                     static_cast<unsigned long long>(pool->capacity));
+  uint32_t fresh = got[0];
+  pool->set_ref(fresh, 1);
+  t->entries[idx] = fresh;
+  pool->mark(*t, idx);
+  if (new_page) *new_page = fresh;
+  int64_t dummy;
+  return pool->release(std::vector<uint32_t>{old}, &dummy);
+}
 
 extern "C" {
 
@@ -333,26 +359,7 @@ int pkv_pool_privatize(pkv_pool* pool, int64_t seq, int64_t block_idx, int64_t* 
   if (old_page) *old_page = -1;
   if (new_page) *new_page = -1;
   TABLE_OR_FAIL(t, pool, seq);
-  const int64_t n = static_cast<int64_t>(t->entries.size());
-  int64_t idx = block_idx < 0 ? block_idx + n : block_idx;
-  if (idx < 0 || idx >= n) return pkv::fail(PKV_INDEX_ERROR, "array index out of range");
-  uint32_t old = t->entries[idx];
-  if (old >= pool->capacity)
-    return pkv::fail(PKV_INDEX_ERROR, "index %u is out of bounds for refcounts", old);
-  if (old_page) *old_page = old;
-  if (pool->ref(old) <= 1) return PKV_OK;
-  std::vector<uint32_t> got;
-  if (!pool->take(1, &got))
-    return pkv::fail(PKV_CAPACITY_EXHAUSTED, "pool cannot supply 1 pages (%zu free, bump at %llu/%llu)",
-                     pool->free_stack.size(), static_cast<unsigned long long>(pool->bump_cursor()),
-                     static_cast<unsigned long long>(pool->capacity));
-  uint32_t fresh = got[0];
-  pool->set_ref(fresh, 1);
-  t->entries[idx] = fresh;
-  pool->mark(*t, idx);
-  if (new_page) *new_page = fresh;
-  int64_t dummy;
-  return pool->release(std::vector<uint32_t>{old}, &dummy);
+  return privatize_locked(pool, t, block_idx, old_page, new_page);
 }
 
 int pkv_pool_privatize_blocks(pkv_pool* pool, int64_t seq, const int64_t* blocks, int64_t n,
@@ -363,6 +370,69 @@ int pkv_pool_privatize_blocks(pkv_pool* pool, int64_t seq, const int64_t* blocks
     const int st = pkv_pool_privatize(pool, seq, blocks[i], &old, &fresh);
     if (st) return st;  // earlier blocks stay privatized, as with the reference's loop
     if (fresh >= 0) {
+      copies_out[2 * *n_copies_out] = old;
+      copies_out[2 * *n_copies_out + 1] = fresh;
+      ++*n_copies_out;
+    }
+  }
+  return PKV_OK;
+}
+
+int pkv_pool_assign_prepare(pkv_pool* pool, int64_t seq, const int64_t* positions, int64_t n,
+                            int64_t* info_out, int64_t* copies_out, int64_t copies_cap, int64_t* n_copies_out) {
+  if (n < 0 || (n > 0 && !positions) || !info_out || !n_copies_out)
+    return pkv::fail(PKV_VALUE_ERROR, "bad assign inputs");
+  *n_copies_out = 0;
+  // the common case first: a contiguous run p0, p0+1, ... (a prompt, a
+  // decode token) is one vectorised xor/or pass; anything else gets the
+  // min / max / non-increasing-step scan
+  const int64_t p0 = n ? positions[0] : 0;
+  uint64_t diff = 0;
+  for (int64_t i = 0; i < n; ++i) diff |= static_cast<uint64_t>(positions[i] ^ (p0 + i));
+  int64_t lo = p0, hi = n ? p0 + n - 1 : p0, steps_down = 0;
+  if (diff) {
+    hi = p0;
+    for (int64_t i = 1; i < n; ++i) {
+      const int64_t x = positions[i];
+      steps_down += x <= positions[i - 1];
+      lo = std::min(lo, x);
+      hi = std::max(hi, x);
+    }
+  }
+  const bool increasing = steps_down == 0;
+  LOCK(pool);
+  TABLE_OR_FAIL(t, pool, seq);
+  const int64_t ps = static_cast<int64_t>(pool->page_size);
+  const int64_t n_pages = static_cast<int64_t>(t->entries.size());
+  int64_t flags = 0;
+  if (increasing) flags |= PKV_ASSIGN_INCREASING;
+  if (increasing && hi - lo == n - 1) flags |= PKV_ASSIGN_CONTIGUOUS;
+  const bool in_range = n == 0 || (lo >= 0 && hi < n_pages * ps);
+  if (!in_range) flags |= PKV_ASSIGN_OUT_OF_RANGE;
+  info_out[0] = lo;
+  info_out[1] = hi;
+  info_out[2] = flags;
+  info_out[3] = n_pages;
+  info_out[4] = t->mirror_row;
+  // no page of the pool is shared: nothing to copy-on-write
+  if (!in_range || !increasing || n == 0 || pool->shared == 0) return PKV_OK;
+  // touched blocks, ascending and distinct (the positions increase): a
+  // contiguous run walks its block range, otherwise every position's block
+  // (a shift for the power-of-two page sizes: no per-position division)
+  const bool pow2 = (ps & (ps - 1)) == 0;
+  const int shift = pow2 ? __builtin_ctzll(static_cast<unsigned long long>(ps)) : 0;
+  const bool contiguous = (flags & PKV_ASSIGN_CONTIGUOUS) != 0;
+  const int64_t n_iter = contiguous ? (hi / ps - lo / ps + 1) : n;
+  int64_t prev = -1;
+  for (int64_t i = 0; i < n_iter; ++i) {
+    const int64_t b = contiguous ? lo / ps + i : (pow2 ? positions[i] >> shift : positions[i] / ps);
+    if (b == prev) continue;
+    prev = b;
+    int64_t old = -1, fresh = -1;
+    const int st = privatize_locked(pool, t, b, &old, &fresh);
+    if (st) return st;  // earlier blocks stay privatized, as with the reference's loop
+    if (fresh >= 0) {
+      if (2 * *n_copies_out + 2 > copies_cap) return pkv::fail(PKV_VALUE_ERROR, "copy buffer too small");
       copies_out[2 * *n_copies_out] = old;
       copies_out[2 * *n_copies_out + 1] = fresh;
       ++*n_copies_out;
