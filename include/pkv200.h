@@ -427,6 +427,19 @@ int64_t pkv_prefill_plan_ints(const int32_t* q_len, int64_t n_seqs, int32_t hq, 
 int pkv_prefill_plan(const int64_t* q_start, const int32_t* q_len, const int32_t* seq_len,
                      const int32_t* seq_row, int64_t n_seqs, int32_t hq, int32_t hkv,
                      int32_t causal, int32_t* plan_out, int64_t cap, int64_t* n_items_out);
+/* The K3 route of paged_attention in one host pass (attention.py:81-84,
+ * 98-110, 332-354): q_seq / q_pos (int64, q_seq non-decreasing), seq_len
+ * (int64) and seq_row per view sequence.  Suffix-shaped metadata (each
+ * sequence's queries one run of consecutive positions ending at its last
+ * key): *n_items_out >= 0, *max_run_out = longest run and, when build > 0 and
+ * the longest run is at least build positions, the memoised plan in plan_out
+ * (else *n_items_out = 0).  Otherwise *n_items_out = -1.
+ * *generation_out names the memoised plan: the same value on the same host
+ * thread means the same plan (a caller may reuse its device copy). */
+int pkv_prefill_plan_meta(const int64_t* q_seq, const int64_t* q_pos, int64_t n_q, const int64_t* seq_len,
+                          const int32_t* seq_row, int64_t n_seqs, int32_t hq, int32_t hkv, int32_t causal,
+                          int32_t build, int32_t* plan_out, int64_t cap, int64_t* n_items_out,
+                          int64_t* max_run_out, int64_t* generation_out);
 int pkv_paged_prefill(const pkv_prefill_args* args, void* stream);
 
 /* number of SMs of the current device (0 when no device is visible) */

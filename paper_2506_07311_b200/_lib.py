@@ -112,6 +112,8 @@ SIGNATURES = {
     "pkv_pool_free_stack": (C.c_int, [_vp, _P(_u32), _i64, _P(_i64)]),
     "pkv_pool_tables_info": (C.c_int, [_vp, _vp, _i64, _vp, _vp]),
     "pkv_pool_assign_prepare": (C.c_int, [_vp, _i64, _vp, _i64, _vp, _vp, _i64, _vp]),
+    "pkv_prefill_plan_meta": (C.c_int, [_vp, _vp, _i64, _vp, _vp, _i64, _i32, _i32, _i32, _i32, _vp, _i64,
+                                        _vp, _vp, _vp]),
     "pkv_pool_mirror_row": (C.c_int, [_vp, _i64, _P(_i32)]),
     "pkv_pool_mirror_shape": (C.c_int, [_vp, _P(_i64), _P(_i64)]),
     "pkv_pool_mirror_drain": (C.c_int, [_vp, _P(_i32), _i64, _P(_i64), _P(_i32)]),

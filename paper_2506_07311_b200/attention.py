@@ -22,6 +22,7 @@ from __future__ import annotations
 
 import ctypes as C
 import math
+import threading
 from dataclasses import dataclass, field
 from enum import IntEnum
 
@@ -311,35 +312,108 @@ def suffix_runs(meta: MaskMeta):
     return q_start, q_len
 
 
-def _prefill_route(meta, config, kv_code, precision):
-    """Query runs for K3, or None to use K2.  "auto" sends bf16 caches with
-    runs of >= PREFILL_MIN_RUN positions (fp16 stays on the fp32 CUDA-core
-    kernel and its 1e-5 contract, like the decode dispatch); "tensor" also
-    takes fp16; "prefill" forces K3 for any suffix-shaped meta."""
+@dataclass
+class _PrefillRoute:
+    """The K3 route of one call: the memoised plan (host view), its size and
+    the generation naming it (pkv_prefill_plan_meta)."""
+
+    plan: np.ndarray
+    n_items: int
+    generation: int
+
+
+_plan_tls = threading.local()
+
+
+def _prefill_plan_meta(meta: MaskMeta, config: AttentionConfig, rows, min_run: int):
+    """(n_items, longest run, plan view, generation): -1 items when the meta
+    is not suffix-shaped; 0 items when no run reaches `min_run`.  One native
+    pass (suffix check, run lengths, memoised planner)."""
+    view = meta.view
+    n_seq, nq = len(view.lengths), meta.query_count
+    qt = 128 // (config.head_count // config.kv_head_count)
+    cap = config.kv_head_count * (nq // (2 * qt) + n_seq + 1) * _lib.PREFILL_ITEM_INTS
+    buf = getattr(_plan_tls, "buf", None)
+    if buf is None or buf.size < cap:
+        buf = _plan_tls.buf = np.empty(max(cap, 1 << 14), dtype=np.int32)
+        _plan_tls.out = np.zeros(3, dtype=np.int64)
+    out = _plan_tls.out
+    q_seq = np.ascontiguousarray(meta.q_seq, dtype=np.int64)
+    q_pos = np.ascontiguousarray(meta.q_pos, dtype=np.int64)
+    lens = np.ascontiguousarray(view.lengths, dtype=np.int64)
+    rows = np.ascontiguousarray(rows, dtype=np.int32)
+    base = out.ctypes.data
+    _lib.check(_lib.load().pkv_prefill_plan_meta(
+        q_seq.ctypes.data, q_pos.ctypes.data, nq, lens.ctypes.data, rows.ctypes.data, n_seq,
+        config.head_count, config.kv_head_count, int(bool(config.causal)), min_run, buf.ctypes.data, buf.size,
+        base, base + 8, base + 16), "pkv_prefill_plan_meta")
+    n_items, max_run, gen = (int(x) for x in out)
+    return n_items, max_run, buf[: max(n_items, 0) * _lib.PREFILL_ITEM_INTS], gen
+
+
+def _prefill_route(meta, config, kv_code, precision, rows):
+    """The K3 plan, or None to use K2.  "auto" sends bf16 caches with
+    query runs of >= PREFILL_MIN_RUN positions (fp16 stays on the fp32
+    CUDA-core kernel and its 1e-5 contract, like the decode dispatch);
+    "tensor" also takes fp16; "prefill" forces K3 for any suffix-shaped meta
+    (attention.py:81-84, 98-110).  `rows`: mirror row (paged) or first K/V
+    row (gathered) per view sequence."""
     if precision == "exact":
         return None
-    supported = kv_code in (_lib.PKV_BF16, _lib.PKV_F16) and _lib.load().pkv_prefill_supported(
-        config.head_count, config.kv_head_count, config.head_dim, config.page_size, kv_code)
-    runs = suffix_runs(meta) if supported else None
-    if precision == "prefill":
-        if runs is None:
+    if precision == "auto" and kv_code != _lib.PKV_BF16 or kv_code not in (_lib.PKV_BF16, _lib.PKV_F16):
+        return None
+    supported = _lib.load().pkv_prefill_supported(config.head_count, config.kv_head_count, config.head_dim,
+                                                  config.page_size, kv_code)
+    if not supported:
+        if precision == "prefill":
             raise ConfigError("the tcgen05 prefill needs a suffix-shaped meta over a 16-bit cache with "
                               "head_dim 64/128, page_size >= 8 and 128 % (hq/hkv) == 0")
-        return runs
-    if runs is None or (precision == "auto" and kv_code != _lib.PKV_BF16):
         return None
-    return runs if runs[1].max(initial=0) >= PREFILL_MIN_RUN else None
+    rows = np.asarray(rows)
+    if rows.size and rows.max() >= 2 ** 31:
+        raise OutOfRange("K/V rows beyond 2^31 are not addressable")
+    min_run = 1 if precision == "prefill" else PREFILL_MIN_RUN
+    n_items, max_run, plan, gen = _prefill_plan_meta(meta, config, rows, min_run)
+    if n_items < 0:
+        if precision == "prefill":
+            raise ConfigError("the tcgen05 prefill needs a suffix-shaped meta over a 16-bit cache with "
+                              "head_dim 64/128, page_size >= 8 and 128 % (hq/hkv) == 0")
+        return None
+    if max_run < min_run or meta.query_count == 0:
+        return None if precision != "prefill" else _PrefillRoute(plan, 0, gen)
+    return _PrefillRoute(plan.reshape(-1, _lib.PREFILL_ITEM_INTS), n_items, gen)
+
+
+# device copy of the last K3 plan per (host thread, device, stream): a call
+# whose memoised plan has the same generation reuses it (layers of a model)
+_prefill_dev_plans: dict = {}
+
+
+def _device_plan(route: _PrefillRoute, device):
+    import torch
+
+    key = (threading.get_ident(), device, torch.cuda.current_stream(device).cuda_stream)
+    ent = _prefill_dev_plans.get(key)
+    size = route.n_items * _lib.PREFILL_ITEM_INTS
+    if ent is not None and ent[0] == route.generation and ent[2] == size:
+        return ent[1]
+    staged = stage_upload(device, route.plan.reshape(-1))
+    dev = ent[1] if ent is not None and ent[1].numel() >= size else torch.empty(
+        max(size, 1 << 12), dtype=torch.int32, device=device)
+    dev[:size].copy_(staged)  # stream-ordered behind any kernel still reading the old plan
+    _prefill_dev_plans[key] = (route.generation, dev, size)
+    return dev
 
 
 @on_device(lambda *a, **k: k.get("device"))
-def _launch_prefill(q, meta, config, runs, *, k, v, kv_code, bt, rows, out_dtype, device, prof=None):
+def _launch_prefill(q, meta, config, runs, *, k, v, kv_code, bt, rows, out_dtype, device, prof=None,
+                    route: _PrefillRoute | None = None):
     """K3: one tcgen05 launch over every sequence's query run.  Paged mode:
     `bt` is the device block-table mirror and `rows` the mirror row of each
     view sequence; gathered mode (bt None): `rows` is each sequence's first
     row in the contiguous K/V."""
     import torch
 
-    q_start, q_len = runs
     nq = meta.query_count
     out_t, out_code = torch_dtype(out_dtype)
     if out_code not in (_lib.PKV_F32, kv_code):
@@ -348,12 +422,16 @@ def _launch_prefill(q, meta, config, runs, *, k, v, kv_code, bt, rows, out_dtype
     if nq == 0:
         return out
     q = q.to(k.dtype).contiguous()
-    rows = np.asarray(rows, dtype=np.int64)
-    if rows.size and rows.max() >= 2 ** 31:
-        raise OutOfRange("K/V rows beyond 2^31 are not addressable")
-    plan = _lib.prefill_plan(q_start, q_len, meta.view.lengths, rows, config.head_count,
-                             config.kv_head_count, config.causal)
-    dev_plan = stage_upload(device, plan.reshape(-1))
+    if route is not None:
+        plan, dev_plan = route.plan, _device_plan(route, device)
+    else:  # explicit runs (tools): plan and upload here
+        rows = np.asarray(rows, dtype=np.int64)
+        if rows.size and rows.max() >= 2 ** 31:
+            raise OutOfRange("K/V rows beyond 2^31 are not addressable")
+        q_start, q_len = runs
+        plan = _lib.prefill_plan(q_start, q_len, meta.view.lengths, rows, config.head_count,
+                                 config.kv_head_count, config.causal)
+        dev_plan = stage_upload(device, plan.reshape(-1))
     args = _lib.PrefillArgs(
         q=q.data_ptr(), total_q=nq, k_cache=k.data_ptr(), v_cache=v.data_ptr(),
         kv_dtype=kv_code, cache_rows=k.shape[0], block_table=bt.data_ptr() if bt is not None else None,
@@ -394,20 +472,23 @@ def paged_attention(queries, store: KvStore, meta: MaskMeta, config: AttentionCo
     if bad.size:
         i = int(bad[0])
         raise OutOfRange(f"length {int(lengths[i])} exceeds reserved capacity of sequence {view.ids[i]!r}")
-    nkeys = allowed_key_counts(meta, config.causal)
-    if meta.query_count and (nkeys <= 0).any():
-        bad = np.nonzero(nkeys <= 0)[0].tolist()
-        raise NoAllowedKeys(f"queries {bad} have zero allowed keys")
-    if stats is not None:
-        _fill_stats(stats, meta, config, nkeys, block_mask)
+    # a suffix-shaped meta (the K3 route) always has >= 1 allowed key per query
+    route = _prefill_route(meta, config, store.dtype_code, precision, seq_row)
+    nkeys = None
+    if route is None or stats is not None:
+        nkeys = allowed_key_counts(meta, config.causal)
+        if meta.query_count and (nkeys <= 0).any():
+            bad = np.nonzero(nkeys <= 0)[0].tolist()
+            raise NoAllowedKeys(f"queries {bad} have zero allowed keys")
+        if stats is not None:
+            _fill_stats(stats, meta, config, nkeys, block_mask)
     device = store.device
     q, qcode = _q_tensor(queries, device)
-    runs = _prefill_route(meta, config, store.dtype_code, precision)
     mirror = store.pool.device_table(device)
-    if runs is not None:
-        return _launch_prefill(q, meta, config, runs, k=store.k_cache, v=store.v_cache,
+    if route is not None:
+        return _launch_prefill(q, meta, config, None, k=store.k_cache, v=store.v_cache,
                                kv_code=store.dtype_code, bt=mirror, rows=seq_row,
-                               out_dtype=out_dtype or torch.float32, device=device)
+                               out_dtype=out_dtype or torch.float32, device=device, route=route)
     return _launch_attention(q, qcode, meta, config, nkeys, k=store.k_cache, v=store.v_cache,
                              kv_code=store.dtype_code, bt=mirror, bt_stride=mirror.shape[1],
                              seq_row=seq_row, seq_start=None,
@@ -441,10 +522,11 @@ def gathered_attention(queries, keys, values, meta: MaskMeta, config: AttentionC
     _, kv_code = torch_dtype(k.dtype)
     q, qcode = _q_tensor(queries, device)
     seq_start = meta.view.prefix_sums.astype(np.int64)
-    runs = _prefill_route(meta, config, kv_code, precision)
-    if runs is not None:
-        return _launch_prefill(q, meta, config, runs, k=k, v=v, kv_code=kv_code, bt=None,
-                               rows=seq_start, out_dtype=out_dtype or torch.float32, device=device)
+    route = _prefill_route(meta, config, kv_code, precision, seq_start)
+    if route is not None:
+        return _launch_prefill(q, meta, config, None, k=k, v=v, kv_code=kv_code, bt=None,
+                               rows=seq_start, out_dtype=out_dtype or torch.float32, device=device,
+                               route=route)
     return _launch_attention(q, qcode, meta, config, nkeys, k=k, v=v, kv_code=kv_code, bt=None,
                              bt_stride=0, seq_row=None, seq_start=seq_start,
                              out_dtype=out_dtype or torch.float32, device=device,

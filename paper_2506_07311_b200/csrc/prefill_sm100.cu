@@ -706,6 +706,7 @@ struct PrefillMemo {
   std::vector<int64_t> key;
   std::vector<int32_t> plan;
   int64_t n_items = -1;
+  int64_t generation = 0;  // bumped whenever the memo is rebuilt
 };
 thread_local PrefillMemo t_prefill_memo;
 }  // namespace
@@ -742,7 +743,52 @@ extern "C" int pkv_prefill_plan(const int64_t* q_start, const int32_t* q_len, co
   m.key.swap(key);
   m.n_items = *n_items_out;
   m.plan.assign(plan_out, plan_out + m.n_items * kItemInts);
+  ++m.generation;
   return PKV_OK;
+}
+
+// The K3 route of paged_attention / gathered_attention in one host pass:
+// decide whether the query metadata is suffix-shaped (attention.py:81-84,
+// 98-110: per view sequence one run of consecutive positions ending at its
+// last key), report the longest run, and build (memoised) the plan.  q_seq is
+// non-decreasing (MaskMeta checks it).  Not suffix-shaped: *n_items_out = -1.
+// *generation_out identifies the memoised plan: equal generations on one host
+// thread mean an identical plan (a caller may keep its device copy).
+extern "C" int pkv_prefill_plan_meta(const int64_t* q_seq, const int64_t* q_pos, int64_t n_q,
+                                     const int64_t* seq_len, const int32_t* seq_row, int64_t n_seqs, int32_t hq,
+                                     int32_t hkv, int32_t causal, int32_t build, int32_t* plan_out, int64_t cap,
+                                     int64_t* n_items_out, int64_t* max_run_out, int64_t* generation_out) {
+  if (n_q < 0 || n_seqs < 0 || (n_q > 0 && (!q_seq || !q_pos)) || (n_seqs > 0 && (!seq_len || !seq_row)))
+    return fail(PKV_VALUE_ERROR, "bad prefill metadata");
+  *n_items_out = -1;
+  *max_run_out = 0;
+  // runs by binary search on the non-decreasing q_seq, then one vectorisable
+  // pass per run checking q_seq[i] == s and q_pos[i] == len - q_len + (i - q_start)
+  // (an unsorted or out-of-range q_seq fails the check: not suffix-shaped)
+  std::vector<int64_t> q_start(static_cast<size_t>(n_seqs) + 1, 0);
+  std::vector<int32_t> q_len(static_cast<size_t>(n_seqs), 0), sl(static_cast<size_t>(n_seqs));
+  for (int64_t s = 0; s <= n_seqs; ++s) q_start[s] = std::lower_bound(q_seq, q_seq + n_q, s) - q_seq;
+  if (q_start[n_seqs] != n_q) return PKV_OK;
+  int64_t max_run = 0;
+  uint64_t diff = static_cast<uint64_t>(q_start[0]);  // queries before sequence 0: negative q_seq
+  for (int64_t s = 0; s < n_seqs; ++s) {
+    if (seq_len[s] < 0 || seq_len[s] > 0x7fffffff) return fail(PKV_OUT_OF_RANGE, "sequence length beyond int32");
+    sl[s] = static_cast<int32_t>(seq_len[s]);
+    const int64_t a = q_start[s], len_q = q_start[s + 1] - a;
+    q_len[s] = static_cast<int32_t>(len_q);
+    max_run = std::max<int64_t>(max_run, len_q);
+    const int64_t base = seq_len[s] - len_q - a;
+    for (int64_t i = a; i < a + len_q; ++i)
+      diff |= static_cast<uint64_t>(q_pos[i] ^ (base + i)) | static_cast<uint64_t>(q_seq[i] ^ s);
+  }
+  if (diff) return PKV_OK;
+  *max_run_out = max_run;
+  *n_items_out = 0;
+  if (build <= 0 || max_run < build) return PKV_OK;
+  const int st = pkv_prefill_plan(q_start.data(), q_len.data(), sl.data(), seq_row, n_seqs, hq, hkv, causal,
+                                  plan_out, cap, n_items_out);
+  if (generation_out) *generation_out = t_prefill_memo.generation;
+  return st;
 }
 
 namespace pkv {

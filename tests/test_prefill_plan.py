@@ -97,3 +97,41 @@ def test_prefill_plan_fuzz_covers_every_query_once():
                     keys = min(pos0 + t * qt + cnt, kv_len) if causal else kv_len
                     assert tiles == -(-keys // 128)
         assert (cover == 1).all()
+
+
+def _metas():
+    view = BatchView.from_lengths([5, 0, 3, 40], ids=["a", "b", "c", "d"])
+    yield MaskMeta.self_attention(view)
+    yield MaskMeta.suffix(view, [2, 0, 3, 17])
+    yield MaskMeta.decode(BatchView.from_lengths([4, 9]))
+    yield MaskMeta(BatchView.from_lengths([5, 3]), q_seq=[0, 0], q_pos=[1, 2])  # not ending at len-1
+    yield MaskMeta(BatchView.from_lengths([5, 3]), q_seq=[0, 0], q_pos=[4, 4])  # repeated position
+    yield MaskMeta(BatchView.from_lengths([5, 3]), q_seq=np.zeros(0, np.int64), q_pos=np.zeros(0, np.int64))
+
+
+@pytest.mark.parametrize("causal", [True, False])
+def test_native_route_matches_suffix_runs_and_planner(causal):
+    """pkv_prefill_plan_meta (the one-pass K3 route) == suffix_runs + the planner."""
+    from paper_2506_07311_b200 import AttentionConfig
+    from paper_2506_07311_b200.attention import _prefill_plan_meta
+
+    cfg = AttentionConfig(head_count=8, head_dim=64, page_size=16, kv_head_count=2, causal=causal)
+    for meta in _metas():
+        rows = np.arange(len(meta.view.lengths), dtype=np.int32) * 3
+        n_items, max_run, plan, gen = _prefill_plan_meta(meta, cfg, rows, 1)
+        runs = suffix_runs(meta)
+        if runs is None:
+            assert n_items == -1
+            continue
+        assert max_run == int(runs[1].max(initial=0))
+        if max_run == 0:
+            assert n_items == 0
+            continue
+        want = _lib.prefill_plan(runs[0], runs[1], meta.view.lengths, rows, 8, 2, causal)
+        assert np.array_equal(plan.reshape(-1, _lib.PREFILL_ITEM_INTS), want)
+        # the same metadata again: memo hit, same generation, same plan
+        n2, _, plan2, gen2 = _prefill_plan_meta(meta, cfg, rows, 1)
+        assert gen2 == gen and n2 == n_items and np.array_equal(plan2, plan)
+        # below the build threshold: route known, nothing planned
+        n3, m3, _, _ = _prefill_plan_meta(meta, cfg, rows, max_run + 1)
+        assert n3 == 0 and m3 == max_run

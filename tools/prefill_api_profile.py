@@ -42,8 +42,6 @@ pstats.Stats(pr).sort_stats("tottime").print_stats(15)
 
 # piecewise host timing of one isolated call's steps
 from paper_2506_07311_b200 import attention as A  # noqa: E402
-from paper_2506_07311_b200 import _lib  # noqa: E402
-from paper_2506_07311_b200.store import stage_upload  # noqa: E402
 
 
 def t(fn, reps=20):
@@ -57,22 +55,19 @@ def t(fn, reps=20):
 
 
 view = meta.view
-runs = A.suffix_runs(meta)
 rows = np.asarray([pool.table(0).mirror_row], dtype=np.int32)
-plan = _lib.prefill_plan(runs[0], runs[1], view.lengths, rows, hq, hkv, True)
+route = A._prefill_route(meta, cfg, store.dtype_code, "auto", rows)
 print({
     "check_queries": t(lambda: A._check_queries(q, meta, cfg)),
     "tables_info": t(lambda: pool.tables_info(view.ids)),
-    "allowed_key_counts": t(lambda: A.allowed_key_counts(meta, cfg.causal)),
     "q_tensor": t(lambda: A._q_tensor(q, dev)),
-    "prefill_route": t(lambda: A._prefill_route(meta, cfg, store.dtype_code, "auto")),
+    "prefill_route (native scan + memoised plan)": t(lambda: A._prefill_route(meta, cfg, store.dtype_code, "auto",
+                                                                              rows)),
     "device_table": t(lambda: pool.device_table(dev)),
-    "out_empty": t(lambda: torch.empty((n, hq, d), dtype=torch.float32, device=dev)),
-    "q_to": t(lambda: q.to(store.k_cache.dtype).contiguous()),
-    "prefill_plan": t(lambda: _lib.prefill_plan(runs[0], runs[1], view.lengths, rows, hq, hkv, True)),
-    "stage_upload": t(lambda: stage_upload(dev, plan.reshape(-1))),
-    "launch_prefill_total": t(lambda: A._launch_prefill(q, meta, cfg, runs, k=store.k_cache, v=store.v_cache,
+    "device_plan (generation hit)": t(lambda: A._device_plan(route, dev)),
+    "launch_prefill_total": t(lambda: A._launch_prefill(q, meta, cfg, None, k=store.k_cache, v=store.v_cache,
                                                         kv_code=store.dtype_code, bt=pool.device_table(dev),
-                                                        rows=rows, out_dtype=torch.float32, device=dev)),
+                                                        rows=rows, out_dtype=torch.float32, device=dev,
+                                                        route=route)),
     "paged_attention_total": t(lambda: paged_attention(q, store, meta, cfg)),
 })
