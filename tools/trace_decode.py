@@ -125,3 +125,20 @@ if os.environ.get("CORR"):
     for e, c, n, p, k in recs:
         by_cuts[k].append(e)
     print("end time by cut pieces:", {n: round(float(np.mean(v)), 1) for n, v in sorted(by_cuts.items())})
+    # epilogue (chunks done -> stored) and streaming time per item, cut vs whole
+    ep = {"whole": [], "cut": []}
+    st_rate = {"whole": [], "cut": []}
+    for c in range(min(148, P["grid"])):
+        its = items[cta[c]:cta[c + 1]]
+        for k, r in enumerate(its[:7]):
+            kind = "cut" if r[4] >= 0 else "whole"
+            for w in range(8):
+                s_, f_, d_, st_ = rel[c, w, 2 + 4 * k: 6 + 4 * k]
+                if not np.isnan(d_) and not np.isnan(st_):
+                    ep[kind].append(st_ - d_)
+                if not np.isnan(f_) and not np.isnan(d_) and r[3] > r[2]:
+                    st_rate[kind].append((d_ - f_) / (r[3] - r[2]))
+    for kind in ep:
+        if ep[kind]:
+            print("%-5s items: epilogue us p50 %.2f mean %.2f | stream us/page p50 %.3f" % (
+                kind, np.median(ep[kind]), np.mean(ep[kind]), np.median(st_rate[kind]) if st_rate[kind] else -1))
