@@ -819,7 +819,7 @@ def prefill_c4(device, n=8192):
     the fraction is of the measured bf16 BURST peak (an isolated kernel)."""
     import torch
 
-    from paper_2506_07311_b200 import AttentionConfig, KvStore, MaskMeta, PagePool, paged_attention
+    from paper_2506_07311_b200 import AttentionConfig, KvStore, MaskMeta, PagePool, _lib, paged_attention
     from paper_2506_07311_b200.attention import _launch_prefill, suffix_runs
 
     hq, hkv, d, ps = 32, 8, 128, 16
@@ -863,6 +863,21 @@ def prefill_c4(device, n=8192):
         app.append(e0.elapsed_time(e1))
         times.append(e1.elapsed_time(e2))
         kern.append(ev[0].elapsed_time(ev[1]))
+    # K1 alone (the append kernel's roofline): CUDA events around the native
+    # range launch only, K and V rows read + written
+    from paper_2506_07311_b200.store import _stream as _raw_stream
+    lib = _lib.load()
+    k1 = []
+    row0 = int(pool.table(0).mirror_row)
+    for _ in range(10):
+        ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        ev0.record()
+        _lib.check(lib.pkv_kv_append_range(k.data_ptr(), v.data_ptr(), n, row0, 0, mirror.data_ptr(),
+                                           mirror.shape[1], ps, store.k_cache.data_ptr(), store.v_cache.data_ptr(),
+                                           store.row_bytes, _raw_stream(device)), "pkv_kv_append_range")
+        ev1.record()
+        torch.cuda.synchronize(device)
+        k1.append(ev0.elapsed_time(ev1))
     # the same call issued back to back (a model's layers): host planning of
     # call i+1 overlaps kernel i
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -884,12 +899,25 @@ def prefill_c4(device, n=8192):
     except Exception:
         burst, sustained = 1590.0, 1400.0
     append_bytes = 2 * 2 * n * hkv * d * 2  # K and V read + written
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            hbm_peak = float(json.load(f)["hbm_gbs"])
+    except Exception:
+        hbm_peak = 6650.0
     return {"workload": f"C4 causal prefill, 1 x {n} tokens, GQA 32q/8kv x128 bf16, page 16",
             "kernel": "prefill_tc_kernel (K3, tcgen05/TMEM)", "kernel_ms": kms, "tflops": round(tf, 1),
             "frac_of_burst_bf16": round(tf / burst, 3), "frac_of_sustained_bf16": round(tf / sustained, 3),
             "api_ms": ms, "api_tflops": round(flops / (ms * 1e-3) / 1e12, 1),
             "api_pipelined_ms": pipelined_ms, "append_ms": min(app),
             "append_gbs": round(append_bytes / (min(app) * 1e-3) / 1e9, 1),
+            "k1_roofline": {"kernel": "kv_append_kernel (K1, contiguous run)", "bound": "hbm",
+                            "kernel_ms": sorted(k1)[len(k1) // 2],
+                            "algorithmic_bytes": append_bytes,
+                            "achieved": round(append_bytes / (sorted(k1)[len(k1) // 2] * 1e-3) / 1e9, 1),
+                            "peak": hbm_peak, "unit": "GB/s",
+                            "frac": round(append_bytes / (sorted(k1)[len(k1) // 2] * 1e-3) / 1e9 / hbm_peak, 3),
+                            "note": "CUDA events around the pkv_kv_append_range launch alone (host launch "
+                                    "cost inside the events); bytes = K and V rows read + written"},
             "note": "kernel_ms: CUDA events around the K3 launch; api_ms: one paged_attention() call on an idle "
                     "GPU (host planning + metadata upload + launch + kernel); api_pipelined_ms: the call issued "
                     "10x back to back (host work of a call hidden behind the previous kernel); append: "
