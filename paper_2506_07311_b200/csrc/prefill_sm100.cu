@@ -264,7 +264,8 @@ __device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t* v) {
 template <typename T, int D>
 __global__ void __launch_bounds__(kThreads, 1)
     prefill_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
-                      const __grid_constant__ CUtensorMap tm_v, const __grid_constant__ PrefillParams p) {
+                      const __grid_constant__ CUtensorMap tm_v, const __grid_constant__ CUtensorMap tm_k128,
+                      const __grid_constant__ CUtensorMap tm_v128, const __grid_constant__ PrefillParams p) {
   constexpr int NCH = D / 64;                 // 64-column chunks of the head dim
   constexpr int kQBytes = NCH * kChunkB;      // one Q tile
   constexpr int kKVBytes = NCH * kChunkB;     // one K (or V) tile of 128 keys
@@ -327,6 +328,10 @@ __global__ void __launch_bounds__(kThreads, 1)
       // ---------------- TMA producer ----------------
       asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<uint64_t>(&tm_k)) : "memory");
       asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<uint64_t>(&tm_v)) : "memory");
+      if (p.bt && p.box_rows < kN) {
+        asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<uint64_t>(&tm_k128)) : "memory");
+        asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<uint64_t>(&tm_v128)) : "memory");
+      }
       const int ntiles_q = cnt[1] > 0 ? 2 : 1;
       mbar_expect_tx(bar(B_Q), kQBytes * ntiles_q);
       for (int t = 0; t < ntiles_q; ++t)
@@ -339,26 +344,33 @@ __global__ void __launch_bounds__(kThreads, 1)
       for (int j = 0; j < n_tiles; ++j) {
         const int st = j & 1;
         int rows[16];
+        bool run = p.bt != nullptr && boxes > 1;  // the tile's pages are one physically contiguous run
         for (int b = 0; b < boxes; ++b) {
           const int key0 = j * kN + b * p.box_rows;
           if (p.bt) {
             const int pg = key0 >> p.log2ps;
             rows[b] = pg < n_pages ? tbl[pg] * ps + (key0 & (ps - 1)) : p.oob_row;
+            run = run && pg < n_pages && rows[b] == rows[0] + b * p.box_rows;
           } else {
             rows[b] = mrow + key0;  // gathered: contiguous rows (past the end: zero fill)
           }
         }
+        // a run of consecutive pages (a fresh pool hands them out in order)
+        // is one 128-row box per chunk instead of one box per page
+        const CUtensorMap* mk = run ? &tm_k128 : &tm_k;
+        const CUtensorMap* mv = run ? &tm_v128 : &tm_v;
+        const int nb = run ? 1 : boxes;
         if (j >= 2) mbar_wait(bar(B_KE + st), ((j >> 1) - 1) & 1);
         mbar_expect_tx(bar(B_KF + st), kKVBytes);
-        for (int b = 0; b < boxes; ++b)
+        for (int b = 0; b < nb; ++b)
           for (int c = 0; c < NCH; ++c)
-            tma_load_3d(sK + st * kKVBytes + c * kChunkB + b * p.box_rows * kRowB, &tm_k, bar(B_KF + st),
+            tma_load_3d(sK + st * kKVBytes + c * kChunkB + b * p.box_rows * kRowB, mk, bar(B_KF + st),
                         c * 64, kvh, rows[b]);
         if (j >= 2) mbar_wait(bar(B_VE + st), ((j >> 1) - 1) & 1);
         mbar_expect_tx(bar(B_VF + st), kKVBytes);
-        for (int b = 0; b < boxes; ++b)
+        for (int b = 0; b < nb; ++b)
           for (int c = 0; c < NCH; ++c)
-            tma_load_3d(sV + st * kKVBytes + c * kChunkB + b * p.box_rows * kRowB, &tm_v, bar(B_VF + st),
+            tma_load_3d(sV + st * kKVBytes + c * kChunkB + b * p.box_rows * kRowB, mv, bar(B_VF + st),
                         c * 64, kvh, rows[b]);
       }
     }
@@ -643,7 +655,7 @@ size_t smem_bytes() {
 
 template <typename T, int D>
 int launch(const pkv_prefill_args* a, const PrefillParams& pp, cudaStream_t stream) {
-  CUtensorMap mq, mk, mv;
+  CUtensorMap mq, mk, mv, mk128, mv128;
   const int G = a->hq / a->hkv;
   int st = make_map(&mq, a->q, a->kv_dtype, D, a->hq, a->total_q, G, kM / G);
   if (st) return st;
@@ -652,6 +664,15 @@ int launch(const pkv_prefill_args* a, const PrefillParams& pp, cudaStream_t stre
   if (st) return st;
   st = make_map(&mv, a->v_cache, a->kv_dtype, D, a->hkv, a->cache_rows, 1, box_rows);
   if (st) return st;
+  // 128-row boxes for tiles whose pages form one contiguous run
+  mk128 = mk;
+  mv128 = mv;
+  if (box_rows < static_cast<uint32_t>(kN)) {
+    st = make_map(&mk128, a->k_cache, a->kv_dtype, D, a->hkv, a->cache_rows, 1, kN);
+    if (st) return st;
+    st = make_map(&mv128, a->v_cache, a->kv_dtype, D, a->hkv, a->cache_rows, 1, kN);
+    if (st) return st;
+  }
   const size_t smem = smem_bytes<T, D>();
   auto kern = prefill_tc_kernel<T, D>;
   static bool attr_set = false;
@@ -659,7 +680,7 @@ int launch(const pkv_prefill_args* a, const PrefillParams& pp, cudaStream_t stre
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
     attr_set = true;
   }
-  kern<<<static_cast<unsigned>(a->n_items), kThreads, smem, stream>>>(mq, mk, mv, pp);
+  kern<<<static_cast<unsigned>(a->n_items), kThreads, smem, stream>>>(mq, mk, mv, mk128, mv128, pp);
   PKV_CHECK_LAUNCH();
   return PKV_OK;
 }

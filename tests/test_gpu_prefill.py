@@ -199,3 +199,58 @@ def test_random_prefill_shapes_stress(seed):
     assert torch.isfinite(out).all()
     ref = dense_prefill_f64(q, ks, vs, lengths, q_lens, g, cfg.scale, causal=causal)
     assert relative_error(as_numpy(out), ref.cpu().numpy()) <= 6e-3, seed
+
+
+@pytest.mark.parametrize("ps", [8, 16, 32])
+def test_fragmented_and_contiguous_page_runs_in_one_prefill(ps):
+    """K3 fetches a 128-key tile whose pages form one physically contiguous
+    run with one 128-row TMA box per chunk, other tiles page by page.  Build
+    sequences whose first pages are interleaved with other allocations
+    (fragmented tiles) and whose later pages are contiguous (run tiles), plus
+    a fully permuted one: paged == gathered bitwise, and float64 parity."""
+    rng = np.random.default_rng(ps)
+    lengths = [1000, 777, 300]
+    hq, hkv, d = 32, 8, 128
+    total = sum(-(-n // ps) for n in lengths)
+    pool = PagePool(3 * total + 64, page_size=ps)
+    store = KvStore(pool, hkv, d, dtype=torch.bfloat16)
+    pads = []
+    for i, n in enumerate(lengths):
+        pool.reserve(i, 0)
+    # sequences 0 and 1: the first half of their pages interleaved with pads
+    for t in range(-(-max(lengths[:2]) // ps) // 2):
+        for i in (0, 1):
+            pool.grow(i, min(lengths[i], (t + 1) * ps))
+            pads.append(("pad", i, t))
+            pool.reserve(pads[-1], ps)
+    for i in (0, 1):
+        pool.grow(i, lengths[i])  # the rest contiguous
+    # sequence 2: pages drawn from a shuffled free list
+    junk = [("junk", j) for j in range(-(-lengths[2] // ps) + 4)]
+    for j in junk:
+        pool.reserve(j, ps)
+    for j in rng.permutation(len(junk)):
+        pool.free(junk[j])
+    pool.grow(2, lengths[2])
+    for pd in pads:
+        pool.free(pd)
+    entries = [np.asarray(pool.table(i).entries) for i in range(3)]
+    assert any((np.diff(e) != 1).any() for e in entries)  # some tiles are fragmented
+    gen = torch.Generator(device="cuda").manual_seed(ps)
+    ks, vs = [], []
+    for i, n in enumerate(lengths):
+        pool.table(i).logical_len = 0
+        k = torch.randn((n, hkv, d), generator=gen, device="cuda").bfloat16()
+        v = torch.randn((n, hkv, d), generator=gen, device="cuda").bfloat16()
+        store.assign(i, np.arange(n), k, v)
+        ks.append(k)
+        vs.append(v)
+    cfg = AttentionConfig(head_count=hq, head_dim=d, page_size=ps, kv_head_count=hkv)
+    view = store.batch_view([0, 1, 2])
+    meta = MaskMeta.self_attention(view)
+    q = torch.randn((meta.query_count, hq, d), generator=gen, device="cuda").bfloat16()
+    paged = paged_attention(q, store, meta, cfg, precision="prefill")
+    gk, gv = store.gather_view(view)
+    assert torch.equal(paged, gathered_attention(q, gk, gv, meta, cfg, precision="prefill"))
+    ref = dense_prefill_f64(q, ks, vs, lengths, lengths, hq // hkv, cfg.scale)
+    assert relative_error(as_numpy(paged), ref.cpu().numpy()) <= 6e-3
