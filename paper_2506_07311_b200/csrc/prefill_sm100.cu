@@ -61,6 +61,11 @@ constexpr int kChunkB = kM * kRowB;  // one 64-column chunk of a 128-row tile: 1
 constexpr int kItemInts = 10;
 constexpr float kLog2eP = 1.4426950408889634f;
 constexpr float kRescaleThreshold = 8.0f;  // log2 units
+#ifndef PKV_K3_PPARTS
+#define PKV_K3_PPARTS 2
+#endif
+constexpr int kPParts = PKV_K3_PPARTS;  // P published in 1, 2 or 4 parts (of 128 / kPParts keys)
+static_assert(kPParts == 1 || kPParts == 2 || kPParts == 4, "P parts");
 
 // ---- PTX wrappers -----------------------------------------------------------
 __device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
@@ -279,7 +284,9 @@ __global__ void __launch_bounds__(kThreads, 1)
   const uint32_t sK = sQ + 2 * kQBytes;               // 2 stages
   const uint32_t sV = sK + 2 * kKVBytes;              // 2 stages
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + 2 * kQBytes + 4 * kKVBytes);
-  enum { B_Q = 0, B_KF = 1, B_VF = 3, B_KE = 5, B_VE = 7, B_SF = 9, B_PF = 11, B_OD = 13, B_N = 15 };
+  // PF + 2*part + t: part `part` (kN / kPParts keys) of P_t stored; PV_t
+  // starts on the first part while the softmax computes the rest
+  enum { B_Q = 0, B_KF = 1, B_VF = 3, B_KE = 5, B_VE = 7, B_SF = 9, B_OD = 11, B_PF = 13, B_N = 13 + 2 * kPParts };
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + B_N);
   auto bar = [&](int i) { return smem_addr(bars + i); };
 
@@ -306,7 +313,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(bar(B_KE + s), 1);
       mbar_init(bar(B_VE + s), 1);
       mbar_init(bar(B_SF + s), 1);
-      mbar_init(bar(B_PF + s), 128);
+      for (int part = 0; part < kPParts; ++part) mbar_init(bar(B_PF + 2 * part + s), 128);
       mbar_init(bar(B_OD + s), 1);
     }
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
@@ -394,14 +401,17 @@ __global__ void __launch_bounds__(kThreads, 1)
     auto issue_pv = [&](int t, int j) {
       const int st = j & 1;
       mbar_wait(bar(B_VF + st), (j >> 1) & 1);
-      mbar_wait(bar(B_PF + t), j & 1);
-      tc_fence_after();
-      if (lane == 0 && j < 64) PDBG(256 + t * 64 + j);
 #pragma unroll
-      for (int k = 0; k < kN / 16; ++k) {
-        // A = P_t in TMEM (16 keys = 8 packed columns per step), B = V (MN-major)
-        const uint64_t bd = smem_desc(uV + st * kKVBytes + k * 16 * kRowB, kChunkB, 1024);
-        tc_mma_ts_elect(uT + 2 * kN + t * D, uT + t * kN + k * 8, bd, kIdescPV, (j > 0 || k > 0) ? 1u : 0u);
+      for (int h = 0; h < kPParts; ++h) {  // each part behind the softmax's store of that part of P
+        mbar_wait(bar(B_PF + 2 * h + t), j & 1);
+        tc_fence_after();
+        if (h == 0 && lane == 0 && j < 64) PDBG(256 + t * 64 + j);
+#pragma unroll
+        for (int k = h * (8 / kPParts); k < (h + 1) * (8 / kPParts); ++k) {
+          // A = P_t in TMEM (16 keys = 8 packed columns per step), B = V (MN-major)
+          const uint64_t bd = smem_desc(uV + st * kKVBytes + k * 16 * kRowB, kChunkB, 1024);
+          tc_mma_ts_elect(uT + 2 * kN + t * D, uT + t * kN + k * 8, bd, kIdescPV, (j > 0 || k > 0) ? 1u : 0u);
+        }
       }
     };
     // iteration j issues, per tile t: PV_t(j-1) (P_t(j-1) must be consumed
@@ -512,6 +522,11 @@ __global__ void __launch_bounds__(kThreads, 1)
           pk[e >> 1] = pack2<T>(pp.x, pp.y);
         }
         tmem_st16(tS + c * 16, pk);
+        if ((c + 1) % (4 / kPParts) == 0 && c + 1 < kN / 32) {  // a part of P stored: its PV may start
+          tmem_wait_st();
+          tc_fence_before();
+          mbar_arrive(bar(B_PF + 2 * ((c + 1) / (4 / kPParts) - 1) + t));
+        }
       }
       {
         const float2 a = fadd2(fadd2(l2[0], l2[1]), fadd2(l2[2], l2[3]));
@@ -520,7 +535,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       PHASE(3);
       tmem_wait_st();
       tc_fence_before();
-      mbar_arrive(bar(B_PF + t));
+      mbar_arrive(bar(B_PF + 2 * (kPParts - 1) + t));
       PHASE(4);
       if (r == 0 && j < 64) PDBG(128 + t * 64 + j);
     }
@@ -650,7 +665,7 @@ template <typename T, int D>
 size_t smem_bytes() {
   constexpr int NCH = D / 64;
   // at least 116 KB: one CTA per SM, so the 512-column TMEM allocation never waits
-  return std::max<size_t>(1024 + NCH * kChunkB * 6 + 16 * 8 + 16, 116 * 1024);
+  return std::max<size_t>(1024 + NCH * kChunkB * 6 + (14 + 2 * kPParts) * 8 + 16, 116 * 1024);
 }
 
 template <typename T, int D>
