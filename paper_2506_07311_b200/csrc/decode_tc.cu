@@ -328,7 +328,33 @@ __global__ void __launch_bounds__(kThreadsTc, 1) decode_tc_kernel(const __grid_c
   trace(0);
   // ---------------- plan (host-computed; staged into shared memory) ---------
   PlanView pv;
-  {
+  if (p.cl_inline) {
+    // cluster mode, plan in the launch parameters: CTA n runs item n — its
+    // cluster rank's even share of the pages of unit n / cluster
+    const int nq = p.nq;
+    pv.nk = p.cl_nkrow;
+    pv.row = p.cl_nkrow + nq;
+    pv.hb = p.cl_hb;
+    pv.wph = p.cl_wph;
+    pv.cluster = p.cl_cluster;
+    pv.qgs = p.cl_qgs;
+    pv.qgroups = p.cl_qgroups;
+    pv.nq = nq;
+    pv.count = 1;
+    if (threadIdx.x == 0) {
+      const int unit = static_cast<int>(blockIdx.x) / pv.cluster, c = static_cast<int>(blockIdx.x) % pv.cluster;
+      const int q = unit / p.cl_head_items;
+      const int pages = (pv.nk[q] + (1 << p.log2ps) - 1) >> p.log2ps;
+      s_cta_items[0] = q;
+      s_cta_items[1] = unit - q * p.cl_head_items;
+      s_cta_items[2] = static_cast<int>(int64_t(pages) * c / pv.cluster);
+      s_cta_items[3] = static_cast<int>(int64_t(pages) * (c + 1) / pv.cluster);
+      s_cta_items[4] = -1;
+      s_cta_items[5] = -1;
+    }
+    __syncthreads();
+    pv.items = s_cta_items;
+  } else {
     const int32_t* g = p.plan;
     const int nq = p.nq;
     const int32_t* off = g + o_cta(nq);
@@ -1137,6 +1163,7 @@ int plan_decode(const int32_t* nk, const int32_t* row, int64_t nq, int page_size
 }
 
 
+static_assert(sizeof(TcParams) <= sizeof(RecordedOp::args), "graph recorder argument buffer too small");
 int launch_decode_tc(TcParams p, const int32_t* plan_host, int kv_dtype, int head_dim, int num_sms,
                      cudaStream_t stream) {
   const bool splitq = p.q_dtype == PKV_F32;
@@ -1148,6 +1175,20 @@ int launch_decode_tc(TcParams p, const int32_t* plan_host, int kv_dtype, int hea
   else
     fn = head_dim == 64 ? pick_rows<__half, 64>(splitq, rows16) : pick_rows<__half, 128>(splitq, rows16);
   const int merge_bytes = kWarpsTc * kMergeRows * head_dim * 4 + kWarpsTc * kMergeRows * 2 * 4;
+  p.cl_inline = 0;
+  if (plan_host[H_CLUSTER] > 1 && p.nq <= 64) {  // the cluster plan fits the launch parameters
+    p.cl_inline = 1;
+    p.cl_hb = plan_host[H_HB];
+    p.cl_wph = plan_host[H_WPH];
+    p.cl_qgs = plan_host[H_QGS];
+    p.cl_qgroups = plan_host[H_QGROUPS];
+    p.cl_head_items = plan_host[H_HEAD_ITEMS];
+    p.cl_cluster = plan_host[H_CLUSTER];
+    for (int i = 0; i < p.nq; ++i) {
+      p.cl_nkrow[i] = plan_host[o_nk(p.nq) + i];
+      p.cl_nkrow[p.nq + i] = plan_host[o_row(p.nq) + i];
+    }
+  }
   const int64_t plan_bytes = o_cta(p.nq) * 4;
   p.plan_in_smem = p.nq <= kSmemPlanMax;
   p.merge_offset = p.plan_in_smem ? static_cast<int>((plan_bytes + 127) / 128 * 128) : 0;

@@ -34,6 +34,11 @@ struct TcParams {
   int merge_offset;
   int ring_offset;
   int kv_dtype;
+  // cluster mode with few queries: the plan is carried in the launch
+  // parameters (no dependent plan loads before the first block-table read)
+  int cl_inline;
+  int cl_hb, cl_wph, cl_qgs, cl_qgroups, cl_head_items, cl_cluster;
+  int32_t cl_nkrow[2 * 64];  // nk[nq] | row[nq]
 };
 
 using TcFn = void (*)(TcParams);

@@ -23,7 +23,7 @@ struct RecordedOp {
   const void* fn = nullptr;
   dim3 grid, block;
   unsigned smem = 0, cluster = 1;
-  alignas(16) unsigned char args[640];
+  alignas(16) unsigned char args[1024];  // >= sizeof(TcParams) (static_assert in decode_tc.cu)
   size_t arg_off[16];
   int nargs = 0;
   size_t args_used = 0;
