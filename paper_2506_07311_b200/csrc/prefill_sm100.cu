@@ -17,24 +17,20 @@
 // describe.  Pages past the end of the block table are fetched with an
 // out-of-range row coordinate, which TMA fills with zeros.
 //
-// Warp roles (256 threads, one CTA per SM):
-//   warp 0     TMA producer: Q once, then K/V tiles through a 2-stage ring;
-//   warp 1     MMA issuer (one thread): S_j = Q K_j^T into TMEM (double
-//              buffered), then O += P_{j-1} V_{j-1} (P from shared memory,
-//              V as an MN-major operand) — QK of the next tile is in flight
-//              while the softmax works on the current one;
-//   warp 2     TMEM allocator (512 columns: S0, S1, O);
-//   warps 4-7  softmax + epilogue: thread t owns query row t (TMEM lane t),
-//              so row max / sum need no shuffles.  One pass over S per tile:
-//              the row's 128 scores come out of TMEM in four loads behind one
-//              wait and stay in registers for the max and for P (measured
-//              +0.6% over two TMEM passes: not the limiter, but one
-//              round trip less).  Online softmax in base 2
-//              with a lazily updated running max: O and l are rescaled only
-//              when the row max grows by more than 2^8 (exact — numerator
-//              and denominator share the stale max — and rare after the
-//              first tiles).  P is rounded to the operand type and written
-//              to shared memory in the swizzled K-major layout.
+// Warp roles (384 threads, one CTA per SM; see the kernel comment):
+//   warp 0     TMA producer: Q (two query tiles) once, then 128-key K/V tiles
+//              through a 2-stage ring (a tile whose pages form one contiguous
+//              run is one 128-row box per chunk);
+//   warp 1     MMA issuer (one elected lane): QK of 64-key sub-tiles into
+//              double-buffered S, PV from P in TMEM;
+//   warp 2     TMEM allocator (512 columns: S_A[2], S_B[2], O_A, O_B);
+//   warps 4-11 two softmax + epilogue warpgroups, one per query tile: thread
+//              = query row (TMEM lane), so row max / sum need no shuffles.
+//              Online softmax in base 2 with a lazily updated running max:
+//              O and l are rescaled only when the row max grows by more than
+//              2^8 (exact — numerator and denominator share the stale max —
+//              and rare after the first sub-tiles).  P is rounded to the
+//              operand type and written over its S columns in TMEM.
 //
 // Causal masking is applied only on tiles that reach past a row's last
 // allowed key; tiles entirely above the diagonal are never visited (the
@@ -42,6 +38,7 @@
 #include <cuda.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <numeric>
@@ -61,11 +58,6 @@ constexpr int kChunkB = kM * kRowB;  // one 64-column chunk of a 128-row tile: 1
 constexpr int kItemInts = 10;
 constexpr float kLog2eP = 1.4426950408889634f;
 constexpr float kRescaleThreshold = 8.0f;  // log2 units
-#ifndef PKV_K3_PPARTS
-#define PKV_K3_PPARTS 2
-#endif
-constexpr int kPParts = PKV_K3_PPARTS;  // P published in 1, 2 or 4 parts (of 128 / kPParts keys)
-static_assert(kPParts == 1 || kPParts == 2 || kPParts == 4, "P parts");
 
 // ---- PTX wrappers -----------------------------------------------------------
 __device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
@@ -260,33 +252,39 @@ __device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t* v) {
 }
 
 // Two query tiles (A: item rows 0-127, B: rows 128-255) share every K/V
-// tile.  TMEM: S_A | S_B | O_A | O_B; P_t (16-bit) overwrites the first 64
-// columns of S_t and is the A operand of O_t += P_t V.  Per tile the chain
-// QK_t(j) -> softmax_t(j) -> PV_t(j) -> QK_t(j+1) is serial (P aliases S, and
-// the MMAs of one issuing thread execute in order), so the two tiles
-// ping-pong: while one softmax warpgroup works, the tensor core runs the
-// other tile's PV and next QK.
+// tile; scores come in 64-key sub-tiles with S double-buffered per query
+// tile, so QK of sub-tile u + 1 runs on the tensor core while the softmax
+// works on sub-tile u: the per-tile chain softmax -> PV -> QK is off the
+// critical path (a 128-key S per tile left the tensor core and the SFU each
+// ~50% busy, profiles/r02/k3_experiments.md).  TMEM: S_A[2] | S_B[2] (64
+// columns each) | O_A | O_B = 512 columns; P_t(u) (16-bit) overwrites the
+// first 32 columns of S_t[u & 1].  K/V still arrive in 128-key tiles (2
+// stages); sub-tile u uses half u & 1 of tile u >> 1.  Issue order of the
+// MMA thread per sub-tile u and query tile t: PV_t(u) (behind P_t(u)), then
+// QK_t(u + 2) into the buffer PV_t(u) has just read.  A lazy rescale of O_t
+// must follow PV_t(u - 1): every sub-tile waits for the previous PV (long
+// complete by then) before publishing its P.
 template <typename T, int D>
 __global__ void __launch_bounds__(kThreads, 1)
     prefill_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
-                      const __grid_constant__ CUtensorMap tm_v, const __grid_constant__ CUtensorMap tm_k128,
-                      const __grid_constant__ CUtensorMap tm_v128, const __grid_constant__ PrefillParams p) {
-  constexpr int NCH = D / 64;                 // 64-column chunks of the head dim
-  constexpr int kQBytes = NCH * kChunkB;      // one Q tile
-  constexpr int kKVBytes = NCH * kChunkB;     // one K (or V) tile of 128 keys
-  constexpr uint32_t kIdescQK = instr_desc(Fmt<T>::kFmt, 0, kM, kN);
+                     const __grid_constant__ CUtensorMap tm_v, const __grid_constant__ CUtensorMap tm_k128,
+                     const __grid_constant__ CUtensorMap tm_v128, const __grid_constant__ PrefillParams p) {
+  constexpr int NCH = D / 64;
+  constexpr int kQBytes = NCH * kChunkB;
+  constexpr int kKVBytes = NCH * kChunkB;
+  constexpr int kS = 64;  // keys per score sub-tile
+  constexpr uint32_t kIdescQK = instr_desc(Fmt<T>::kFmt, 0, kM, kS);
   constexpr uint32_t kIdescPV = instr_desc(Fmt<T>::kFmt, 1, kM, D);
   constexpr uint32_t kTmemCols = 512;
 
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  const uint32_t sQ = smem_addr(smem);                // 2 tiles
-  const uint32_t sK = sQ + 2 * kQBytes;               // 2 stages
-  const uint32_t sV = sK + 2 * kKVBytes;              // 2 stages
+  const uint32_t sQ = smem_addr(smem);
+  const uint32_t sK = sQ + 2 * kQBytes;
+  const uint32_t sV = sK + 2 * kKVBytes;
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + 2 * kQBytes + 4 * kKVBytes);
-  // PF + 2*part + t: part `part` (kN / kPParts keys) of P_t stored; PV_t
-  // starts on the first part while the softmax computes the rest
-  enum { B_Q = 0, B_KF = 1, B_VF = 3, B_KE = 5, B_VE = 7, B_SF = 9, B_OD = 11, B_PF = 13, B_N = 13 + 2 * kPParts };
+  // SF / PF: [tile t][buffer b] at + 2t + b
+  enum { B_Q = 0, B_KF = 1, B_VF = 3, B_KE = 5, B_VE = 7, B_SF = 9, B_PF = 13, B_OD = 17, B_N = 19 };
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + B_N);
   auto bar = [&](int i) { return smem_addr(bars + i); };
 
@@ -298,6 +296,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int cnt[2] = {it[1], it[2]};
   const int nt[2] = {it[7], it[8]};
   const int n_tiles = max(nt[0], nt[1]);
+  const int nu[2] = {2 * nt[0], 2 * nt[1]};
+  const int nu_max = 2 * n_tiles;
 
   if (p.dbg && threadIdx.x == 0) {  // per-CTA record: start, first S, end, SM
     p.dbg[512 + 4 * blockIdx.x] = gtime();
@@ -312,9 +312,11 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(bar(B_VF + s), 1);
       mbar_init(bar(B_KE + s), 1);
       mbar_init(bar(B_VE + s), 1);
-      mbar_init(bar(B_SF + s), 1);
-      for (int part = 0; part < kPParts; ++part) mbar_init(bar(B_PF + 2 * part + s), 128);
       mbar_init(bar(B_OD + s), 1);
+    }
+    for (int s = 0; s < 4; ++s) {
+      mbar_init(bar(B_SF + s), 1);
+      mbar_init(bar(B_PF + s), 128);
     }
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
@@ -332,13 +334,9 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   if (warp == 0) {
     if (lane == 0) {
-      // ---------------- TMA producer ----------------
+      // ---------------- TMA producer (128-key K/V tiles, 2 stages) ----------------
       asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<uint64_t>(&tm_k)) : "memory");
       asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<uint64_t>(&tm_v)) : "memory");
-      if (p.bt && p.box_rows < kN) {
-        asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<uint64_t>(&tm_k128)) : "memory");
-        asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<uint64_t>(&tm_v128)) : "memory");
-      }
       const int ntiles_q = cnt[1] > 0 ? 2 : 1;
       mbar_expect_tx(bar(B_Q), kQBytes * ntiles_q);
       for (int t = 0; t < ntiles_q; ++t)
@@ -351,7 +349,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       for (int j = 0; j < n_tiles; ++j) {
         const int st = j & 1;
         int rows[16];
-        bool run = p.bt != nullptr && boxes > 1;  // the tile's pages are one physically contiguous run
+        bool run = p.bt != nullptr && boxes > 1;
         for (int b = 0; b < boxes; ++b) {
           const int key0 = j * kN + b * p.box_rows;
           if (p.bt) {
@@ -359,11 +357,9 @@ __global__ void __launch_bounds__(kThreads, 1)
             rows[b] = pg < n_pages ? tbl[pg] * ps + (key0 & (ps - 1)) : p.oob_row;
             run = run && pg < n_pages && rows[b] == rows[0] + b * p.box_rows;
           } else {
-            rows[b] = mrow + key0;  // gathered: contiguous rows (past the end: zero fill)
+            rows[b] = mrow + key0;
           }
         }
-        // a run of consecutive pages (a fresh pool hands them out in order)
-        // is one 128-row box per chunk instead of one box per page
         const CUtensorMap* mk = run ? &tm_k128 : &tm_k;
         const CUtensorMap* mv = run ? &tm_v128 : &tm_v;
         const int nb = run ? 1 : boxes;
@@ -371,82 +367,95 @@ __global__ void __launch_bounds__(kThreads, 1)
         mbar_expect_tx(bar(B_KF + st), kKVBytes);
         for (int b = 0; b < nb; ++b)
           for (int c = 0; c < NCH; ++c)
-            tma_load_3d(sK + st * kKVBytes + c * kChunkB + b * p.box_rows * kRowB, mk, bar(B_KF + st),
-                        c * 64, kvh, rows[b]);
+            tma_load_3d(sK + st * kKVBytes + c * kChunkB + b * p.box_rows * kRowB, mk, bar(B_KF + st), c * 64, kvh,
+                        rows[b]);
         if (j >= 2) mbar_wait(bar(B_VE + st), ((j >> 1) - 1) & 1);
         mbar_expect_tx(bar(B_VF + st), kKVBytes);
         for (int b = 0; b < nb; ++b)
           for (int c = 0; c < NCH; ++c)
-            tma_load_3d(sV + st * kKVBytes + c * kChunkB + b * p.box_rows * kRowB, mv, bar(B_VF + st),
-                        c * 64, kvh, rows[b]);
+            tma_load_3d(sV + st * kKVBytes + c * kChunkB + b * p.box_rows * kRowB, mv, bar(B_VF + st), c * 64, kvh,
+                        rows[b]);
       }
     }
   } else if (warp == 1) {
-    // ---------------- MMA issuer (whole warp, one elected lane issues) ----------------
-    // broadcast the operand bases so the compiler sees warp-uniform values
+    // ---------------- MMA issuer ----------------
     const uint32_t uQ = __shfl_sync(0xffffffffu, sQ, 0), uK = __shfl_sync(0xffffffffu, sK, 0);
     const uint32_t uV = __shfl_sync(0xffffffffu, sV, 0), uT = __shfl_sync(0xffffffffu, tmem, 0);
     mbar_wait(bar(B_Q), 0);
     tc_fence_after();
-    auto issue_qk = [&](int t, int j) {
-      const int st = j & 1;
+    int k_waited = -1, v_waited = -1;  // last K / V tile whose full barrier was waited
+    auto need_k = [&](int j) {
+      if (j > k_waited) {
+        mbar_wait(bar(B_KF + (j & 1)), (j >> 1) & 1);
+        tc_fence_after();
+        k_waited = j;
+      }
+    };
+    auto need_v = [&](int j) {
+      if (j > v_waited) {
+        mbar_wait(bar(B_VF + (j & 1)), (j >> 1) & 1);
+        tc_fence_after();
+        v_waited = j;
+      }
+    };
+    // S_t[u & 1] = Q_t K(u)^T over the 64 keys of sub-tile u
+    auto issue_qk = [&](int t, int u) {
+      const int j = u >> 1, st = j & 1, h = u & 1;
+      need_k(j);
 #pragma unroll
       for (int k = 0; k < D / 16; ++k) {
         const uint64_t ad = smem_desc(uQ + t * kQBytes + (k >> 2) * kChunkB + (k & 3) * 32, 16, 1024);
-        const uint64_t bd = smem_desc(uK + st * kKVBytes + (k >> 2) * kChunkB + (k & 3) * 32, 16, 1024);
-        tc_mma_elect(uT + t * kN, ad, bd, kIdescQK, k > 0 ? 1u : 0u);
+        const uint64_t bd =
+            smem_desc(uK + st * kKVBytes + (k >> 2) * kChunkB + h * kS * kRowB + (k & 3) * 32, 16, 1024);
+        tc_mma_elect(uT + t * 2 * kS + h * kS, ad, bd, kIdescQK, k > 0 ? 1u : 0u);
       }
-      tc_commit_elect(bar(B_SF + t));
+      tc_commit_elect(bar(B_SF + 2 * t + h));
     };
-    auto issue_pv = [&](int t, int j) {
-      const int st = j & 1;
-      mbar_wait(bar(B_VF + st), (j >> 1) & 1);
+    // O_t += P_t(u) V(u): P in the first 32 columns of S_t[u & 1]
+    auto issue_pv = [&](int t, int u) {
+      const int j = u >> 1, st = j & 1, h = u & 1;
+      need_v(j);
+      mbar_wait(bar(B_PF + 2 * t + h), (u >> 1) & 1);
+      tc_fence_after();
 #pragma unroll
-      for (int h = 0; h < kPParts; ++h) {  // each part behind the softmax's store of that part of P
-        mbar_wait(bar(B_PF + 2 * h + t), j & 1);
-        tc_fence_after();
-        if (h == 0 && lane == 0 && j < 64) PDBG(256 + t * 64 + j);
-#pragma unroll
-        for (int k = h * (8 / kPParts); k < (h + 1) * (8 / kPParts); ++k) {
-          // A = P_t in TMEM (16 keys = 8 packed columns per step), B = V (MN-major)
-          const uint64_t bd = smem_desc(uV + st * kKVBytes + k * 16 * kRowB, kChunkB, 1024);
-          tc_mma_ts_elect(uT + 2 * kN + t * D, uT + t * kN + k * 8, bd, kIdescPV, (j > 0 || k > 0) ? 1u : 0u);
+      for (int k = 0; k < kS / 16; ++k) {
+        const uint64_t bd = smem_desc(uV + st * kKVBytes + (h * kS + k * 16) * kRowB, kChunkB, 1024);
+        tc_mma_ts_elect(uT + 4 * kS + t * D, uT + t * 2 * kS + h * kS + k * 8, bd, kIdescPV,
+                        (u > 0 || k > 0) ? 1u : 0u);
+      }
+      tc_commit_elect(bar(B_OD + t));
+    };
+    for (int t = 0; t < 2; ++t)
+      for (int u = 0; u < 2; ++u)
+        if (u < nu[t]) issue_qk(t, u);
+    if (n_tiles > 0) tc_commit_elect(bar(B_KE + 0));  // K tile 0: both halves, both query tiles
+    for (int u = 0; u < nu_max; ++u) {
+      for (int t = 0; t < 2; ++t) {
+        if (u < nu[t]) {
+          issue_pv(t, u);
+          if (u + 2 < nu[t]) issue_qk(t, u + 2);
         }
       }
-    };
-    // iteration j issues, per tile t: PV_t(j-1) (P_t(j-1) must be consumed
-    // before QK_t(j) overwrites it) then QK_t(j); j == n_tiles drains
-    for (int j = 0; j <= n_tiles; ++j) {
-      const int st = j & 1;
-      if (j < n_tiles) {
-        mbar_wait(bar(B_KF + st), (j >> 1) & 1);
-        tc_fence_after();
-        if (lane == 0 && j < 64) PDBG(384 + j);
+      // V tile u >> 1 fully read once its second half was issued for both tiles;
+      // K tile (u + 2) >> 1 fully read once both its halves were issued
+      if (u & 1) {
+        tc_commit_elect(bar(B_VE + ((u >> 1) & 1)));
+        const int jk = (u + 1) >> 1;  // QK(u + 2) for odd u completes K tile (u + 1) / 2
+        if (jk < n_tiles) tc_commit_elect(bar(B_KE + (jk & 1)));
       }
-      for (int t = 0; t < 2; ++t) {
-        if (j > 0 && j - 1 < nt[t]) issue_pv(t, j - 1);
-        if (j < nt[t]) issue_qk(t, j);
-        if (j == nt[t] && nt[t] > 0) tc_commit_elect(bar(B_OD + t));  // after its final PV
-      }
-      if (j < n_tiles) tc_commit_elect(bar(B_KE + st));
-      if (j > 0) tc_commit_elect(bar(B_VE + ((j - 1) & 1)));  // every PV of V tile j-1 is issued
     }
   } else if (warp >= 4) {
-    // ---------------- softmax + epilogue: warpgroup t, thread = query row ----------------
+    // ---------------- softmax + epilogue ----------------
     const int t = (warp - 4) >> 2;
     const int r = threadIdx.x - 128 - 128 * t;
     const uint32_t lane_base = static_cast<uint32_t>((warp & 3) * 32) << 16;
-    const uint32_t tS = tmem + lane_base + t * kN;
-    const uint32_t tO = tmem + lane_base + 2 * kN + t * D;
+    const uint32_t tO = tmem + lane_base + 4 * kS + t * D;
     const int qi = r / p.group;
     const int qpos = qpos0 + t * p.qt + qi;
-    const int nk = p.causal ? min(qpos + 1, kv_len) : kv_len;  // allowed key prefix of this row
+    const int nk = p.causal ? min(qpos + 1, kv_len) : kv_len;
     float m_used = -INFINITY, l = 0.f;
     const float2 qs2 = make_float2(p.qscale, p.qscale);
 #ifdef PKV_K3_PHASES
-    // -DPKV_K3_PHASES: clock64 per softmax phase (wait S, TMEM load, max,
-    // exp + store, publish) summed over the tiles of row 0 of each query tile
-    // of CTA 0, into dbg[448 + 8t + k] (tools/bench_prefill.py prints them)
     long long ph[5] = {0, 0, 0, 0, 0}, pc = clock64();
 #define PHASE(k)                      \
   do {                                \
@@ -459,59 +468,43 @@ __global__ void __launch_bounds__(kThreads, 1)
   do {           \
   } while (0)
 #endif
-    for (int j = 0; j < nt[t]; ++j) {
-      mbar_wait(bar(B_SF + t), j & 1);
+    for (int u = 0; u < nu[t]; ++u) {
+      const int h = u & 1;
+      const uint32_t tS = tmem + lane_base + t * 2 * kS + h * kS;
+      mbar_wait(bar(B_SF + 2 * t + h), (u >> 1) & 1);
       tc_fence_after();
       PHASE(0);
-      if (r == 0 && j < 64) PDBG(t * 64 + j);
-      if (p.dbg && r == 0 && t == 0 && j == 0) p.dbg[512 + 4 * blockIdx.x + 1] = gtime();
-      const int kbase = j * kN;
-      // diagonal / tail tiles take the masked code path (warp-uniform branch)
-      const bool masked = __any_sync(0xffffffffu, kbase + kN > nk);
-      // one pass over S: the row's 128 scores are loaded into registers with
-      // all four TMEM loads in flight behind one wait (masked entries -> -inf),
-      // then the max, then P from the registers
-      uint32_t v[kN];
+      if (r == 0 && u < 64) PDBG(t * 64 + u);
+      if (p.dbg && r == 0 && t == 0 && u == 0) p.dbg[512 + 4 * blockIdx.x + 1] = gtime();
+      const int kbase = u * kS;
+      const bool masked = __any_sync(0xffffffffu, kbase + kS > nk);
+      uint32_t v[kS];
 #pragma unroll
-      for (int c = 0; c < kN / 32; ++c) tmem_ld32(tS + c * 32, v + 32 * c);
+      for (int c = 0; c < kS / 32; ++c) tmem_ld32(tS + c * 32, v + 32 * c);
       tmem_wait_ld();
       PHASE(1);
       if (masked) {
-        const int lim = nk - kbase;  // element e is allowed iff e < lim
+        const int lim = nk - kbase;
 #pragma unroll
-        for (int e = 0; e < kN; ++e)
+        for (int e = 0; e < kS; ++e)
           if (e >= lim) v[e] = __float_as_uint(-INFINITY);
       }
       float mx4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
 #pragma unroll
-      for (int e = 0; e < kN; ++e) mx4[e & 3] = fmaxf(mx4[e & 3], __uint_as_float(v[e]));
-      float mx = fmaxf(fmaxf(mx4[0], mx4[1]), fmaxf(mx4[2], mx4[3]));
-      mx *= p.qscale;
+      for (int e = 0; e < kS; ++e) mx4[e & 3] = fmaxf(mx4[e & 3], __uint_as_float(v[e]));
+      const float mx = fmaxf(fmaxf(mx4[0], mx4[1]), fmaxf(mx4[2], mx4[3])) * p.qscale;
       float factor = 1.f;
       const bool need = mx > m_used + kRescaleThreshold;
       if (need) {
-        factor = ex2_ftz(m_used - mx);  // 0 on the first tile (m_used = -inf)
+        factor = ex2_ftz(m_used - mx);  // 0 while m_used = -inf
         m_used = mx;
       }
       l *= factor;
-      // O_t is stable here: PV_t(j-1) completed before S_t(j) was committed
-      if (j > 0 && __any_sync(0xffffffffu, need)) {
-#pragma unroll 1
-        for (int c = 0; c < D / 32; ++c) {
-          uint32_t o[32];
-          tmem_ld32(tO + c * 32, o);
-          tmem_wait_ld();
-#pragma unroll
-          for (int e = 0; e < 32; ++e) o[e] = __float_as_uint(__uint_as_float(o[e]) * factor);
-          tmem_st32(tO + c * 32, o);
-        }
-      }
       PHASE(2);
-      // P = 2^(s*qscale - m) rounded to 16 bits, written over S
       const float2 negm2 = make_float2(-m_used, -m_used);
       float2 l2[4] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
 #pragma unroll
-      for (int c = 0; c < kN / 32; ++c) {
+      for (int c = 0; c < kS / 32; ++c) {
         uint32_t pk[16];
 #pragma unroll
         for (int e = 0; e < 32; e += 2) {
@@ -522,31 +515,41 @@ __global__ void __launch_bounds__(kThreads, 1)
           pk[e >> 1] = pack2<T>(pp.x, pp.y);
         }
         tmem_st16(tS + c * 16, pk);
-        if ((c + 1) % (4 / kPParts) == 0 && c + 1 < kN / 32) {  // a part of P stored: its PV may start
-          tmem_wait_st();
-          tc_fence_before();
-          mbar_arrive(bar(B_PF + 2 * ((c + 1) / (4 / kPParts) - 1) + t));
-        }
       }
       {
         const float2 a = fadd2(fadd2(l2[0], l2[1]), fadd2(l2[2], l2[3]));
         l += a.x + a.y;
       }
       PHASE(3);
+      if (u > 0) {
+        // PV_t(u - 1) done: O_t holds every earlier sub-tile (rescale point)
+        mbar_wait(bar(B_OD + t), (u - 1) & 1);
+        tc_fence_after();
+        if (__any_sync(0xffffffffu, need)) {
+#pragma unroll 1
+          for (int c = 0; c < D / 32; ++c) {
+            uint32_t o[32];
+            tmem_ld32(tO + c * 32, o);
+            tmem_wait_ld();
+#pragma unroll
+            for (int e = 0; e < 32; ++e) o[e] = __float_as_uint(__uint_as_float(o[e]) * factor);
+            tmem_st32(tO + c * 32, o);
+          }
+        }
+      }
       tmem_wait_st();
       tc_fence_before();
-      mbar_arrive(bar(B_PF + 2 * (kPParts - 1) + t));
+      mbar_arrive(bar(B_PF + 2 * t + h));
       PHASE(4);
-      if (r == 0 && j < 64) PDBG(128 + t * 64 + j);
+      if (r == 0 && u < 64) PDBG(128 + t * 64 + u);
     }
 #ifdef PKV_K3_PHASES
     if (p.dbg && blockIdx.x == 0 && r == 0)
       for (int k = 0; k < 5; ++k) p.dbg[448 + 8 * t + k] = static_cast<unsigned long long>(ph[k]);
 #endif
 #undef PHASE
-    // epilogue: O / l for the valid rows
-    if (nt[t] > 0) {
-      mbar_wait(bar(B_OD + t), 0);
+    if (nu[t] > 0) {
+      mbar_wait(bar(B_OD + t), (nu[t] - 1) & 1);
       tc_fence_after();
       const bool valid = qi < cnt[t];
       const float inv = l > 0.f ? 1.f / l : 0.f;
@@ -570,10 +573,10 @@ __global__ void __launch_bounds__(kThreads, 1)
             for (int e = 0; e < 4; ++e) {
               uint32_t w[4];
 #pragma unroll
-              for (int h = 0; h < 4; ++h) {
-                const float a = __uint_as_float(o[8 * e + 2 * h]) * inv;
-                const float b = __uint_as_float(o[8 * e + 2 * h + 1]) * inv;
-                w[h] = p.out_dtype == PKV_BF16 ? pack2<__nv_bfloat16>(a, b) : pack2<__half>(a, b);
+              for (int hh = 0; hh < 4; ++hh) {
+                const float a = __uint_as_float(o[8 * e + 2 * hh]) * inv;
+                const float b = __uint_as_float(o[8 * e + 2 * hh + 1]) * inv;
+                w[hh] = p.out_dtype == PKV_BF16 ? pack2<__nv_bfloat16>(a, b) : pack2<__half>(a, b);
               }
               dst[e] = make_uint4(w[0], w[1], w[2], w[3]);
             }
@@ -665,7 +668,7 @@ template <typename T, int D>
 size_t smem_bytes() {
   constexpr int NCH = D / 64;
   // at least 116 KB: one CTA per SM, so the 512-column TMEM allocation never waits
-  return std::max<size_t>(1024 + NCH * kChunkB * 6 + (14 + 2 * kPParts) * 8 + 16, 116 * 1024);
+  return std::max<size_t>(1024 + NCH * kChunkB * 6 + 20 * 8 + 16, 116 * 1024);
 }
 
 template <typename T, int D>
