@@ -284,7 +284,12 @@ __global__ void __launch_bounds__(kThreads, 1)
   const uint32_t sV = sK + 2 * kKVBytes;
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + 2 * kQBytes + 4 * kKVBytes);
   // SF / PF: [tile t][buffer b] at + 2t + b
-  enum { B_Q = 0, B_KF = 1, B_VF = 3, B_KE = 5, B_VE = 7, B_SF = 9, B_PF = 13, B_OD = 17, B_N = 19 };
+  // OD: [tile t][parity of u] at + 2t + (u & 1): PV_t(u) complete.  Two
+  // alternating barriers per tile let the softmax skip the wait when no
+  // row rescales: PV_t(u + 2), the next completion on a barrier, cannot be
+  // issued before the softmax publishes P_t(u + 2), so a later wait never
+  // sees a barrier two phases ahead
+  enum { B_Q = 0, B_KF = 1, B_VF = 3, B_KE = 5, B_VE = 7, B_SF = 9, B_PF = 13, B_OD = 17, B_N = 21 };
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + B_N);
   auto bar = [&](int i) { return smem_addr(bars + i); };
 
@@ -312,11 +317,11 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(bar(B_VF + s), 1);
       mbar_init(bar(B_KE + s), 1);
       mbar_init(bar(B_VE + s), 1);
-      mbar_init(bar(B_OD + s), 1);
     }
     for (int s = 0; s < 4; ++s) {
       mbar_init(bar(B_SF + s), 1);
       mbar_init(bar(B_PF + s), 128);
+      mbar_init(bar(B_OD + s), 1);
     }
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
@@ -423,7 +428,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         tc_mma_ts_elect(uT + 4 * kS + t * D, uT + t * 2 * kS + h * kS + k * 8, bd, kIdescPV,
                         (u > 0 || k > 0) ? 1u : 0u);
       }
-      tc_commit_elect(bar(B_OD + t));
+      tc_commit_elect(bar(B_OD + 2 * t + h));
     };
     for (int t = 0; t < 2; ++t)
       for (int u = 0; u < 2; ++u)
@@ -521,11 +526,11 @@ __global__ void __launch_bounds__(kThreads, 1)
         l += a.x + a.y;
       }
       PHASE(3);
-      if (u > 0) {
-        // PV_t(u - 1) done: O_t holds every earlier sub-tile (rescale point)
-        mbar_wait(bar(B_OD + t), (u - 1) & 1);
+      if (u > 0 && __any_sync(0xffffffffu, need)) {
+        // rescale point: PV_t(u - 1) done, O_t holds every earlier sub-tile
+        mbar_wait(bar(B_OD + 2 * t + ((u - 1) & 1)), ((u - 1) >> 1) & 1);
         tc_fence_after();
-        if (__any_sync(0xffffffffu, need)) {
+        {
 #pragma unroll 1
           for (int c = 0; c < D / 32; ++c) {
             uint32_t o[32];
@@ -549,7 +554,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 #endif
 #undef PHASE
     if (nu[t] > 0) {
-      mbar_wait(bar(B_OD + t), (nu[t] - 1) & 1);
+      mbar_wait(bar(B_OD + 2 * t + ((nu[t] - 1) & 1)), ((nu[t] - 1) >> 1) & 1);
       tc_fence_after();
       const bool valid = qi < cnt[t];
       const float inv = l > 0.f ? 1.f / l : 0.f;
@@ -668,7 +673,7 @@ template <typename T, int D>
 size_t smem_bytes() {
   constexpr int NCH = D / 64;
   // at least 116 KB: one CTA per SM, so the 512-column TMEM allocation never waits
-  return std::max<size_t>(1024 + NCH * kChunkB * 6 + 20 * 8 + 16, 116 * 1024);
+  return std::max<size_t>(1024 + NCH * kChunkB * 6 + 22 * 8 + 16, 116 * 1024);
 }
 
 template <typename T, int D>
