@@ -209,6 +209,7 @@ struct PrefillParams {
   void* out;
   int out_dtype;
   const int32_t* items;
+  int o_cols;               // > 0: full tiles leave by TMA stores of o_cols-column boxes (tm_o)
   unsigned long long* dbg;  // debug timeline of CTA 0 (nullptr = off)
 };
 __device__ __forceinline__ unsigned long long gtime() {
@@ -268,7 +269,8 @@ template <typename T, int D>
 __global__ void __launch_bounds__(kThreads, 1)
     prefill_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
                      const __grid_constant__ CUtensorMap tm_v, const __grid_constant__ CUtensorMap tm_k128,
-                     const __grid_constant__ CUtensorMap tm_v128, const __grid_constant__ PrefillParams p) {
+                     const __grid_constant__ CUtensorMap tm_v128, const __grid_constant__ CUtensorMap tm_o,
+                     const __grid_constant__ PrefillParams p) {
   constexpr int NCH = D / 64;
   constexpr int kQBytes = NCH * kChunkB;
   constexpr int kKVBytes = NCH * kChunkB;
@@ -558,32 +560,88 @@ __global__ void __launch_bounds__(kThreads, 1)
       tc_fence_after();
       const bool valid = qi < cnt[t];
       const float inv = l > 0.f ? 1.f / l : 0.f;
-      const int64_t orow =
-          (static_cast<int64_t>(q_row0) + t * p.qt + qi) * p.hq + kvh * p.group + (r - qi * p.group);
-#pragma unroll 1
-      for (int c = 0; c < D / 32; ++c) {
-        uint32_t o[32];
-        tmem_ld32(tO + c * 32, o);
-        tmem_wait_ld();
-        if (valid) {
+      if (p.o_cols > 0 && cnt[t] == p.qt) {
+        // full tile: stage O / l in Q_t's buffer (free: every QK of this tile
+        // is done) and leave by TMA stores of o_cols-column boxes; the CTA only
+        // waits for the bulk stores to READ shared memory, so it retires
+        // without waiting for its 64-128 KB of output to reach memory (register
+        // stores held each CTA ~6-9 us on the SM, tools/probes/cta_gap_probe.cu)
+        // 128-byte staging rows (o_cols = 32 fp32 or 64 16-bit columns) in the
+        // 128-byte-swizzled layout of the output map: the 16-byte units of a
+        // row land at unit ^ (row & 7), so a warp's stores hit every bank
+        uint8_t* my = smem + t * kQBytes + r * 128;
+        const uint32_t stage_s = sQ + t * kQBytes;
+        const uint32_t swz = static_cast<uint32_t>(r & 7);
+        for (int c0 = 0; c0 < D; c0 += p.o_cols) {
           if (p.out_dtype == PKV_F32) {
-            float4* dst = reinterpret_cast<float4*>(static_cast<float*>(p.out) + orow * D + c * 32);
+            uint32_t o[32];
+            tmem_ld32(tO + c0, o);
+            tmem_wait_ld();
 #pragma unroll
-            for (int e = 0; e < 8; ++e)
-              dst[e] = make_float4(__uint_as_float(o[4 * e]) * inv, __uint_as_float(o[4 * e + 1]) * inv,
-                                   __uint_as_float(o[4 * e + 2]) * inv, __uint_as_float(o[4 * e + 3]) * inv);
+            for (int k = 0; k < 8; ++k)
+              *reinterpret_cast<float4*>(my + ((k ^ swz) << 4)) =
+                  make_float4(__uint_as_float(o[4 * k]) * inv, __uint_as_float(o[4 * k + 1]) * inv,
+                              __uint_as_float(o[4 * k + 2]) * inv, __uint_as_float(o[4 * k + 3]) * inv);
           } else {
-            uint4* dst = reinterpret_cast<uint4*>(static_cast<uint16_t*>(p.out) + orow * D + c * 32);
 #pragma unroll
-            for (int e = 0; e < 4; ++e) {
-              uint32_t w[4];
+            for (int half = 0; half < 2; ++half) {
+              uint32_t o[32];
+              tmem_ld32(tO + c0 + 32 * half, o);
+              tmem_wait_ld();
 #pragma unroll
-              for (int hh = 0; hh < 4; ++hh) {
-                const float a = __uint_as_float(o[8 * e + 2 * hh]) * inv;
-                const float b = __uint_as_float(o[8 * e + 2 * hh + 1]) * inv;
-                w[hh] = p.out_dtype == PKV_BF16 ? pack2<__nv_bfloat16>(a, b) : pack2<__half>(a, b);
+              for (int k = 0; k < 4; ++k) {
+                uint32_t w[4];
+#pragma unroll
+                for (int hh = 0; hh < 4; ++hh) {
+                  const float a = __uint_as_float(o[8 * k + 2 * hh]) * inv;
+                  const float b = __uint_as_float(o[8 * k + 2 * hh + 1]) * inv;
+                  w[hh] = p.out_dtype == PKV_BF16 ? pack2<__nv_bfloat16>(a, b) : pack2<__half>(a, b);
+                }
+                *reinterpret_cast<uint4*>(my + (((4 * half + k) ^ swz) << 4)) = make_uint4(w[0], w[1], w[2], w[3]);
               }
-              dst[e] = make_uint4(w[0], w[1], w[2], w[3]);
+            }
+          }
+          asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+          asm volatile("bar.sync %0, 128;\n" ::"r"(1 + t) : "memory");
+          if (r == 0) {
+            asm volatile(
+                "cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%2, %3, %4}], [%1];\n" ::"l"(
+                    reinterpret_cast<uint64_t>(&tm_o)),
+                "r"(stage_s), "r"(c0), "r"(kvh * p.group), "r"(q_row0 + t * p.qt)
+                : "memory");
+            asm volatile("cp.async.bulk.commit_group;\n" ::: "memory");
+            asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory");
+          }
+          asm volatile("bar.sync %0, 128;\n" ::"r"(1 + t) : "memory");  // staging free again
+        }
+      } else {
+        const int64_t orow =
+            (static_cast<int64_t>(q_row0) + t * p.qt + qi) * p.hq + kvh * p.group + (r - qi * p.group);
+#pragma unroll 1
+        for (int c = 0; c < D / 32; ++c) {
+          uint32_t o[32];
+          tmem_ld32(tO + c * 32, o);
+          tmem_wait_ld();
+          if (valid) {
+            if (p.out_dtype == PKV_F32) {
+              float4* dst = reinterpret_cast<float4*>(static_cast<float*>(p.out) + orow * D + c * 32);
+#pragma unroll
+              for (int e = 0; e < 8; ++e)
+                dst[e] = make_float4(__uint_as_float(o[4 * e]) * inv, __uint_as_float(o[4 * e + 1]) * inv,
+                                     __uint_as_float(o[4 * e + 2]) * inv, __uint_as_float(o[4 * e + 3]) * inv);
+            } else {
+              uint4* dst = reinterpret_cast<uint4*>(static_cast<uint16_t*>(p.out) + orow * D + c * 32);
+#pragma unroll
+              for (int e = 0; e < 4; ++e) {
+                uint32_t w[4];
+#pragma unroll
+                for (int hh = 0; hh < 4; ++hh) {
+                  const float a = __uint_as_float(o[8 * e + 2 * hh]) * inv;
+                  const float b = __uint_as_float(o[8 * e + 2 * hh + 1]) * inv;
+                  w[hh] = p.out_dtype == PKV_BF16 ? pack2<__nv_bfloat16>(a, b) : pack2<__half>(a, b);
+                }
+                dst[e] = make_uint4(w[0], w[1], w[2], w[3]);
+              }
             }
           }
         }
@@ -619,17 +677,20 @@ EncodeTiledFn encode_fn() {
 
 // 3-D map over [dim2][dim1][dim0] 16-bit elements, box (64, box1, box2), 128-B swizzle
 int encode_map(CUtensorMap* map, const void* base, int dtype, uint64_t dim0, uint64_t dim1, uint64_t dim2,
-               uint32_t box1, uint32_t box2) {
+               uint32_t box1, uint32_t box2, uint32_t box0 = 64, bool swizzle = true) {
   EncodeTiledFn fn = encode_fn();
   if (!fn) return fail(PKV_CUDA_ERROR, "cuTensorMapEncodeTiled unavailable");
+  const uint64_t es = dtype == PKV_F32 ? 4 : 2;
   const cuuint64_t dims[3] = {dim0, dim1, dim2};
-  const cuuint64_t strides[2] = {dim0 * 2, dim0 * dim1 * 2};
-  const cuuint32_t box[3] = {64, box1, box2};
+  const cuuint64_t strides[2] = {dim0 * es, dim0 * dim1 * es};
+  const cuuint32_t box[3] = {box0, box1, box2};
   const cuuint32_t estr[3] = {1, 1, 1};
-  const CUresult r = fn(map, dtype == PKV_BF16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT16,
-                        3, const_cast<void*>(base), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                        CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                        CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  const CUtensorMapDataType ty = dtype == PKV_F32    ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32
+                                 : dtype == PKV_BF16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16
+                                                     : CU_TENSOR_MAP_DATA_TYPE_FLOAT16;
+  const CUresult r = fn(map, ty, 3, const_cast<void*>(base), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                        swizzle ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE,
+                        CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) return fail(PKV_CUDA_ERROR, "cuTensorMapEncodeTiled failed (%d)", static_cast<int>(r));
   return PKV_OK;
 }
@@ -638,12 +699,13 @@ int encode_map(CUtensorMap* map, const void* base, int dtype, uint64_t dim0, uin
 // call; a caller that reuses its query buffer hits too): a small per-process
 // table keyed by every encode argument, most recent first.
 int make_map(CUtensorMap* map, const void* base, int dtype, uint64_t dim0, uint64_t dim1, uint64_t dim2,
-             uint32_t box1, uint32_t box2) {
+             uint32_t box1, uint32_t box2, uint32_t box0 = 64, bool swizzle = true) {
   struct Entry {
     const void* base;
     uint64_t d0, d1, d2;
-    uint32_t b1, b2;
+    uint32_t b0, b1, b2;
     int dtype;
+    bool swz;
     CUtensorMap map;
   };
   static std::mutex mu;
@@ -654,17 +716,17 @@ int make_map(CUtensorMap* map, const void* base, int dtype, uint64_t dim0, uint6
     for (size_t i = 0; i < cache.size(); ++i) {
       const Entry& e = cache[i];
       if (e.base == base && e.d0 == dim0 && e.d1 == dim1 && e.d2 == dim2 && e.b1 == box1 && e.b2 == box2 &&
-          e.dtype == dtype) {
+          e.dtype == dtype && e.b0 == box0 && e.swz == swizzle) {
         *map = e.map;
         if (i > 0) std::rotate(cache.begin(), cache.begin() + i, cache.begin() + i + 1);
         return PKV_OK;
       }
     }
   }
-  const int st = encode_map(map, base, dtype, dim0, dim1, dim2, box1, box2);
+  const int st = encode_map(map, base, dtype, dim0, dim1, dim2, box1, box2, box0, swizzle);
   if (st) return st;
   std::lock_guard<std::mutex> g(mu);
-  cache.insert(cache.begin(), Entry{base, dim0, dim1, dim2, box1, box2, dtype, *map});
+  cache.insert(cache.begin(), Entry{base, dim0, dim1, dim2, box0, box1, box2, dtype, swizzle, *map});
   if (cache.size() > kMaxEntries) cache.pop_back();
   return PKV_OK;
 }
@@ -696,6 +758,22 @@ int launch(const pkv_prefill_args* a, const PrefillParams& pp, cudaStream_t stre
     st = make_map(&mv128, a->v_cache, a->kv_dtype, D, a->hkv, a->cache_rows, 1, kN);
     if (st) return st;
   }
+  // output map: full tiles leave by TMA stores through Q_t's buffer (no
+  // swizzle; a box of o_cols columns x G heads x qt positions fills it)
+  CUtensorMap mo = mq;
+  PrefillParams pq = pp;
+  static const bool bulk_out = [] {
+    const char* e = std::getenv("PKV_K3_BULK_OUT");
+    return !(e && e[0] == '0');
+  }();
+  const int es = a->out_dtype == PKV_F32 ? 4 : 2;
+  const int o_cols = 128 / es;  // 128-byte swizzled rows: a box of kM x 128 B fills 16 KB of Q_t's buffer
+  pq.o_cols = 0;
+  if (bulk_out && (reinterpret_cast<uintptr_t>(a->out) & 15) == 0 && D % o_cols == 0) {
+    st = make_map(&mo, a->out, a->out_dtype, D, a->hq, a->total_q, G, kM / G, static_cast<uint32_t>(o_cols), true);
+    if (st) return st;
+    pq.o_cols = o_cols;
+  }
   const size_t smem = smem_bytes<T, D>();
   auto kern = prefill_tc_kernel<T, D>;
   static bool attr_set = false;
@@ -703,7 +781,7 @@ int launch(const pkv_prefill_args* a, const PrefillParams& pp, cudaStream_t stre
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
     attr_set = true;
   }
-  kern<<<static_cast<unsigned>(a->n_items), kThreads, smem, stream>>>(mq, mk, mv, mk128, mv128, pp);
+  kern<<<static_cast<unsigned>(a->n_items), kThreads, smem, stream>>>(mq, mk, mv, mk128, mv128, mo, pq);
   PKV_CHECK_LAUNCH();
   return PKV_OK;
 }
