@@ -302,7 +302,7 @@ __device__ __forceinline__ void finish_split_group(const TcParams& p, const int3
 }
 
 template <typename T, int D, bool SPLITQ, bool ROWS16>
-__global__ void __launch_bounds__(kThreadsTc, 1) decode_tc_kernel(const __grid_constant__ TcParams p) {
+__device__ __forceinline__ void decode_tc_body(const TcParams& p, const ClusterInline* ci) {
   constexpr int ROWB = D * 2;            // smem row bytes
   constexpr int CPR = ROWB / 16;         // 16-B chunks per row (8 or 16)
   constexpr int RPI = 32 / CPR;          // rows per copy iteration
@@ -328,25 +328,25 @@ __global__ void __launch_bounds__(kThreadsTc, 1) decode_tc_kernel(const __grid_c
   trace(0);
   // ---------------- plan (host-computed; staged into shared memory) ---------
   PlanView pv;
-  if (p.cl_inline) {
+  if (ci) {
     // cluster mode, plan in the launch parameters: CTA n runs item n — its
     // cluster rank's even share of the pages of unit n / cluster
     const int nq = p.nq;
-    pv.nk = p.cl_nkrow;
-    pv.row = p.cl_nkrow + nq;
-    pv.hb = p.cl_hb;
-    pv.wph = p.cl_wph;
-    pv.cluster = p.cl_cluster;
-    pv.qgs = p.cl_qgs;
-    pv.qgroups = p.cl_qgroups;
+    pv.nk = ci->nkrow;
+    pv.row = ci->nkrow + nq;
+    pv.hb = ci->hb;
+    pv.wph = ci->wph;
+    pv.cluster = ci->cluster;
+    pv.qgs = ci->qgs;
+    pv.qgroups = ci->qgroups;
     pv.nq = nq;
     pv.count = 1;
     if (threadIdx.x == 0) {
       const int unit = static_cast<int>(blockIdx.x) / pv.cluster, c = static_cast<int>(blockIdx.x) % pv.cluster;
-      const int q = unit / p.cl_head_items;
+      const int q = unit / ci->head_items;
       const int pages = (pv.nk[q] + (1 << p.log2ps) - 1) >> p.log2ps;
       s_cta_items[0] = q;
-      s_cta_items[1] = unit - q * p.cl_head_items;
+      s_cta_items[1] = unit - q * ci->head_items;
       s_cta_items[2] = static_cast<int>(int64_t(pages) * c / pv.cluster);
       s_cta_items[3] = static_cast<int>(int64_t(pages) * (c + 1) / pv.cluster);
       s_cta_items[4] = -1;
@@ -798,6 +798,22 @@ __global__ void __launch_bounds__(kThreadsTc, 1) decode_tc_kernel(const __grid_c
   trace(31);
 }
 
+template <typename T, int D, bool SPLITQ, bool ROWS16>
+__global__ void __launch_bounds__(kThreadsTc, 1) decode_tc_kernel(const __grid_constant__ TcParams p) {
+  decode_tc_body<T, D, SPLITQ, ROWS16>(p, nullptr);
+}
+template <typename T, int D, bool SPLITQ, bool ROWS16>
+__global__ void __launch_bounds__(kThreadsTc, 1)
+    decode_tc_cluster_kernel(const __grid_constant__ TcParams p, const __grid_constant__ ClusterInline ci) {
+  decode_tc_body<T, D, SPLITQ, ROWS16>(p, &ci);
+}
+using TcClusterFn = void (*)(TcParams, ClusterInline);
+template <typename T, int D>
+TcClusterFn pick_rows_cluster(bool splitq, bool rows16) {
+  if (splitq) return rows16 ? decode_tc_cluster_kernel<T, D, true, true> : decode_tc_cluster_kernel<T, D, true, false>;
+  return rows16 ? decode_tc_cluster_kernel<T, D, false, true> : decode_tc_cluster_kernel<T, D, false, false>;
+}
+
 template <typename T, int D>
 TcFn pick_rows(bool splitq, bool rows16) {
   if (splitq) return rows16 ? decode_tc_kernel<T, D, true, true> : decode_tc_kernel<T, D, true, false>;
@@ -1163,7 +1179,8 @@ int plan_decode(const int32_t* nk, const int32_t* row, int64_t nq, int page_size
 }
 
 
-static_assert(sizeof(TcParams) <= sizeof(RecordedOp::args), "graph recorder argument buffer too small");
+static_assert(sizeof(TcParams) + sizeof(ClusterInline) + 16 <= sizeof(RecordedOp::args),
+              "graph recorder argument buffer too small");
 int launch_decode_tc(TcParams p, const int32_t* plan_host, int kv_dtype, int head_dim, int num_sms,
                      cudaStream_t stream) {
   const bool splitq = p.q_dtype == PKV_F32;
@@ -1175,20 +1192,29 @@ int launch_decode_tc(TcParams p, const int32_t* plan_host, int kv_dtype, int hea
   else
     fn = head_dim == 64 ? pick_rows<__half, 64>(splitq, rows16) : pick_rows<__half, 128>(splitq, rows16);
   const int merge_bytes = kWarpsTc * kMergeRows * head_dim * 4 + kWarpsTc * kMergeRows * 2 * 4;
-  p.cl_inline = 0;
-  if (plan_host[H_CLUSTER] > 1 && p.nq <= 64) {  // the cluster plan fits the launch parameters
-    p.cl_inline = 1;
-    p.cl_hb = plan_host[H_HB];
-    p.cl_wph = plan_host[H_WPH];
-    p.cl_qgs = plan_host[H_QGS];
-    p.cl_qgroups = plan_host[H_QGROUPS];
-    p.cl_head_items = plan_host[H_HEAD_ITEMS];
-    p.cl_cluster = plan_host[H_CLUSTER];
+  // cluster mode with <= 64 queries: the plan-in-parameters instantiation
+  const bool inline_plan = plan_host[H_CLUSTER] > 1 && p.nq <= 64;
+  ClusterInline ci{};
+  TcClusterFn fnc = nullptr;
+  if (inline_plan) {
+    ci.hb = plan_host[H_HB];
+    ci.wph = plan_host[H_WPH];
+    ci.qgs = plan_host[H_QGS];
+    ci.qgroups = plan_host[H_QGROUPS];
+    ci.head_items = plan_host[H_HEAD_ITEMS];
+    ci.cluster = plan_host[H_CLUSTER];
     for (int i = 0; i < p.nq; ++i) {
-      p.cl_nkrow[i] = plan_host[o_nk(p.nq) + i];
-      p.cl_nkrow[p.nq + i] = plan_host[o_row(p.nq) + i];
+      ci.nkrow[i] = plan_host[o_nk(p.nq) + i];
+      ci.nkrow[p.nq + i] = plan_host[o_row(p.nq) + i];
     }
+    if (kv_dtype == PKV_BF16)
+      fnc = head_dim == 64 ? pick_rows_cluster<__nv_bfloat16, 64>(splitq, rows16)
+                           : pick_rows_cluster<__nv_bfloat16, 128>(splitq, rows16);
+    else
+      fnc = head_dim == 64 ? pick_rows_cluster<__half, 64>(splitq, rows16)
+                           : pick_rows_cluster<__half, 128>(splitq, rows16);
   }
+  const void* fn_any = inline_plan ? reinterpret_cast<const void*>(fnc) : reinterpret_cast<const void*>(fn);
   const int64_t plan_bytes = o_cta(p.nq) * 4;
   p.plan_in_smem = p.nq <= kSmemPlanMax;
   p.merge_offset = p.plan_in_smem ? static_cast<int>((plan_bytes + 127) / 128 * 128) : 0;
@@ -1196,7 +1222,7 @@ int launch_decode_tc(TcParams p, const int32_t* plan_host, int kv_dtype, int hea
   const int smem = p.ring_offset + kWarpsTc * kStagesTc * 2 * kCh * head_dim * 2;
   const int key = (kv_dtype == PKV_BF16) * 8 + (head_dim == 128) * 4 + splitq * 2 + rows16;
   {
-    const cudaError_t e = ensure_smem(reinterpret_cast<const void*>(fn), smem);
+    const cudaError_t e = ensure_smem(fn_any, smem);
     if (e != cudaSuccess)
       return fail(PKV_CUDA_ERROR, "decode_tc smem attribute (%d B): %s", smem, pkv::cuda_err_str(e));
   }
@@ -1204,15 +1230,20 @@ int launch_decode_tc(TcParams p, const int32_t* plan_host, int kv_dtype, int hea
   const int cluster = plan_host[H_CLUSTER];
   cudaError_t e;
   if (cluster > 1) {
-    static bool nonportable[16] = {false};
-    if (!nonportable[key]) {
-      cudaFuncSetAttribute(reinterpret_cast<const void*>(fn), cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-      nonportable[key] = true;
+    static bool nonportable[32] = {false};
+    const int k2 = key + 16 * inline_plan;
+    if (!nonportable[k2]) {
+      cudaFuncSetAttribute(fn_any, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+      nonportable[k2] = true;
     }
   }
   if (launch_recorder()) {  // CUDA-graph mode of the batched step
-    record_kernel(fn, dim3(static_cast<unsigned>(grid)), dim3(kThreadsTc), static_cast<unsigned>(smem),
-                  static_cast<unsigned>(cluster), p);
+    if (inline_plan)
+      record_kernel(fnc, dim3(static_cast<unsigned>(grid)), dim3(kThreadsTc), static_cast<unsigned>(smem),
+                    static_cast<unsigned>(cluster), p, ci);
+    else
+      record_kernel(fn, dim3(static_cast<unsigned>(grid)), dim3(kThreadsTc), static_cast<unsigned>(smem),
+                    static_cast<unsigned>(cluster), p);
     return PKV_OK;
   }
   if (cluster > 1) {
@@ -1231,11 +1262,11 @@ int launch_decode_tc(TcParams p, const int32_t* plan_host, int kv_dtype, int hea
     static const bool debug_cluster = std::getenv("PKV_DEBUG_CLUSTER") != nullptr;
     if (debug_cluster) {
       int n = -1;
-      cudaError_t oe = cudaOccupancyMaxActiveClusters(&n, fn, &cfg);
+      cudaError_t oe = cudaOccupancyMaxActiveClusters(&n, fn_any, &cfg);
       std::fprintf(stderr, "pkv: cluster %d grid %d smem %d -> max active clusters %d (%s)\n", cluster, grid, smem,
                    n, cudaGetErrorString(oe));
     }
-    e = cudaLaunchKernelEx(&cfg, fn, p);
+    e = inline_plan ? cudaLaunchKernelEx(&cfg, fnc, p, ci) : cudaLaunchKernelEx(&cfg, fn, p);
   } else {
     fn<<<grid, kThreadsTc, smem, stream>>>(p);
     e = cudaGetLastError();

@@ -34,11 +34,14 @@ struct TcParams {
   int merge_offset;
   int ring_offset;
   int kv_dtype;
-  // cluster mode with few queries: the plan is carried in the launch
-  // parameters (no dependent plan loads before the first block-table read)
-  int cl_inline;
-  int cl_hb, cl_wph, cl_qgs, cl_qgroups, cl_head_items, cl_cluster;
-  int32_t cl_nkrow[2 * 64];  // nk[nq] | row[nq]
+};
+
+// cluster mode with few queries: the plan rides in a second launch parameter
+// of a separate kernel instantiation (no dependent plan loads before the
+// first block-table read; the other instantiations keep the small TcParams)
+struct ClusterInline {
+  int hb, wph, qgs, qgroups, head_items, cluster;
+  int32_t nkrow[2 * 64];  // nk[nq] | row[nq]
 };
 
 using TcFn = void (*)(TcParams);
