@@ -291,7 +291,10 @@ __global__ void __launch_bounds__(kThreads, 1)
   // row rescales: PV_t(u + 2), the next completion on a barrier, cannot be
   // issued before the softmax publishes P_t(u + 2), so a later wait never
   // sees a barrier two phases ahead
-  enum { B_Q = 0, B_KF = 1, B_VF = 3, B_KE = 5, B_VE = 7, B_SF = 9, B_PF = 13, B_OD = 17, B_N = 21 };
+  // KE / VE: [issuer (query tile) t][stage s] at + 2t + s: tile t's MMAs no
+  // longer read that stage (each issuer releases only the K / V tiles its
+  // query tile uses; the producer waits for the tiles' users)
+  enum { B_Q = 0, B_KF = 1, B_VF = 3, B_KE = 5, B_VE = 9, B_SF = 13, B_PF = 17, B_OD = 21, B_N = 25 };
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + B_N);
   auto bar = [&](int i) { return smem_addr(bars + i); };
 
@@ -304,7 +307,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int nt[2] = {it[7], it[8]};
   const int n_tiles = max(nt[0], nt[1]);
   const int nu[2] = {2 * nt[0], 2 * nt[1]};
-  const int nu_max = 2 * n_tiles;
+  const int n_issuers = nt[1] > 0 ? 2 : 1;  // tile A always has work
 
   if (p.dbg && threadIdx.x == 0) {  // per-CTA record: start, first S, end, SM
     p.dbg[512 + 4 * blockIdx.x] = gtime();
@@ -317,10 +320,10 @@ __global__ void __launch_bounds__(kThreads, 1)
     for (int s = 0; s < 2; ++s) {
       mbar_init(bar(B_KF + s), 1);
       mbar_init(bar(B_VF + s), 1);
-      mbar_init(bar(B_KE + s), 1);
-      mbar_init(bar(B_VE + s), 1);
     }
     for (int s = 0; s < 4; ++s) {
+      mbar_init(bar(B_KE + s), 1);
+      mbar_init(bar(B_VE + s), 1);
       mbar_init(bar(B_SF + s), 1);
       mbar_init(bar(B_PF + s), 128);
       mbar_init(bar(B_OD + s), 1);
@@ -370,13 +373,18 @@ __global__ void __launch_bounds__(kThreads, 1)
         const CUtensorMap* mk = run ? &tm_k128 : &tm_k;
         const CUtensorMap* mv = run ? &tm_v128 : &tm_v;
         const int nb = run ? 1 : boxes;
-        if (j >= 2) mbar_wait(bar(B_KE + st), ((j >> 1) - 1) & 1);
+        // stage st last held tile j - 2: wait for the query tiles that read it
+        if (j >= 2)
+          for (int t = 0; t < 2; ++t)
+            if (j - 2 < nt[t]) mbar_wait(bar(B_KE + 2 * t + st), ((j >> 1) - 1) & 1);
         mbar_expect_tx(bar(B_KF + st), kKVBytes);
         for (int b = 0; b < nb; ++b)
           for (int c = 0; c < NCH; ++c)
             tma_load_3d(sK + st * kKVBytes + c * kChunkB + b * p.box_rows * kRowB, mk, bar(B_KF + st), c * 64, kvh,
                         rows[b]);
-        if (j >= 2) mbar_wait(bar(B_VE + st), ((j >> 1) - 1) & 1);
+        if (j >= 2)
+          for (int t = 0; t < 2; ++t)
+            if (j - 2 < nt[t]) mbar_wait(bar(B_VE + 2 * t + st), ((j >> 1) - 1) & 1);
         mbar_expect_tx(bar(B_VF + st), kKVBytes);
         for (int b = 0; b < nb; ++b)
           for (int c = 0; c < NCH; ++c)
@@ -384,8 +392,11 @@ __global__ void __launch_bounds__(kThreads, 1)
                         rows[b]);
       }
     }
-  } else if (warp == 1) {
-    // ---------------- MMA issuer ----------------
+  } else if (warp == 1 || (warp == 3 && n_issuers == 2)) {
+    // ---------------- MMA issuers: warp 1 for query tile A, warp 3 for B ----------------
+    // one issuing warp per query tile: a tile's PV / QK never queue behind the
+    // other tile's softmax; K / V stages are released by both issuers
+    const int t = warp == 1 ? 0 : 1;
     const uint32_t uQ = __shfl_sync(0xffffffffu, sQ, 0), uK = __shfl_sync(0xffffffffu, sK, 0);
     const uint32_t uV = __shfl_sync(0xffffffffu, sV, 0), uT = __shfl_sync(0xffffffffu, tmem, 0);
     mbar_wait(bar(B_Q), 0);
@@ -432,23 +443,16 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       tc_commit_elect(bar(B_OD + 2 * t + h));
     };
-    for (int t = 0; t < 2; ++t)
-      for (int u = 0; u < 2; ++u)
-        if (u < nu[t]) issue_qk(t, u);
-    if (n_tiles > 0) tc_commit_elect(bar(B_KE + 0));  // K tile 0: both halves, both query tiles
-    for (int u = 0; u < nu_max; ++u) {
-      for (int t = 0; t < 2; ++t) {
-        if (u < nu[t]) {
-          issue_pv(t, u);
-          if (u + 2 < nu[t]) issue_qk(t, u + 2);
-        }
-      }
-      // V tile u >> 1 fully read once its second half was issued for both tiles;
-      // K tile (u + 2) >> 1 fully read once both its halves were issued
-      if (u & 1) {
-        tc_commit_elect(bar(B_VE + ((u >> 1) & 1)));
-        const int jk = (u + 1) >> 1;  // QK(u + 2) for odd u completes K tile (u + 1) / 2
-        if (jk < n_tiles) tc_commit_elect(bar(B_KE + (jk & 1)));
+    // this tile's sub-tiles: nu[t] = 2 nt[t] (even); K tile j is read by
+    // QK(2j), QK(2j + 1), V tile j by PV(2j), PV(2j + 1)
+    for (int u = 0; u < 2 && u < nu[t]; ++u) issue_qk(t, u);
+    tc_commit_elect(bar(B_KE + 2 * t + 0));  // K tile 0 read (nt[t] >= 1)
+    for (int u = 0; u < nu[t]; ++u) {
+      issue_pv(t, u);
+      if (u & 1) tc_commit_elect(bar(B_VE + 2 * t + ((u >> 1) & 1)));  // V tile u >> 1 read
+      if (u + 2 < nu[t]) {
+        issue_qk(t, u + 2);
+        if (u & 1) tc_commit_elect(bar(B_KE + 2 * t + (((u + 2) >> 1) & 1)));  // K tile (u + 2) >> 1 read
       }
     }
   } else if (warp >= 4) {
@@ -735,7 +739,7 @@ template <typename T, int D>
 size_t smem_bytes() {
   constexpr int NCH = D / 64;
   // at least 116 KB: one CTA per SM, so the 512-column TMEM allocation never waits
-  return std::max<size_t>(1024 + NCH * kChunkB * 6 + 22 * 8 + 16, 116 * 1024);
+  return std::max<size_t>(1024 + NCH * kChunkB * 6 + 26 * 8 + 16, 116 * 1024);
 }
 
 template <typename T, int D>
