@@ -21,8 +21,8 @@
 //   warp 0     TMA producer: Q (two query tiles) once, then 128-key K/V tiles
 //              through a 2-stage ring (a tile whose pages form one contiguous
 //              run is one 128-row box per chunk);
-//   warp 1     MMA issuer (one elected lane): QK of 64-key sub-tiles into
-//              double-buffered S, PV from P in TMEM;
+//   warps 1, 3 MMA issuers (one elected lane each), one per query tile: QK
+//              of 64-key sub-tiles into double-buffered S, PV from P in TMEM;
 //   warp 2     TMEM allocator (512 columns: S_A[2], S_B[2], O_A, O_B);
 //   warps 4-11 two softmax + epilogue warpgroups, one per query tile: thread
 //              = query row (TMEM lane), so row max / sum need no shuffles.
