@@ -329,6 +329,12 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(bar(B_OD + s), 1);
     }
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    // Q goes out right away, overlapping the TMEM allocation and the barrier
+    const int ntiles_q = cnt[1] > 0 ? 2 : 1;
+    mbar_expect_tx(bar(B_Q), kQBytes * ntiles_q);
+    for (int t = 0; t < ntiles_q; ++t)
+      for (int c = 0; c < NCH; ++c)
+        tma_load_3d(sQ + t * kQBytes + c * kChunkB, &tm_q, bar(B_Q), c * 64, kvh * p.group, q_row0 + t * p.qt);
   }
   if (warp == 2) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(
@@ -347,11 +353,6 @@ __global__ void __launch_bounds__(kThreads, 1)
       // ---------------- TMA producer (128-key K/V tiles, 2 stages) ----------------
       asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<uint64_t>(&tm_k)) : "memory");
       asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<uint64_t>(&tm_v)) : "memory");
-      const int ntiles_q = cnt[1] > 0 ? 2 : 1;
-      mbar_expect_tx(bar(B_Q), kQBytes * ntiles_q);
-      for (int t = 0; t < ntiles_q; ++t)
-        for (int c = 0; c < NCH; ++c)
-          tma_load_3d(sQ + t * kQBytes + c * kChunkB, &tm_q, bar(B_Q), c * 64, kvh * p.group, q_row0 + t * p.qt);
       const int ps = 1 << p.log2ps;
       const int n_pages = (kv_len + ps - 1) >> p.log2ps;
       const int boxes = kN / p.box_rows;
