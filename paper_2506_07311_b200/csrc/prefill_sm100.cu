@@ -58,6 +58,18 @@ constexpr int kChunkB = kM * kRowB;  // one 64-column chunk of a 128-row tile: 1
 constexpr int kItemInts = 10;
 constexpr float kLog2eP = 1.4426950408889634f;
 constexpr float kRescaleThreshold = 8.0f;  // log2 units
+#ifndef PKV_K3_EMU
+#define PKV_K3_EMU 1
+#endif
+#ifndef PKV_K3_EMU_PERIOD
+#define PKV_K3_EMU_PERIOD 16
+#endif
+// of every kEmuPeriod packed pairs of scores, how many take the FMA-pipe
+// exp2 below instead of MUFU.EX2 (16 / clk / SM, the softmax's bound once
+// both query tiles' softmaxes run concurrently; period over the 32 pairs
+// of a 64-key sub-tile row)
+constexpr int kEmuPairs = PKV_K3_EMU;
+constexpr int kEmuPeriod = PKV_K3_EMU_PERIOD;
 
 // ---- PTX wrappers -----------------------------------------------------------
 __device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
@@ -221,6 +233,25 @@ __device__ __forceinline__ unsigned long long gtime() {
   do {             \
     if (p.dbg && blockIdx.x == 0) p.dbg[slot] = gtime(); \
   } while (0)
+
+// 2^x on the FMA pipe for two lanes: x = i + f with i = round(x) (the
+// 1.5 * 2^23 magic add leaves i in the low mantissa bits), 2^f by a degree-3
+// polynomial on [-0.5, 0.5] (max relative error 1.0e-4, below the 2^-9 of
+// the 16-bit P it feeds), then i is added to the exponent field.  x is
+// clamped to >= -125 so the exponent stays normal (2^-125 ~ 0 next to the
+// row maximum's 1; masked -inf scores land there too).
+__device__ __forceinline__ float2 ex2_emu2(float2 x) {
+  x.x = fmaxf(x.x, -125.f);
+  x.y = fmaxf(x.y, -125.f);
+  const float2 j = fadd2(x, make_float2(12582912.f, 12582912.f));
+  const float2 i = fadd2(j, make_float2(-12582912.f, -12582912.f));
+  const float2 f = ffma2(i, make_float2(-1.f, -1.f), x);
+  float2 pv = ffma2(f, make_float2(0.05500882f, 0.05500882f), make_float2(0.24221077f, 0.24221077f));
+  pv = ffma2(pv, f, make_float2(0.69328291f, 0.69328291f));
+  pv = ffma2(pv, f, make_float2(1.f, 1.f));
+  return make_float2(__int_as_float(__float_as_int(pv.x) + (__float_as_int(j.x) << 23)),
+                     __int_as_float(__float_as_int(pv.y) + (__float_as_int(j.y) << 23)));
+}
 
 template <typename T>
 struct Fmt;
@@ -522,7 +553,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int e = 0; e < 32; e += 2) {
           const float2 x = make_float2(__uint_as_float(v[32 * c + e]), __uint_as_float(v[32 * c + e + 1]));
           const float2 tt = ffma2(x, qs2, negm2);
-          const float2 pp = make_float2(ex2_ftz(tt.x), ex2_ftz(tt.y));
+          const float2 pp =
+              ((c * 16 + (e >> 1)) % kEmuPeriod) < kEmuPairs ? ex2_emu2(tt)
+                                                             : make_float2(ex2_ftz(tt.x), ex2_ftz(tt.y));
           l2[(e >> 1) & 3] = fadd2(l2[(e >> 1) & 3], pp);
           pk[e >> 1] = pack2<T>(pp.x, pp.y);
         }
