@@ -254,3 +254,21 @@ def test_fragmented_and_contiguous_page_runs_in_one_prefill(ps):
     assert torch.equal(paged, gathered_attention(q, gk, gv, meta, cfg, precision="prefill"))
     ref = dense_prefill_f64(q, ks, vs, lengths, lengths, hq // hkv, cfg.scale)
     assert relative_error(as_numpy(paged), ref.cpu().numpy()) <= 6e-3
+
+
+@pytest.mark.parametrize("out_dtype", [torch.float32, torch.bfloat16])
+@pytest.mark.parametrize("d", [64, 128])
+def test_tma_store_and_register_store_epilogues(out_dtype, d):
+    """Full query tiles leave K3 by TMA stores staged in shared memory,
+    partial tiles (a prompt length that is not a multiple of the tile) by
+    register stores: both, in fp32 and bf16 output, against float64."""
+    lengths = [700, 333, 64]  # 700 / 32 and 333 / 32 leave partial tiles (G = 4: 32 positions per tile)
+    pool, store, ks, vs = build(lengths, 8, d, 16, torch.bfloat16, seed=d)
+    cfg = AttentionConfig(head_count=32, head_dim=d, page_size=16, kv_head_count=8)
+    meta = MaskMeta.self_attention(store.batch_view([0, 1, 2]))
+    gen = torch.Generator(device="cuda").manual_seed(d)
+    q = torch.randn((meta.query_count, 32, d), generator=gen, device="cuda").bfloat16()
+    out = paged_attention(q, store, meta, cfg, precision="prefill", out_dtype=out_dtype)
+    assert out.dtype == out_dtype
+    ref = dense_prefill_f64(q, ks, vs, lengths, lengths, 4, cfg.scale)
+    assert relative_error(as_numpy(out.float()), ref.cpu().numpy()) <= (6e-3 if out_dtype == torch.float32 else 1e-2)
