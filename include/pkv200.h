@@ -142,6 +142,14 @@ int pkv_pool_mirror_row(pkv_pool* pool, int64_t seq, int32_t* row_out);
 int pkv_pool_assign_prepare(pkv_pool* pool, int64_t seq, const int64_t* positions, int64_t n,
                             int64_t* info_out, int64_t* copies_out, int64_t copies_cap, int64_t* n_copies_out);
 
+/* mutation counter of the pool: every call that can change a block table,
+ * the page state or the mirror (reserve, grow, free, fork, privatize, assign
+ * preparation, decode-step staging and its rollback, entry / logical-length
+ * setters) bumps it.  Two equal reads bracket no such call, so a caller may
+ * reuse what it derived from the tables in between (the prefill fast path of
+ * paged_attention).  No reference counterpart (an engine-side memo key). */
+int pkv_pool_generation(pkv_pool* pool, uint64_t* out);
+
 /* batched table query for n sequence handles: page count and mirror row of
  * each (either output may be NULL); one call instead of two per sequence */
 int pkv_pool_tables_info(pkv_pool* pool, const int64_t* seqs, int64_t n, int64_t* n_pages_out,
@@ -195,6 +203,19 @@ int pkv_kv_append(const void* k_new, const void* v_new, int64_t n_tok, const int
 int pkv_kv_append_range(const void* k_new, const void* v_new, int64_t n_tok, int32_t seq_row, int32_t pos0,
                         const int32_t* block_table, int64_t bt_stride, int32_t page_size, void* k_cache,
                         void* v_cache, int64_t row_bytes, void* stream);
+
+/* KvStore.assign in one call (store.py:117-150) for the common case:
+ * pkv_pool_assign_prepare (info_out / copies_out / n_copies_out exactly as
+ * there), then — when the positions form one in-range contiguous run, no
+ * block needed copy-on-write, the pool's device mirror has no pending cells
+ * and block_table (that mirror, on the stream's device) is given — the K1
+ * range launch and the logical-length update (max(len, last position + 1)).
+ * *launched_out = 1 when it launched; 0 leaves the caller to finish the
+ * assign from info_out (the preparation is never repeated). */
+int pkv_kv_assign(pkv_pool* pool, int64_t seq, const int64_t* positions, int64_t n, int64_t* info_out,
+                  int64_t* copies_out, int64_t copies_cap, int64_t* n_copies_out, const void* k_new,
+                  const void* v_new, const int32_t* block_table, int64_t bt_stride, int32_t page_size,
+                  void* k_cache, void* v_cache, int64_t row_bytes, void* stream, int32_t* launched_out);
 
 /* K-gather: contiguous copies of paged rows — KvStore.gather / gather_view
  * (store.py:152-161, 187-190).  For view sequence s (s < n_seq) with block

@@ -111,6 +111,9 @@ SIGNATURES = {
     "pkv_pool_census": (C.c_int, [_vp, _P(_i64)]),
     "pkv_pool_free_stack": (C.c_int, [_vp, _P(_u32), _i64, _P(_i64)]),
     "pkv_pool_tables_info": (C.c_int, [_vp, _vp, _i64, _vp, _vp]),
+    "pkv_pool_generation": (C.c_int, [_vp, _vp]),
+    "pkv_kv_assign": (C.c_int, [_vp, _i64, _vp, _i64, _vp, _vp, _i64, _vp, _vp, _vp, _vp, _i64, _i32, _vp, _vp,
+                                _i64, _vp, _vp]),
     "pkv_pool_assign_prepare": (C.c_int, [_vp, _i64, _vp, _i64, _vp, _vp, _i64, _vp]),
     "pkv_prefill_plan_meta": (C.c_int, [_vp, _vp, _i64, _vp, _vp, _i64, _i32, _i32, _i32, _i32, _vp, _i64,
                                         _vp, _vp, _vp]),

@@ -801,6 +801,33 @@ int pkv_kv_append_range(const void* k_new, const void* v_new, int64_t n_tok, int
   return PKV_OK;
 }
 
+int pkv_kv_assign(pkv_pool* pool, int64_t seq, const int64_t* positions, int64_t n, int64_t* info_out,
+                  int64_t* copies_out, int64_t copies_cap, int64_t* n_copies_out, const void* k_new,
+                  const void* v_new, const int32_t* block_table, int64_t bt_stride, int32_t page_size,
+                  void* k_cache, void* v_cache, int64_t row_bytes, void* stream, int32_t* launched_out) {
+  if (!launched_out) return pkv::fail(PKV_VALUE_ERROR, "bad assign inputs");
+  *launched_out = 0;
+  int st = pkv_pool_assign_prepare(pool, seq, positions, n, info_out, copies_out, copies_cap, n_copies_out);
+  if (st || n <= 0 || !block_table) return st;
+  const int64_t want = PKV_ASSIGN_INCREASING | PKV_ASSIGN_CONTIGUOUS;
+  if (info_out[2] != want || *n_copies_out != 0) return PKV_OK;
+  int64_t pending = 0;
+  int32_t full = 0;
+  st = pkv_pool_mirror_pending(pool, &pending, &full);
+  if (st || pending || full) return st;  // the caller brings the mirror up to date first
+  if (info_out[0] >= (int64_t(1) << 31)) return PKV_OK;
+  st = pkv_kv_append_range(k_new, v_new, n, static_cast<int32_t>(info_out[4]), static_cast<int32_t>(info_out[0]),
+                           block_table, bt_stride, page_size, k_cache, v_cache, row_bytes,
+                           stream);
+  if (st) return st;
+  *launched_out = 1;
+  int64_t len = 0;
+  st = pkv_pool_get_logical_len(pool, seq, &len);
+  if (st) return st;
+  if (info_out[1] + 1 > len) st = pkv_pool_set_logical_len(pool, seq, info_out[1] + 1);
+  return st;
+}
+
 int pkv_kv_gather(const void* k_cache, const void* v_cache, const int32_t* block_table, int64_t bt_stride,
                   const int32_t* seq_row, const int32_t* cu_rows, int64_t n_seq, int64_t n_rows,
                   int32_t page_size, int64_t row_bytes, void* k_out, void* v_out, void* stream) {

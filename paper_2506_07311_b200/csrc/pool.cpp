@@ -15,6 +15,7 @@
 #include <cstdint>
 #include <cstring>
 #include <memory>
+#include <atomic>
 #include <mutex>
 #include <string>
 #include <unordered_map>
@@ -44,6 +45,10 @@ inline int64_t floordiv(int64_t a, int64_t b) {
 
 struct pkv_pool {
   std::mutex mu;
+  // bumped by every entry point that can change a table, the page state or
+  // the mirror's contents: equal values across two reads mean no such call
+  // ran in between (the attention entry points' memo check)
+  std::atomic<uint64_t> generation{0};
   uint64_t capacity = 0;
   uint32_t page_size = 0;
   std::vector<uint32_t> free_stack;  // back() is the top (deque.pop())
@@ -192,6 +197,11 @@ void copy_out(const std::vector<uint32_t>& v, uint32_t* out, int64_t* n) {
   if (!(p)) return pkv::fail(PKV_VALUE_ERROR, "null pool handle");     \
   std::lock_guard<std::mutex> _guard((p)->mu)
 
+// LOCK for the mutating entry points
+#define LOCK_MUT(p) \
+  LOCK(p);          \
+  (p)->generation.fetch_add(1, std::memory_order_relaxed)
+
 #define TABLE_OR_FAIL(t, p, seq)                                                      \
   Table* t = (p)->find(seq);                                                          \
   if (!t) return pkv::fail(PKV_UNKNOWN_SEQUENCE, "no block table for sequence %lld", \
@@ -245,7 +255,7 @@ void pkv_pool_destroy(pkv_pool* pool) { delete pool; }
 
 int pkv_pool_reserve(pkv_pool* pool, int64_t seq, int64_t length, uint32_t* pages_out,
                      int64_t* n_out) {
-  LOCK(pool);
+  LOCK_MUT(pool);
   if (n_out) *n_out = 0;
   if (length < 0) return pkv::fail(PKV_VALUE_ERROR, "length must be non-negative, got %lld",
                                    static_cast<long long>(length));
@@ -269,7 +279,7 @@ int pkv_pool_reserve(pkv_pool* pool, int64_t seq, int64_t length, uint32_t* page
 
 int pkv_pool_grow(pkv_pool* pool, int64_t seq, int64_t new_len, uint32_t* pages_out,
                   int64_t* n_out) {
-  LOCK(pool);
+  LOCK_MUT(pool);
   if (n_out) *n_out = 0;
   TABLE_OR_FAIL(t, pool, seq);
   int64_t needed = pool->pages_for(new_len) - static_cast<int64_t>(t->entries.size());
@@ -287,7 +297,7 @@ int pkv_pool_grow(pkv_pool* pool, int64_t seq, int64_t new_len, uint32_t* pages_
 }
 
 int pkv_pool_free(pkv_pool* pool, int64_t seq, int64_t* reclaimed_out) {
-  LOCK(pool);
+  LOCK_MUT(pool);
   if (reclaimed_out) *reclaimed_out = 0;
   TABLE_OR_FAIL(t, pool, seq);
   std::vector<uint32_t> pages = std::move(t->entries);
@@ -300,7 +310,7 @@ int pkv_pool_free(pkv_pool* pool, int64_t seq, int64_t* reclaimed_out) {
 
 int pkv_pool_fork(pkv_pool* pool, int64_t parent, int64_t child, int64_t prefix_len,
                   int64_t* copy_src, int64_t* copy_dst, int64_t* copy_rows) {
-  LOCK(pool);
+  LOCK_MUT(pool);
   if (copy_src) *copy_src = -1;
   if (copy_dst) *copy_dst = -1;
   if (copy_rows) *copy_rows = 0;
@@ -355,7 +365,7 @@ int pkv_pool_fork(pkv_pool* pool, int64_t parent, int64_t child, int64_t prefix_
 
 int pkv_pool_privatize(pkv_pool* pool, int64_t seq, int64_t block_idx, int64_t* old_page,
                        int64_t* new_page) {
-  LOCK(pool);
+  LOCK_MUT(pool);
   if (old_page) *old_page = -1;
   if (new_page) *new_page = -1;
   TABLE_OR_FAIL(t, pool, seq);
@@ -400,7 +410,7 @@ int pkv_pool_assign_prepare(pkv_pool* pool, int64_t seq, const int64_t* position
     }
   }
   const bool increasing = steps_down == 0;
-  LOCK(pool);
+  LOCK(pool);  // a read unless it privatizes blocks below
   TABLE_OR_FAIL(t, pool, seq);
   const int64_t ps = static_cast<int64_t>(pool->page_size);
   const int64_t n_pages = static_cast<int64_t>(t->entries.size());
@@ -416,6 +426,7 @@ int pkv_pool_assign_prepare(pkv_pool* pool, int64_t seq, const int64_t* position
   info_out[4] = t->mirror_row;
   // no page of the pool is shared: nothing to copy-on-write
   if (!in_range || !increasing || n == 0 || pool->shared == 0) return PKV_OK;
+  pool->generation.fetch_add(1, std::memory_order_relaxed);
   // touched blocks, ascending and distinct (the positions increase): a
   // contiguous run walks its block range, otherwise every position's block
   // (a shift for the power-of-two page sizes: no per-position division)
@@ -473,7 +484,7 @@ int pkv_pool_prepare_append_undo(pkv_pool* pool, const int64_t* seqs, int64_t n,
                                  int32_t* rows_out, uint32_t* pages_out, int64_t pages_cap,
                                  int64_t* n_pages_out, int64_t* copies_out, pkv_append_undo** undo_out) {
   if (undo_out) *undo_out = nullptr;
-  LOCK(pool);
+  LOCK_MUT(pool);
   *n_pages_out = 0;
   const int64_t ps = pool->page_size;
   // phase 1: validate and count pages without mutating
@@ -568,7 +579,7 @@ int pkv_pool_prepare_append_undo(pkv_pool* pool, const int64_t* seqs, int64_t n,
 int pkv_pool_rollback_append(pkv_pool* pool, pkv_append_undo* undo) {
   if (!undo) return PKV_OK;
   std::unique_ptr<pkv_append_undo> hold(undo);
-  LOCK(pool);
+  LOCK_MUT(pool);
   for (auto it = undo->seqs.rbegin(); it != undo->seqs.rend(); ++it) {
     Table* t = pool->find(it->handle);
     if (!t) return pkv::fail(PKV_UNKNOWN_SEQUENCE, "rollback: table %lld vanished", static_cast<long long>(it->handle));
@@ -634,7 +645,7 @@ int pkv_pool_table_entries(pkv_pool* pool, int64_t seq, uint32_t* out, int64_t c
 }
 
 int pkv_pool_table_set_entry(pkv_pool* pool, int64_t seq, int64_t idx, uint32_t value) {
-  LOCK(pool);
+  LOCK_MUT(pool);
   TABLE_OR_FAIL(t, pool, seq);
   const int64_t n = static_cast<int64_t>(t->entries.size());
   if (idx < 0) idx += n;
@@ -652,7 +663,7 @@ int pkv_pool_get_logical_len(pkv_pool* pool, int64_t seq, int64_t* out) {
 }
 
 int pkv_pool_set_logical_len(pkv_pool* pool, int64_t seq, int64_t value) {
-  LOCK(pool);
+  LOCK_MUT(pool);
   TABLE_OR_FAIL(t, pool, seq);
   t->logical_len = value;
   return PKV_OK;
@@ -700,6 +711,12 @@ int pkv_pool_free_stack(pkv_pool* pool, uint32_t* out, int64_t cap, int64_t* n_o
     if (cap < *n_out) return pkv::fail(PKV_VALUE_ERROR, "output buffer too small");
     copy_out(pool->free_stack, out, nullptr);
   }
+  return PKV_OK;
+}
+
+int pkv_pool_generation(pkv_pool* pool, uint64_t* out) {
+  if (!pool) return pkv::fail(PKV_VALUE_ERROR, "null pool handle");
+  *out = pool->generation.load(std::memory_order_relaxed);
   return PKV_OK;
 }
 

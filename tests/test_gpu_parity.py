@@ -481,3 +481,57 @@ def test_gather_kernel_bit_exact(dtype, heads, dim, ps):
         assert torch.equal(k1, store.k_cache.index_select(0, r1)) and torch.equal(v1, store.v_cache.index_select(0, r1))
     with pytest.raises(OutOfRange):
         store.gather(2, ps + 1)
+
+
+def test_one_call_assign_path_and_its_fallbacks(monkeypatch):
+    """KvStore.assign's one-call path (pkv_kv_assign: preparation + K1 range
+    launch + logical length) runs for an in-range contiguous run over a
+    current mirror; a pending mirror, copy-on-write or a non-contiguous run
+    finish through the full path.  Every case bit-exact against numpy."""
+    rng = np.random.default_rng(21)
+    pool = PagePool(64, page_size=16)
+    store = KvStore(pool, 2, 8)
+    want = {}
+
+    def put(seq, pos, scale=1.0):
+        pos = np.asarray(pos)
+        k = (rng.standard_normal((pos.size, 2, 8)) * scale).astype(np.float32)
+        v = (rng.standard_normal((pos.size, 2, 8)) * scale).astype(np.float32)
+        store.assign(seq, pos, k, v)
+        kk, vv = want.setdefault(seq, (np.zeros((64, 2, 8), np.float32), np.zeros((64, 2, 8), np.float32)))
+        kk[pos], vv[pos] = k, v
+
+    calls = {"n": 0}
+    real = pool.device_table
+
+    def counting(device):
+        calls["n"] += 1
+        return real(device)
+
+    monkeypatch.setattr(pool, "device_table", counting)
+    pool.reserve("a", 64)
+    put("a", np.arange(20))  # mirror pending after the reserve: full path
+    assert calls["n"] == 1 and pool.table("a").logical_len == 20
+    put("a", np.arange(20, 50))  # one call
+    put("a", np.arange(5, 9))  # overwrite inside the run: one call, logical length stays
+    assert calls["n"] == 1 and pool.table("a").logical_len == 50
+    put("a", [50, 52, 51])  # not increasing: full path
+    assert calls["n"] == 2 and pool.table("a").logical_len == 53
+    pool.fork("a", "b", 40)  # shares pages 0-1, copies the partial third
+    put("b", np.arange(40, 48))  # fork left mirror cells pending: full path
+    put("b", np.arange(30, 34))  # shared page: copy-on-write through the full path
+    assert calls["n"] == 4
+    want["b"][0][:30] = want["a"][0][:30]
+    want["b"][1][:30] = want["a"][1][:30]
+    want["b"][0][34:40] = want["a"][0][34:40]
+    want["b"][1][34:40] = want["a"][1][34:40]
+    pool.grow("b", 64)
+    put("b", np.arange(48, 52))  # grant pending in the mirror: full path
+    put("b", np.arange(52, 56))  # back on the one-call path
+    assert calls["n"] == 5 and pool.table("b").logical_len == 56
+    with pytest.raises(OutOfRange):
+        put("b", np.arange(60, 70))
+    assert pool.table("b").logical_len == 56
+    for seq, n in (("a", 53), ("b", 56)):
+        gk, gv = store.gather(seq, n)
+        assert np.array_equal(as_numpy(gk), want[seq][0][:n]) and np.array_equal(as_numpy(gv), want[seq][1][:n])

@@ -272,3 +272,66 @@ def test_tma_store_and_register_store_epilogues(out_dtype, d):
     assert out.dtype == out_dtype
     ref = dense_prefill_f64(q, ks, vs, lengths, lengths, 4, cfg.scale)
     assert relative_error(as_numpy(out.float()), ref.cpu().numpy()) <= (6e-3 if out_dtype == torch.float32 else 1e-2)
+
+
+def test_repeat_call_fast_path_and_its_invalidation(monkeypatch):
+    """paged_attention's repeat-call path (attention._prefill_fast): the same
+    sealed meta / store / config again relaunches the prepared K3 argument
+    block — bitwise the full path's result, new q / out pointers honoured —
+    and any pool change, another plan in this thread's device buffer, a
+    corrupted view or an unsealed meta falls back to the full path."""
+    from paper_2506_07311_b200 import attention as A
+    from paper_2506_07311_b200.errors import NoAllowedKeys
+
+    hq, hkv, d, ps = 8, 2, 128, 16
+    lengths = [300, 129]
+    pool, store, ks, vs = build(lengths, hkv, d, ps, torch.bfloat16, seed=11)
+    cfg = AttentionConfig(head_count=hq, head_dim=d, page_size=ps, kv_head_count=hkv)
+    meta = MaskMeta.self_attention(store.batch_view([0, 1]))
+    assert not meta.q_seq.flags.writeable and not meta.q_pos.flags.writeable
+    gen = torch.Generator(device="cuda").manual_seed(3)
+    qs = [torch.randn((sum(lengths), hq, d), generator=gen, device="cuda").bfloat16() for _ in range(2)]
+    full = [paged_attention(q, store, meta, cfg).clone() for q in qs]  # second call may already be fast
+
+    calls = {"route": 0}
+    real_route = A._prefill_route
+
+    def counting_route(*a, **k):
+        calls["route"] += 1
+        return real_route(*a, **k)
+
+    monkeypatch.setattr(A, "_prefill_route", counting_route)
+    for i in range(4):  # alternate q tensors: every call on the fast path, each with its own q
+        out = paged_attention(qs[i % 2], store, meta, cfg)
+        assert torch.equal(out, full[i % 2])
+    assert calls["route"] == 0
+
+    # another meta's plan replaces this thread's device plan: full path, same result
+    other = MaskMeta.suffix(store.batch_view([0]), [40])
+    paged_attention(qs[0][:40], store, other, cfg)
+    before = calls["route"]
+    assert torch.equal(paged_attention(qs[0], store, meta, cfg), full[0])
+    assert calls["route"] == before + 1
+    assert torch.equal(paged_attention(qs[1], store, meta, cfg), full[1])
+    assert calls["route"] == before + 1  # fast again
+
+    # a pool mutation (unrelated sequence) bumps the generation: full path once
+    pool.reserve("other", 40)
+    assert torch.equal(paged_attention(qs[0], store, meta, cfg), full[0])
+    assert calls["route"] == before + 2
+    # the output dtype is part of the key
+    o16 = paged_attention(qs[0], store, meta, cfg, out_dtype=torch.bfloat16)
+    assert o16.dtype == torch.bfloat16 and calls["route"] == before + 3
+
+    # an unsealed meta with equal content never takes the fast path
+    loose = MaskMeta(view=meta.view, q_seq=meta.q_seq.copy(), q_pos=meta.q_pos.copy())
+    paged_attention(qs[0], store, loose, cfg)
+    paged_attention(qs[0], store, loose, cfg)
+    assert calls["route"] == before + 5
+
+    # corrupting the view in place (the reference suite does this) is seen
+    paged_attention(qs[0], store, meta, cfg)
+    meta.view.lengths[1] = 0
+    with pytest.raises((NoAllowedKeys, Exception)):
+        paged_attention(qs[0], store, meta, cfg)
+    meta.view.lengths[1] = lengths[1]
