@@ -27,6 +27,7 @@ def main():
     ap.add_argument("--hkv", type=int, default=8)
     ap.add_argument("--d", type=int, default=128)
     ap.add_argument("--batch", type=int, default=1)
+    ap.add_argument("--out", default="f32", choices=("f32", "bf16"), help="output dtype")
     ap.add_argument("--gathered", action="store_true",
                     help="experiment: contiguous K/V rows without the block table (one TMA box per 128 keys)")
     args = ap.parse_args()
@@ -47,7 +48,7 @@ def main():
             store.assign(b, np.arange(n), k[b * n:(b + 1) * n], v[b * n:(b + 1) * n])
         meta = MaskMeta.self_attention(store.batch_view(list(range(B))))
         q = torch.randn((B * n, hq, d), device=dev).bfloat16()
-        out = torch.empty((B * n, hq, d), device=dev, dtype=torch.float32)
+        out = torch.empty((B * n, hq, d), device=dev, dtype=torch.float32 if args.out == "f32" else torch.bfloat16)
         runs = suffix_runs(meta)
         rows = np.asarray([pool.table(b).mirror_row for b in range(B)], dtype=np.int32)
         if args.gathered:
@@ -63,7 +64,8 @@ def main():
                              cache_rows=store.keys.shape[0],
                              block_table=None if args.gathered else mirror.data_ptr(),
                              bt_stride=0 if args.gathered else mirror.shape[1], page_size=ps, hq=hq, hkv=hkv, head_dim=d,
-                             scale=cfg.scale, causal=1, out=out.data_ptr(), out_dtype=_lib.PKV_F32,
+                             scale=cfg.scale, causal=1, out=out.data_ptr(),
+                             out_dtype=_lib.PKV_F32 if args.out == "f32" else _lib.PKV_BF16,
                              plan=dplan.data_ptr(), n_items=plan.shape[0])
         sp = _stream(dev)
         if os.environ.get("PF_DEBUG"):
