@@ -59,6 +59,7 @@ namespace pkv {
 // [start, plan loaded, item k consumer start..., chunks done, published, end].
 __device__ unsigned long long g_trace[1024 * 64];
 __device__ volatile int g_trace_on;
+__device__ unsigned long long g_trace_sm[256];  // SM id per traced CTA (read after the timeline)
 
 namespace {
 
@@ -326,6 +327,11 @@ __device__ __forceinline__ void decode_tc_body(const TcParams& p, const ClusterI
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const bool trace_on = g_trace_on != 0;
   trace(0);
+  if (trace_on && threadIdx.x == 0 && blockIdx.x < 256) {  // SM of this CTA
+    uint32_t smid;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+    g_trace_sm[blockIdx.x] = smid;
+  }
   // ---------------- plan (host-computed; staged into shared memory) ---------
   PlanView pv;
   if (ci) {
@@ -1289,6 +1295,8 @@ int debug_trace(int enable, uint64_t* out, int64_t n) {
   if (out && n > 0) {
     const int64_t m = n < 1024 * kTraceSlots ? n : 1024 * kTraceSlots;
     cudaMemcpyFromSymbol(out, g_trace, m * sizeof(unsigned long long));
+    if (n >= 1024 * kTraceSlots + 256)  // the SM ids follow the timeline
+      cudaMemcpyFromSymbol(out + 1024 * kTraceSlots, g_trace_sm, 256 * sizeof(unsigned long long));
   }
   cudaError_t e = cudaGetLastError();
   return e == cudaSuccess ? PKV_OK : fail(PKV_CUDA_ERROR, "debug trace: %s", pkv::cuda_err_str(e));
