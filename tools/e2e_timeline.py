@@ -72,3 +72,35 @@ labels = {1: "input H2D issued", 2: "slot event", 3: "allocator+plan", 7: "stage
           8: "decode launched", 9: "output D2H issued", 10: "next plan speculated"}
 for j, lab in labels.items():
     print("  native stamp %2d %-26s median %6.1f us after entry" % (j, lab, np.median(nat[:, j + 1])))
+
+# calibration: the same measurement on a tiny decode (1 sequence x 64 keys):
+# its "last CTA end -> sync returns" is the wake-up floor plus the clock
+# offset, which cancels in the difference with the C2 step above
+pool2, store2, cfg2 = bench.build_cache([64], hq, hkv, d, ps, extra_tokens=200, device=dev)
+b2 = DecodeBatch(store2, [0], cfg2)
+q2 = torch.zeros((1, hq, d), dtype=torch.bfloat16).pin_memory()
+k2 = torch.zeros((1, hkv, d), dtype=torch.bfloat16).pin_memory()
+o2 = torch.empty((1, hq, d), dtype=torch.float32).pin_memory()
+for _ in range(5):
+    b2.step(q2, k2, k2, out=o2)
+torch.cuda.synchronize()
+cal = []
+for i in range(12):
+    torch.cuda.synchronize()
+    lib.pkv_debug_trace(1, None, 0)
+    t0 = time.time_ns()
+    b2.step(q2, k2, k2, out=o2)
+    stream.synchronize()
+    t2 = time.time_ns()
+    buf = (C.c_uint64 * n)()
+    lib.pkv_debug_trace(-1, buf, n)
+    lib.pkv_debug_trace(0, None, 0)
+    t = np.array(buf, dtype=np.float64).reshape(256, 8, 32)
+    ks = t[:, :, 0][t[:, :, 0] > 0].min()
+    ke = t[:, :, 31][t[:, :, 31] > 0].max()
+    cal.append(((ks - t0) / 1e3, (ke - ks) / 1e3, (t2 - ke) / 1e3, (t2 - t0) / 1e3))
+cal = np.array(cal)
+pre_d = np.median(r[:, 0]) - np.median(cal[:, 0])
+post_d = np.median(r[:, 2]) - np.median(cal[:, 2])
+print("tiny decode: wall %.1f us, span %.1f us" % (np.median(cal[:, 3]), np.median(cal[:, 1])))
+print("C2 minus tiny: call->first CTA %+.1f us, last CTA->sync %+.1f us" % (pre_d, post_d))
