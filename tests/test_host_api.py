@@ -93,3 +93,19 @@ def test_attention_config_defaults_and_validation():
     for bad in (dict(page_size=48), dict(scale=-1.0), dict(kv_head_count=3)):
         with pytest.raises(ValueError):
             AttentionConfig(head_count=8, head_dim=64, **bad)
+
+
+def test_mask_meta_constructors_seal_their_query_arrays():
+    """self_attention / decode / suffix build fresh query arrays and mark them
+    read-only (the identity key of paged_attention's repeat-call path); a
+    directly constructed meta keeps the caller's arrays as they are, and the
+    view's lengths stay writeable (the reference suite corrupts them)."""
+    view = BatchView.from_lengths([5, 3])
+    for meta in (MaskMeta.self_attention(view), MaskMeta.decode(view), MaskMeta.suffix(view, [2, 1])):
+        assert not meta.q_seq.flags.writeable and not meta.q_pos.flags.writeable
+        with pytest.raises(ValueError):
+            meta.q_pos[0] = 0
+    q_seq, q_pos = np.array([0, 1]), np.array([4, 2])
+    loose = MaskMeta(view=view, q_seq=q_seq, q_pos=q_pos)
+    assert loose.q_seq.flags.writeable and loose.q_pos.flags.writeable
+    assert view.lengths.flags.writeable
