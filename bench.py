@@ -434,6 +434,8 @@ class DecodeBench:
             batch.step(q, k, v, out=out_host)
             stream.synchronize()
             dt = time.perf_counter() - t0
+            if os.environ.get("PKV_E2E_STEP_TIMES"):  # diagnostic: per-step wall times
+                print(f"e2e step {i}: {dt * 1e6:.1f} us", file=sys.stderr)
             if i >= W:
                 times.append(dt)
                 launches += batch.last_launches

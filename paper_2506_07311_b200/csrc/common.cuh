@@ -32,16 +32,24 @@ inline const char* cuda_err_str(cudaError_t e) {
 // device is current (a store on cuda:1 driven from a thread whose current
 // device is cuda:0).  The legacy null stream has no device of its own and
 // keeps the current one.  Restores the caller's device on exit.
+// Load every kernel of the library on the current device once (CUDA's lazy
+// module loading would otherwise load a kernel at its first launch — ~10 ms
+// in the middle of a serving loop the first time a step needs, say, the
+// cluster-mode decode variant).  Cheap after the first call: one flag test.
+void preload_kernels();
+
 struct DeviceGuard {
   int prev = -1;
   explicit DeviceGuard(cudaStream_t s) {
-    if (!s) return;
-    int dev = 0, cur = 0;
-    if (cudaStreamGetDevice(s, &dev) != cudaSuccess || cudaGetDevice(&cur) != cudaSuccess) {
-      cudaGetLastError();
-      return;
+    if (s) {
+      int dev = 0, cur = 0;
+      if (cudaStreamGetDevice(s, &dev) != cudaSuccess || cudaGetDevice(&cur) != cudaSuccess) {
+        cudaGetLastError();
+      } else if (dev != cur && cudaSetDevice(dev) == cudaSuccess) {
+        prev = cur;
+      }
     }
-    if (dev != cur && cudaSetDevice(dev) == cudaSuccess) prev = cur;
+    preload_kernels();
   }
   ~DeviceGuard() {
     if (prev >= 0) cudaSetDevice(prev);

@@ -391,6 +391,12 @@ __device__ __forceinline__ void decode_tc_body(const TcParams& p, const ClusterI
   // cluster mode: announce that this CTA runs (its shared memory may receive
   // peer stores once every CTA has arrived; waited on before the first push)
   if (pv.cluster > 1) cluster_arrive_relaxed();
+  // Launched with programmatic stream serialization: everything above reads
+  // only the plan / launch parameters (uploaded before the preceding kernel
+  // started); the block table, the pages and the queries may still be being
+  // written by that kernel (the step's page-clear / mirror aux kernel), so
+  // wait for its completion here.  A no-op without a programmatic predecessor.
+  asm volatile("griddepcontrol.wait;" ::: "memory");
   trace(1);
   float* s_mo = reinterpret_cast<float*>(smem + p.merge_offset);  // [W][4][D]
   float* s_ml = s_mo + kWarpsTc * kMergeRows * D;                 // [W][4][2]
@@ -826,6 +832,16 @@ TcFn pick_rows(bool splitq, bool rows16) {
   return rows16 ? decode_tc_kernel<T, D, false, true> : decode_tc_kernel<T, D, false, false>;
 }
 
+template <typename T, int D>
+void touch_tc_kernels() {
+  cudaFuncAttributes fa;
+  for (int sq = 0; sq < 2; ++sq)
+    for (int r16 = 0; r16 < 2; ++r16) {
+      cudaFuncGetAttributes(&fa, reinterpret_cast<const void*>(pick_rows<T, D>(sq, r16)));
+      cudaFuncGetAttributes(&fa, reinterpret_cast<const void*>(pick_rows_cluster<T, D>(sq, r16)));
+    }
+}
+
 }  // namespace
 
 bool decode_tc_supported(int kv_dtype, int head_dim) {
@@ -1185,8 +1201,27 @@ int plan_decode(const int32_t* nk, const int32_t* row, int64_t nq, int page_size
 }
 
 
+// Programmatic dependent launch of the decode kernel behind the step's aux
+// kernel (which triggers at its start): the decode prologue (plan staging,
+// launch latency) overlaps the page clears / mirror update.  PKV_DECODE_PDL=0
+// turns it off (A/B switch).
+static bool pdl_on() {
+  static const bool on = [] {
+    const char* e = std::getenv("PKV_DECODE_PDL");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
 static_assert(sizeof(TcParams) + sizeof(ClusterInline) + 16 <= sizeof(RecordedOp::args),
               "graph recorder argument buffer too small");
+void preload_decode_tc_kernels() {
+  touch_tc_kernels<__nv_bfloat16, 64>();
+  touch_tc_kernels<__nv_bfloat16, 128>();
+  touch_tc_kernels<__half, 64>();
+  touch_tc_kernels<__half, 128>();
+}
+
 int launch_decode_tc(TcParams p, const int32_t* plan_host, int kv_dtype, int head_dim, int num_sms,
                      cudaStream_t stream) {
   const bool splitq = p.q_dtype == PKV_F32;
@@ -1258,13 +1293,15 @@ int launch_decode_tc(TcParams p, const int32_t* plan_host, int kv_dtype, int hea
     cfg.blockDim = dim3(kThreadsTc);
     cfg.dynamicSmemBytes = static_cast<size_t>(smem);
     cfg.stream = stream;
-    cudaLaunchAttribute attr[1];
+    cudaLaunchAttribute attr[2];
     attr[0].id = cudaLaunchAttributeClusterDimension;
     attr[0].val.clusterDim.x = static_cast<unsigned>(cluster);
     attr[0].val.clusterDim.y = 1;
     attr[0].val.clusterDim.z = 1;
+    attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[1].val.programmaticStreamSerializationAllowed = pdl_on() ? 1 : 0;
     cfg.attrs = attr;
-    cfg.numAttrs = 1;
+    cfg.numAttrs = 2;
     static const bool debug_cluster = std::getenv("PKV_DEBUG_CLUSTER") != nullptr;
     if (debug_cluster) {
       int n = -1;
@@ -1274,8 +1311,17 @@ int launch_decode_tc(TcParams p, const int32_t* plan_host, int kv_dtype, int hea
     }
     e = inline_plan ? cudaLaunchKernelEx(&cfg, fnc, p, ci) : cudaLaunchKernelEx(&cfg, fn, p);
   } else {
-    fn<<<grid, kThreadsTc, smem, stream>>>(p);
-    e = cudaGetLastError();
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(static_cast<unsigned>(grid));
+    cfg.blockDim = dim3(kThreadsTc);
+    cfg.dynamicSmemBytes = static_cast<size_t>(smem);
+    cfg.stream = stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = pdl_on() ? 1 : 0;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    e = cudaLaunchKernelEx(&cfg, fn, p);
   }
   if (e != cudaSuccess)
     return fail(PKV_CUDA_ERROR, "decode_tc launch: %s (grid %d cluster %d smem %d nq %d key %d)",

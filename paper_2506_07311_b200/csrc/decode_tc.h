@@ -50,6 +50,9 @@ bool decode_tc_supported(int kv_dtype, int head_dim);
 int64_t decode_plan_ints(int64_t nq, int hq);
 int plan_decode(const int32_t* nk, const int32_t* row, int64_t nq, int page_size, int hq, int hkv, int head_dim,
                 int num_sms, int waves, int32_t* out, int64_t cap, int64_t* n_out);
+// cudaFuncGetAttributes on every decode_tc instance (forces lazy loading)
+void preload_decode_tc_kernels();
+void preload_prefill_kernels();  // prefill_sm100.cu
 int launch_decode_tc(TcParams p, const int32_t* plan_host, int kv_dtype, int head_dim, int num_sms,
                      cudaStream_t stream);
 int decode_tc_warps();

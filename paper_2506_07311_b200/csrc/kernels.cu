@@ -27,6 +27,8 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <atomic>
+#include <mutex>
 #include <chrono>
 #include <vector>
 #include <cstdint>
@@ -90,6 +92,9 @@ __global__ void step_aux_kernel(const uint64_t* __restrict__ caches, int n_store
                                 const int32_t* __restrict__ triples, int64_t n_copy,
                                 int32_t* __restrict__ mirror, const int32_t* __restrict__ pairs,
                                 int64_t n_pairs, int64_t row_bytes, int page_size) {
+  // the decode launch behind this kernel may start its prologue now (PDL;
+  // it waits for this grid's completion before touching pages or the table)
+  asm volatile("griddepcontrol.launch_dependents;");
   const int64_t pb = row_bytes * page_size;
   const int64_t per_store = n_zero + n_copy;
   for (int64_t w = blockIdx.x; w < per_store * n_stores; w += gridDim.x) {
@@ -663,6 +668,14 @@ DecodeFn pick_r(int r, int dp) {
 }
 template <typename T, int DP, int R>
 int stage_bytes_of() { return Geo<T, DP, R>::STAGE; }
+
+template <typename T>
+void touch_k2_kernels() {
+  cudaFuncAttributes fa;
+  for (int r : {1, 2, 4})
+    for (int dp : {4, 8, 16, 32, 64, 128, 256})
+      if (DecodeFn f = pick_r<T>(r, dp)) cudaFuncGetAttributes(&fa, reinterpret_cast<const void*>(f));
+}
 
 int ring_bytes(int dtype, int dp) {
   const int s = elem_bytes(dtype);
@@ -1424,3 +1437,38 @@ extern "C" int pkv_attention_plan(const int32_t* q_nkeys, const int32_t* q_row, 
 extern "C" int pkv_debug_trace(int32_t enable, uint64_t* out, int64_t n) {
   return pkv::debug_trace(enable, out, n);
 }
+
+namespace pkv {
+void preload_kernels() {
+  static std::atomic<uint64_t> done{0};  // one bit per device ordinal (< 64)
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) {
+    cudaGetLastError();
+    return;
+  }
+  const uint64_t bit = uint64_t(1) << dev;
+  if (done.load(std::memory_order_acquire) & bit) return;
+  static std::mutex mu;
+  std::lock_guard<std::mutex> lock(mu);
+  if (done.load(std::memory_order_relaxed) & bit) return;
+  cudaFuncAttributes fa;
+  auto touch = [&](const void* f) { cudaFuncGetAttributes(&fa, f); };
+  touch(reinterpret_cast<const void*>(mirror_apply_kernel));
+  touch(reinterpret_cast<const void*>(page_zero_kernel));
+  touch(reinterpret_cast<const void*>(page_copy_kernel));
+  touch(reinterpret_cast<const void*>(step_aux_kernel));
+  touch(reinterpret_cast<const void*>(kv_append_kernel<true>));
+  touch(reinterpret_cast<const void*>(kv_append_kernel<false>));
+  touch(reinterpret_cast<const void*>(kv_gather_kernel));
+  touch(reinterpret_cast<const void*>(append_decode_kernel));
+  touch(reinterpret_cast<const void*>(plan_kernel));
+  touch(reinterpret_cast<const void*>(combine_kernel));
+  touch_k2_kernels<float>();
+  touch_k2_kernels<__nv_bfloat16>();
+  touch_k2_kernels<__half>();
+  preload_decode_tc_kernels();
+  preload_prefill_kernels();
+  cudaGetLastError();  // a query failure only means that kernel loads lazily
+  done.fetch_or(bit, std::memory_order_release);
+}
+}  // namespace pkv

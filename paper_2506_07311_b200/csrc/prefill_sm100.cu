@@ -827,6 +827,14 @@ int launch(const pkv_prefill_args* a, const PrefillParams& pp, cudaStream_t stre
 int query_tile(int hq, int hkv) { return kM / (hq / hkv); }
 
 }  // namespace
+
+void preload_prefill_kernels() {
+  cudaFuncAttributes fa;
+  cudaFuncGetAttributes(&fa, reinterpret_cast<const void*>(prefill_tc_kernel<__nv_bfloat16, 64>));
+  cudaFuncGetAttributes(&fa, reinterpret_cast<const void*>(prefill_tc_kernel<__nv_bfloat16, 128>));
+  cudaFuncGetAttributes(&fa, reinterpret_cast<const void*>(prefill_tc_kernel<__half, 64>));
+  cudaFuncGetAttributes(&fa, reinterpret_cast<const void*>(prefill_tc_kernel<__half, 128>));
+}
 }  // namespace pkv
 
 using namespace pkv;

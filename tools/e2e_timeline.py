@@ -20,8 +20,13 @@ from paper_2506_07311_b200.workloads import CONFIG_SHAPES, config_lengths  # noq
 
 dev = torch.device("cuda:0")
 torch.cuda.set_device(dev)
-lengths = config_lengths("c2")
-hq, hkv, d, ps, _ = CONFIG_SHAPES["c2"]
+if os.environ.get("C3"):  # C3 point: "B:CTX"
+    b3, ctx3 = (int(x) for x in os.environ["C3"].split(":"))
+    lengths = [ctx3] * b3
+    hq, hkv, d, ps, _ = CONFIG_SHAPES["c3"]
+else:
+    lengths = config_lengths("c2")
+    hq, hkv, d, ps, _ = CONFIG_SHAPES["c2"]
 pool, store, cfg = bench.build_cache(lengths, hq, hkv, d, ps, extra_tokens=200, device=dev)
 B = len(lengths)
 batch = DecodeBatch(store, list(range(B)), cfg)
